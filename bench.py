@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""bench.py -- GLA layer (core op) forward+backward throughput at the paper's 1.3B shapes on B200.
+
+Metric (BASELINE.json): "GLA layer fwd+bwd tokens/s at 1.3B shapes, T=2K-16K; % of bf16 tensor peak".
+One step = gla_chunk_fwd + gla_chunk_bwd over one synthetic batch (all four parts of the method).
+Default workload (N=1): BASELINE.json configs[2] -- B=16, H=4, T=2048, per-head K=256, V=512 (d_model 2048,
+d_k = d/2, d_v = d), chunk 64, sub-chunk 16, bf16 q/k/v/d_out, fp32 log alpha = logsigmoid(z)/16.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config 1p3b|340m|long4k|...]
+
+Multi-GPU (torchrun): batch x head sharding with no communication on the data path ("scaling": "weak":
+every rank runs the full per-GPU workload on its own seed); time = max over ranks (all_reduce MAX).
+--impl reference: the fp64 CPU oracle (the only reference that exists for this paper), timed on the host
+cores on a bounded sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+CONFIGS = {
+    # name: (B, H, T, K, V)
+    "1p3b": (16, 4, 2048, 256, 512),
+    "340m": (8, 4, 2048, 128, 256),
+    "long4k": (8, 4, 4096, 256, 512),
+    "long8k": (4, 4, 8192, 256, 512),
+    "long16k": (2, 4, 16384, 256, 512),
+    "tiny": (1, 1, 64, 16, 32),
+}
+METRIC = "GLA layer fwd+bwd tokens/s at 1.3B shapes, T=2K-16K; % of bf16 tensor peak"
+L2_BYTES = 126 * 2**20
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ---- algorithmic work ------------------------------------------------------
+def flops_per_token_head(K, V, C, c):
+    fwd = 4 * K * V + (C + 1) * K + (C + c) * V
+    bwd = 8 * K * V + 2 * (C + 1) * K + 2 * (C + c) * V
+    return fwd, bwd
+
+
+def kernel_algo(name, B, H, T, K, V, C, c, g_bytes=4, e=2):
+    """(algorithmic HBM bytes per launch, algorithmic FLOPs per launch) for one kernel launch.
+    Bytes = unique inputs read once + outputs written once (no re-reads, no recompute)."""
+    u = B * H * T          # token-heads per launch
+    BH = B * H
+    fwd_f, bwd_f = flops_per_token_head(K, V, C, c)
+    table = {
+        # fused forward: q, k, v, g in; o out
+        "tc::fwd": (u * (2 * e * K + e * V + g_bytes * K + e * V), u * fwd_f),
+        "simt::k_fwd_state": (u * (2 * e * K + e * V + g_bytes * K + e * V + 4 * C), u * 4 * K * V + u * (C + 1) * V),
+        "simt::k_intra_P": (u * (2 * e * K + g_bytes * K + 4 * C), u * (C + 1) * K),
+        "simt::k_intra_dP": (u * (2 * e * V + 4 * C), u * (C + 1) * V),
+        # dq kernel: q?, k, v, g, dO, dP in; dq (+fp32 copy) out
+        "simt::k_bwd_dq": (u * (e * K + e * V + g_bytes * K + e * V + 4 * C + e * K + 4 * K), u * 4 * K * V),
+        "simt::k_bwd_dk": (u * (2 * e * K + e * V + g_bytes * K + e * V + 4 * C + 4 * K + e * K + 4 * K),
+                           u * 4 * K * V),
+        "simt::k_bwd_dv": (u * (2 * e * K + g_bytes * K + e * V + 4 * C + e * V), u * 4 * K * V),
+        "tc::bwd": (u * (2 * e * K + e * V + g_bytes * K + e * V + 2 * e * K + e * V + 4 * K), u * bwd_f),
+    }
+    for key, val in table.items():
+        if name.endswith(key) or name == key:
+            return val
+    return None
+
+
+# ---- clocks sampler -------------------------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = str(gpu_index)
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8 and parts[0] == self.idx:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---- CPU oracle baseline -------------------------------------------------------------------------------------
+def cpu_oracle_sample(cfg, seed=0, n_slices=None, T_sample=None):
+    """Time the fp64 oracle fwd+bwd on a bounded sample of (b,h) slices of the workload on the host cores."""
+    import oracle
+    import synth
+    B, H, T, K, V = cfg
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    n = n_slices or max(1, min(cores, 16))
+    Ts = T_sample or T
+    p = synth.problem(1, n, Ts, K, V, seed=seed)
+    f = {k: v.double().numpy() for k, v in p.items()}
+    t0 = time.perf_counter()
+    oracle.fwd(f["q"], f["k"], f["v"], f["g"], nthreads=n)
+    oracle.bwd(f["q"], f["k"], f["v"], f["g"], f["do"], nthreads=n)
+    dt = time.perf_counter() - t0
+    tokens = n * Ts / H          # a token of the layer = H head-slices
+    return {"value": tokens / dt, "unit": "tokens/s", "cores": min(n, cores), "kind": "oracle",
+            "sample": f"{n} (b,h) slices x T={Ts} of B={B},H={H},T={T},K={K},V={V} fwd+bwd in fp64 "
+                      f"({dt:.2f} s; tokens = slices*T/H)", "seconds": dt}
+
+
+# ---- main ---------------------------------------------------------------------------------------------------
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="1p3b")
+    ap.add_argument("--path", choices=["auto", "simt", "tc"], default="auto")
+    ap.add_argument("--chunk", type=int, default=64)
+    ap.add_argument("--subchunk", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def config_dict(args, cfg, n):
+    B, H, T, K, V = cfg
+    return {"workload": f"GLA core fwd+bwd, BASELINE.json configs[2] shapes ({args.config})", "model": "gla-1.3b-layer"
+            if args.config == "1p3b" else f"gla-{args.config}", "global_batch": B * n, "per_gpu_batch": B, "heads": H,
+            "seq_len": T, "d_k_head": K, "d_v_head": V, "chunk": args.chunk, "subchunk": args.subchunk,
+            "parallelism": f"bh-shard x{n} (no data-path collective)", "gates": "logsigmoid(N(0,1))/16 fp32",
+            "l2": "inputs > L2 (no flush)" if input_bytes(cfg) > 2 * L2_BYTES else "L2 flushed between steps"}
+
+
+def input_bytes(cfg):
+    B, H, T, K, V = cfg
+    return B * H * T * (2 * K * 2 + 2 * V * 2 + 4 * K)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    B, H, T, K, V = cfg
+    vals = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_oracle_sample(cfg, seed=i, n_slices=None, T_sample=T)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            base = r
+    v = statistics.mean(vals)
+    ms = (B * T) / v * 1e3
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args, cfg, 1),
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": base["cores"], "kind": "oracle",
+                             "sample": base["sample"]},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import synth
+    from paper_2312_06635_b200 import binding as G
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = CONFIGS[args.config]
+    B, H, T, K, V = cfg
+    C, c = args.chunk, args.subchunk
+    p = synth.problem(B, H, T, K, V, seed=1000 * rank + 1)
+    q, k, v, g, do = (p[n].to(dev) for n in ("q", "k", "v", "g", "do"))
+    path = G.resolve_path(q, v, g, C, c, args.path)
+    wf = G.fwd_workspace(q, v, g, C, c, args.path)
+    wb = G.bwd_workspace(q, v, g, C, c, args.path)
+    o = torch.empty((B, H, T, V), dtype=q.dtype, device=dev)
+    grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v),
+             torch.empty(q.shape, dtype=torch.float32, device=dev), None)
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if input_bytes(cfg) <= 2 * L2_BYTES \
+        else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        G.chunk_fwd(q, k, v, g, C, c, None, False, args.path, out=o, workspace=wf)
+        G.chunk_bwd(q, k, v, g, do, C, c, None, None, False, args.path, grads=grads, workspace=wb)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    G.profile(True)
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    G.lib().gla_profile_enable(0)
+    prof = G.profile_read()
+    launches = G.lib().gla_profile_count()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([total_ms], device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    tokens = B * T * world
+    value = tokens / (ms_step / 1e3)
+
+    # e2e through the public API with pinned host buffers (H2D of the inputs, D2H of every result, each step)
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv, hg, hdo = (x.cpu().pin_memory() for x in (q, k, v, g, do))
+        ho = torch.empty(o.shape, dtype=o.dtype).pin_memory()
+        hgr = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in grads[:4]]
+        n_e2e = max(1, min(args.steps, 5))
+        h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hg, hdo))
+        d2h = ho.numel() * ho.element_size() + sum(x.numel() * x.element_size() for x in hgr)
+        dq_, dk_, dv_, dg_ = (torch.empty_like(x) for x in grads[:4])
+        dd = [torch.empty_like(x) for x in (q, k, v, g, do)]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(n_e2e):
+            for dst, src in zip(dd, (hq, hk, hv, hg, hdo)):
+                dst.copy_(src, non_blocking=True)
+            G.chunk_fwd(dd[0], dd[1], dd[2], dd[3], C, c, None, False, args.path, out=o, workspace=wf)
+            G.chunk_bwd(dd[0], dd[1], dd[2], dd[3], dd[4], C, c, None, None, False, args.path,
+                        grads=(dq_, dk_, dv_, dg_, None), workspace=wb)
+            ho.copy_(o, non_blocking=True)
+            for dst, src in zip(hgr, (dq_, dk_, dv_, dg_)):
+                dst.copy_(src, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([e0.elapsed_time(e1) / n_e2e], device=dev)
+        if dist:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": tokens / (float(et.item()) / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": float(et.item())}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    hbm, tf_burst, tf_sus, peak_src = load_peaks()
+    roof = None
+    if prof:
+        top = max(prof, key=lambda n: prof[n][0])
+        tot, nl = prof[top]
+        per_launch_s = tot / nl / 1e3
+        algo = kernel_algo(top, B, H, T, K, V, C, c)
+        if algo:
+            by, fl = algo
+            roof = {"kernel": top, "bound": "hbm", "achieved": by / per_launch_s / 1e9, "peak": hbm, "unit": "GB/s",
+                    "frac": by / per_launch_s / 1e9 / hbm, "traffic": None, "peak_source": peak_src,
+                    "algo_bytes_per_launch": by, "algo_flops_per_launch": fl,
+                    "tensor_tflops": fl / per_launch_s / 1e12,
+                    "share_of_step": tot / total_ms if total_ms else None, "ms_per_launch": per_launch_s * 1e3}
+    fwd_f, bwd_f = flops_per_token_head(K, V, C, c)
+    layer_tflops = B * H * T * (fwd_f + bwd_f) / (ms_step / 1e3) / 1e12
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16" if q.dtype == torch.bfloat16 else "f32", "data": "synthetic",
+            "config": config_dict(args, cfg, world), "path": path,
+            "algorithmic_tflops": layer_tflops, "frac_of_bf16_peak": layer_tflops * 1e12 / (tf_burst * 1e12),
+            "roofline": roof, "kernels": {n: {"ms_total": v_[0], "launches": v_[1]} for n, v_ in prof.items()},
+            "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = {k_: v_ for k_, v_ in cpu_oracle_sample(cfg, T_sample=T).items()
+                                if k_ != "seconds"}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,262 @@
+"""Thin Python binding over libgla.so (include/gla.h).  Argument marshalling only: every step of the
+method runs in the library's CUDA kernels.  torch provides device memory and the current stream.
+
+There is no CPU fallback: if libgla.so is missing or the tensors are not on a CUDA device, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgla.so")
+
+BF16, FP32 = 0, 1
+PATHS = {"auto": 0, "simt": 1, "tc": 2}
+_STATUS = {0: "ok", 1: "shape", 2: "plan", 3: "dtype", 4: "align", 5: "null", 6: "unsupported", 7: "cuda",
+           8: "workspace"}
+
+
+class GLAError(RuntimeError):
+    def __init__(self, fn: str, status: int, lib):
+        self.status = status
+        msg = lib.gla_status_string(status).decode()
+        if status == 7:
+            msg += f" (cudaError {lib.gla_last_cuda_error()})"
+        super().__init__(f"{fn}: {msg} [status {status}]")
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in
+                ("B", "H", "T", "K", "V", "chunk", "subchunk", "qkv_dtype", "gate_dtype", "path")]
+
+
+_lib = None
+
+
+def lib():
+    """Load libgla.so (raises if it has not been built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libgla.so not built ({LIB_PATH}); run `python -c 'import __graft_entry__ as g; "
+                               f"g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, sz, ip = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+        dp = ctypes.POINTER(_Desc)
+        L.gla_fwd_workspace_size.argtypes = [dp]
+        L.gla_fwd_workspace_size.restype = sz
+        L.gla_bwd_workspace_size.argtypes = [dp]
+        L.gla_bwd_workspace_size.restype = sz
+        L.gla_chunk_fwd.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        L.gla_chunk_bwd.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        L.gla_recurrent_step.argtypes = [ip, ip, ip, ip, ip, ip, vp, vp, vp, vp, vp, vp, vp]
+        L.gla_state_summary.argtypes = [dp, vp, vp, vp, vp, vp, vp, sz, vp]
+        L.gla_dstate_summary.argtypes = [dp, vp, vp, vp, vp, vp, sz, vp]
+        L.gla_state_combine.argtypes = [ip, ip, ip, vp, vp, vp, vp, vp]
+        L.gla_status_string.argtypes = [ip]
+        L.gla_status_string.restype = ctypes.c_char_p
+        L.gla_resolve_path.argtypes = [dp]
+        L.gla_profile_enable.argtypes = [ip]
+        L.gla_profile_enable.restype = None
+        L.gla_profile_reset.restype = None
+        L.gla_profile_count.restype = ip
+        L.gla_profile_get.argtypes = [ip, ctypes.c_char_p, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ip)]
+        L.gla_profile_get.restype = ip
+        for f in (L.gla_chunk_fwd, L.gla_chunk_bwd, L.gla_recurrent_step, L.gla_state_summary,
+                  L.gla_dstate_summary, L.gla_state_combine, L.gla_last_cuda_error, L.gla_version,
+                  L.gla_resolve_path):
+            f.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+EXPORTS = ("gla_fwd_workspace_size", "gla_bwd_workspace_size", "gla_chunk_fwd", "gla_chunk_bwd",
+           "gla_recurrent_step", "gla_state_summary", "gla_dstate_summary", "gla_state_combine",
+           "gla_status_string", "gla_last_cuda_error", "gla_resolve_path", "gla_version", "gla_profile_enable",
+           "gla_profile_reset", "gla_profile_count", "gla_profile_get")
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return BF16
+    if t.dtype == torch.float32:
+        return FP32
+    raise TypeError(f"unsupported dtype {t.dtype} (bf16 or fp32)")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _check(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise RuntimeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise RuntimeError(f"{name} must be contiguous")
+
+
+def _stream(dev):
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def desc(q, v, log_alpha, chunk, subchunk, path) -> _Desc:
+    B, H, T, K = q.shape
+    return _Desc(B, H, T, K, v.shape[-1], chunk, subchunk, _dt(q), _dt(log_alpha), PATHS[path])
+
+
+def resolve_path(q, v, log_alpha, chunk=64, subchunk=16, path="auto") -> str:
+    r = lib().gla_resolve_path(ctypes.byref(desc(q, v, log_alpha, chunk, subchunk, path)))
+    return {1: "simt", 2: "tc"}.get(r, f"error{r}")
+
+
+def _call(fn, name, *args):
+    s = fn(*args)
+    if s != 0:
+        raise GLAError(name, s, lib())
+
+
+def fwd_workspace(q, v, log_alpha, chunk=64, subchunk=16, path="auto") -> torch.Tensor:
+    n = lib().gla_fwd_workspace_size(ctypes.byref(desc(q, v, log_alpha, chunk, subchunk, path)))
+    return torch.empty(max(n, 16), dtype=torch.uint8, device=q.device)
+
+
+def bwd_workspace(q, v, log_alpha, chunk=64, subchunk=16, path="auto") -> torch.Tensor:
+    n = lib().gla_bwd_workspace_size(ctypes.byref(desc(q, v, log_alpha, chunk, subchunk, path)))
+    return torch.empty(max(n, 16), dtype=torch.uint8, device=q.device)
+
+
+def chunk_fwd(q, k, v, log_alpha, chunk: int = 64, subchunk: int = 16, initial_state=None,
+              output_final_state: bool = False, path: str = "auto", out=None, final_state=None, workspace=None):
+    """o [B,H,T,V] (q's dtype) and final_state [B,H,K,V] fp32 (or None).  gla_chunk_fwd."""
+    for t, n in ((q, "q"), (k, "k"), (v, "v"), (log_alpha, "log_alpha")):
+        _check(t, n)
+    B, H, T, K = q.shape
+    V = v.shape[-1]
+    d = desc(q, v, log_alpha, chunk, subchunk, path)
+    if out is None:
+        out = torch.empty((B, H, T, V), dtype=q.dtype, device=q.device)
+    if output_final_state and final_state is None:
+        final_state = torch.empty((B, H, K, V), dtype=torch.float32, device=q.device)
+    if workspace is None:
+        workspace = fwd_workspace(q, v, log_alpha, chunk, subchunk, path)
+    _call(lib().gla_chunk_fwd, "gla_chunk_fwd", ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(log_alpha),
+          _ptr(initial_state), _ptr(out), _ptr(final_state), _ptr(workspace), workspace.numel(),
+          _stream(q.device))
+    return out, final_state
+
+
+def chunk_bwd(q, k, v, log_alpha, d_out, chunk: int = 64, subchunk: int = 16, initial_state=None,
+              d_final_state=None, need_d_initial_state: bool = False, path: str = "auto", grads=None,
+              workspace=None):
+    """(dq, dk, dv, d_log_alpha fp32, d_initial_state fp32 or None).  gla_chunk_bwd."""
+    for t, n in ((q, "q"), (k, "k"), (v, "v"), (log_alpha, "log_alpha"), (d_out, "d_out")):
+        _check(t, n)
+    B, H, T, K = q.shape
+    d = desc(q, v, log_alpha, chunk, subchunk, path)
+    if grads is None:
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        dg = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+        dh0 = torch.empty((B, H, K, v.shape[-1]), dtype=torch.float32, device=q.device) \
+            if need_d_initial_state else None
+    else:
+        dq, dk, dv, dg, dh0 = grads
+    if workspace is None:
+        workspace = bwd_workspace(q, v, log_alpha, chunk, subchunk, path)
+    _call(lib().gla_chunk_bwd, "gla_chunk_bwd", ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(log_alpha),
+          _ptr(initial_state), _ptr(d_out), _ptr(d_final_state), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dg),
+          _ptr(dh0), _ptr(workspace), workspace.numel(), _stream(q.device))
+    return dq, dk, dv, dg, dh0
+
+
+def recurrent_step(q_t, k_t, v_t, log_alpha_t, state, out=None):
+    """One decode step; ``state`` [B,H,K,V] fp32 is updated in place; returns o_t [B,H,V]."""
+    for t, n in ((q_t, "q_t"), (k_t, "k_t"), (v_t, "v_t"), (log_alpha_t, "log_alpha_t"), (state, "state")):
+        _check(t, n)
+    B, H, K = q_t.shape
+    V = v_t.shape[-1]
+    if out is None:
+        out = torch.empty((B, H, V), dtype=q_t.dtype, device=q_t.device)
+    _call(lib().gla_recurrent_step, "gla_recurrent_step", B, H, K, V, _dt(q_t), _dt(log_alpha_t), _ptr(q_t),
+          _ptr(k_t), _ptr(v_t), _ptr(log_alpha_t), _ptr(state), _ptr(out), _stream(q_t.device))
+    return out
+
+
+def state_summary(k, v, log_alpha, chunk: int = 64, subchunk: int = 16):
+    """(S_loc [B,H,K,V] fp32, log_decay [B,H,K] fp32) of a segment with zero initial state."""
+    B, H, T, K = k.shape
+    V = v.shape[-1]
+    d = desc(k, v, log_alpha, chunk, subchunk, "simt")
+    S = torch.empty((B, H, K, V), dtype=torch.float32, device=k.device)
+    D = torch.empty((B, H, K), dtype=torch.float32, device=k.device)
+    _call(lib().gla_state_summary, "gla_state_summary", ctypes.byref(d), _ptr(k), _ptr(v), _ptr(log_alpha),
+          _ptr(S), _ptr(D), None, 0, _stream(k.device))
+    return S, D
+
+
+def dstate_summary(q, d_out, log_alpha, chunk: int = 64, subchunk: int = 16):
+    """dh0_loc [B,H,K,V] fp32 = d_initial_state of a segment when d_final_state = 0."""
+    B, H, T, K = q.shape
+    V = d_out.shape[-1]
+    d = desc(q, d_out, log_alpha, chunk, subchunk, "simt")
+    out = torch.empty((B, H, K, V), dtype=torch.float32, device=q.device)
+    _call(lib().gla_dstate_summary, "gla_dstate_summary", ctypes.byref(d), _ptr(q), _ptr(d_out),
+          _ptr(log_alpha), _ptr(out), None, 0, _stream(q.device))
+    return out
+
+
+def state_combine(H_in, log_decay, S_loc, out=None):
+    """H_out = diag(e^{log_decay}) H_in + S_loc (per (b,h) unit)."""
+    B, H, K, V = H_in.shape
+    if out is None:
+        out = torch.empty_like(H_in)
+    _call(lib().gla_state_combine, "gla_state_combine", B * H, K, V, _ptr(H_in), _ptr(log_decay), _ptr(S_loc),
+          _ptr(out), _stream(H_in.device))
+    return out
+
+
+class GLAFunction(torch.autograd.Function):
+    """Autograd wrapper: forward gla_chunk_fwd, backward gla_chunk_bwd (recomputes, stores no state)."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, log_alpha, initial_state, chunk, subchunk, path):
+        o, fs = chunk_fwd(q, k, v, log_alpha, chunk, subchunk, initial_state, True, path)
+        ctx.save_for_backward(q, k, v, log_alpha, initial_state)
+        ctx.cfg = (chunk, subchunk, path)
+        return o, fs
+
+    @staticmethod
+    def backward(ctx, do, dfs):
+        q, k, v, g, h0 = ctx.saved_tensors
+        chunk, subchunk, path = ctx.cfg
+        dq, dk, dv, dg, dh0 = chunk_bwd(q, k, v, g, do.contiguous(), chunk, subchunk, h0,
+                                        None if dfs is None else dfs.contiguous(), h0 is not None, path)
+        return dq, dk, dv, dg.to(g.dtype), dh0, None, None, None
+
+
+def gla(q, k, v, log_alpha, initial_state=None, chunk: int = 64, subchunk: int = 16, path: str = "auto"):
+    """Differentiable chunk-wise GLA core: returns (o, final_state)."""
+    return GLAFunction.apply(q, k, v, log_alpha, initial_state, chunk, subchunk, path)
+
+
+def profile(enable: bool = True):
+    """Turn the library's per-launch CUDA-event tracing on/off (resets the record)."""
+    lib().gla_profile_reset()
+    lib().gla_profile_enable(1 if enable else 0)
+
+
+def profile_read():
+    """{kernel name: (total_ms, launches)} for the launches recorded since profile(True)."""
+    cap = 64
+    names = ctypes.create_string_buffer(64 * cap)
+    ms = (ctypes.c_float * cap)()
+    n = (ctypes.c_int * cap)()
+    cnt = lib().gla_profile_get(cap, names, ms, n)
+    out = {}
+    for i in range(min(cnt, cap)):
+        nm = names.raw[64 * i: 64 * i + 64].split(b"\0", 1)[0].decode()
+        out[nm] = (float(ms[i]), int(n[i]))
+    return out

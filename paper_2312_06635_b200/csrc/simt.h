@@ -1,0 +1,39 @@
+// simt.h -- host-side interface of the fp32 SIMT kernels (simt.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace gla {
+
+struct Problem {           // forward / state summary
+    int B, H, T, K, V, C, c, qkv_dtype, gate_dtype;
+    int mode;              // 0 forward, 1 state summary
+    const void *q, *k, *v, *g;
+    const float* h0;
+    void* out;
+    float* final_state;
+    float* log_decay;
+    void* ws;
+};
+
+struct BwdProblem {
+    int B, H, T, K, V, C, c, qkv_dtype, gate_dtype;
+    int mode;              // 0 backward, 1 dstate summary (dh0 only)
+    const void *q, *k, *v, *g, *dO;
+    const float *h0, *dfinal;
+    void *dq, *dk, *dv;
+    float *dg, *dh0;
+    void* ws;
+};
+
+namespace simt {
+cudaError_t fwd(const Problem& p, cudaStream_t st);
+cudaError_t bwd(const BwdProblem& p, cudaStream_t st);
+cudaError_t step(int BH, int K, int V, int qkv_dtype, int gate_dtype, const void* q, const void* k,
+                 const void* v, const void* g, float* state, void* out, cudaStream_t st);
+cudaError_t combine(int BH, int K, int V, const float* Hin, const float* D, const float* S, float* Hout,
+                    cudaStream_t st);
+size_t fwd_ws(int B, int H, int T, int K, int V, int C);
+size_t bwd_ws(int B, int H, int T, int K, int V, int C);
+}  // namespace simt
+}  // namespace gla

@@ -1,0 +1,16 @@
+// tc.h -- host-side interface of the tensor-core (tcgen05/TMEM/TMA, sm_100a) kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "simt.h"
+
+namespace gla {
+namespace tc {
+bool supported(int B, int H, int T, int K, int V, int C, int c, int qkv_dtype, int gate_dtype);
+cudaError_t fwd(const Problem& p, cudaStream_t st);
+cudaError_t bwd(const BwdProblem& p, cudaStream_t st);
+size_t fwd_ws(int B, int H, int T, int K, int V, int C);
+size_t bwd_ws(int B, int H, int T, int K, int V, int C);
+}  // namespace tc
+}  // namespace gla
