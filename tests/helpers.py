@@ -30,7 +30,7 @@ def problem(B, H, T, K, V, seed=0, gate="std", dtype=torch.bfloat16, h0=False, d
 
 
 def cuda(p):
-    return {k: (None if v is None else v.cuda().contiguous()) for k, v in p.items()}
+    return {k: (v.cuda().contiguous() if isinstance(v, torch.Tensor) else v) for k, v in p.items()}
 
 
 def f64(t):
