@@ -9,6 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgla.so")
+PROBE = os.path.join(HERE, "libgla_probe.so")   # tests only: tcgen05/TMA convention probe
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr",
@@ -23,7 +24,7 @@ def stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+    deps = sources() + glob.glob(os.path.join(CSRC, "probe", "*.cu")) + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         [os.path.join(HERE, "..", "include", "gla.h")]
     return any(os.path.getmtime(p) > t for p in deps)
 
@@ -40,6 +41,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write(res.stderr)
     with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
         f.write(res.stderr)
+    probe = [NVCC, *ARCH, *FLAGS, "-o", PROBE, os.path.join(CSRC, "probe", "tc_probe.cu")]
+    res = subprocess.run(probe, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libgla_probe.so")
     return LIB
 
 

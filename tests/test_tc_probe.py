@@ -1,0 +1,32 @@
+"""tcgen05 / UMMA-descriptor / TMA conventions (tc_common.cuh) vs torch.matmul, on one CTA."""
+import ctypes
+import os
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2312_06635_b200",
+                   "libgla_probe.so")
+
+
+@pytest.fixture(scope="module")
+def probe():
+    L = ctypes.CDLL(LIB)
+    L.probe_gemm.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int] * 6
+    return L
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (128, 256, 256), (64, 64, 256), (128, 128, 128), (64, 128, 64)])
+@pytest.mark.parametrize("a_mn,b_mn,tma", [(0, 0, 0), (1, 0, 0), (0, 1, 0), (1, 1, 0), (1, 1, 1), (1, 0, 1)])
+def test_probe_gemm(probe, M, N, K, a_mn, b_mn, tma):
+    torch.manual_seed(0)
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = torch.randn(K, N, device="cuda").bfloat16()
+    At = A.t().contiguous()
+    D = torch.full((M, N), float("nan"), device="cuda")
+    rc = probe.probe_gemm(A.data_ptr(), At.data_ptr(), B.data_ptr(), D.data_ptr(), M, N, K, a_mn, b_mn, tma)
+    assert rc == 0, rc
+    ref = A.float() @ B.float()
+    err = (D - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-5, err
