@@ -1,0 +1,445 @@
+// tc_fwd.cu -- fused chunk-wise GLA forward on sm_100a tensor cores (tcgen05 + TMEM + TMA).
+//
+// One CTA = one (b,h) unit x one 128-wide V tile; it walks the T/64 chunks in order, keeping the state in
+// TMEM for the whole sequence (never in HBM, unlike the paper's materialised chunk states).
+// Per chunk i (C = 64 tokens), PAPER.md P:245-284 with SURVEY App. A.1/A.2 equations:
+//   (1) b = chunk-local inclusive cumsum of log alpha, per channel, from registers
+//   (2) cross-chunk output  O^T  = (H_i e^{r})^T (Q (.) e^{b-r})^T          (first term)
+//       state passing       Y   += V^T (K (.) e^{r-b}) ;  H_{i+1} = e^{Gamma - r} (.) Y
+//   (3) intra-chunk scores  P    = (Q (.) e^{b-r}) (K (.) e^{r-b})^T (.) M   and  O^T += V^T P^T
+// where r = b at the chunk's middle row (a per-channel normaliser, every factor within e^{+-G}).
+// Precision: Q~, K~ are formed in fp32 from log-space differences and split into bf16 hi + lo; P is one
+// M=128 x N=128 tcgen05 MMA of [Q~hi; Q~lo] x [K~hi; K~lo]^T whose four 64x64 blocks sum to Q~ K~^T at
+// ~2^-16 relative precision, so the diagonal sub-chunk blocks get the paper's "full precision"
+// at the same tensor-core cost a diagonal-only correction would have.  O_inter and the state update use
+// the bf16 hi parts with fp32 accumulation (the paper's half-precision matmuls).
+// Guard: if a chunk's half-chunk log decay exceeds G = 60 in any channel, that chunk takes the exact path:
+// P in fp32 log space on CUDA cores (per-element exponent b_t - b_s <= 0), Q~ = q e^{b}, K^ = k e^{Gamma-b}
+// (all factors <= 1) and the state decay applied before the update.
+//
+// Thread roles (256 threads): every thread builds operands for 2 channels x 64/RG rows; all 8 warps run the
+// TMEM passes (warp w -> TMEM lanes 32(w%4).., column half w/4); thread 0 issues TMA and tcgen05.mma.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "prof.h"
+#include "tc.h"
+#include "tc_common.cuh"
+
+namespace gla {
+namespace tc {
+
+constexpr int CH = 64;          // chunk length C
+constexpr int VT = 128;         // V tile per CTA (TMEM lanes)
+constexpr int NTH = 256;
+constexpr float L2E = 1.4426950408889634f;
+constexpr float GUARD = 60.f;   // max half-chunk |log decay| for the factorised fast path
+
+template <int K>
+struct FwdCfg {
+    static constexpr int NPAIR = K / 2;             // channel pairs = threads per row group
+    static constexpr int RG = NTH / NPAIR;          // row groups
+    static constexpr int RPG = CH / RG;             // rows per group
+    static constexpr int KB = K / 64;               // 64-channel blocks
+    static constexpr uint32_t QT_BYTES = KB * 16384;  // [KB][128 rows: hi 0-63, lo 64-127][128 B]
+    static constexpr uint32_t SB_BYTES = KB * 16384;  // [KB][128 rows v][128 B]
+    static constexpr uint32_t OFF_QT = 0;
+    static constexpr uint32_t OFF_KB = OFF_QT + QT_BYTES;
+    static constexpr uint32_t OFF_SB = OFF_KB + QT_BYTES;
+    static constexpr uint32_t OFF_V = OFF_SB + SB_BYTES;       // [2 boxes][64 t][128 B]
+    static constexpr uint32_t OFF_P = OFF_V + 16384;           // [64 t][128 B]
+    static constexpr uint32_t OFF_STG = K >= 128 ? OFF_SB + 16384 : OFF_P + 8192;   // O staging [2][64 t][128 B]
+    static constexpr uint32_t OFF_F = K >= 128 ? OFF_P + 8192 : OFF_STG + 16384;     // fsb, fy, pend, gtot[RG]
+    static constexpr uint32_t SMEM = OFF_F + 4 * (3 * K + RG * K) + 1024;
+    static constexpr uint32_t TCOLS = 512;
+    static constexpr uint32_t COL_S = 0, COL_O = K, COL_P = 2 * K >= 256 ? 384 : 2 * K;  // P needs 128 cols
+};
+
+template <typename TG>
+__device__ __forceinline__ float2 ld_g2(const TG* p);
+template <>
+__device__ __forceinline__ float2 ld_g2<float>(const float* p) {
+    return __ldg(reinterpret_cast<const float2*>(p));
+}
+template <>
+__device__ __forceinline__ float2 ld_g2<__nv_bfloat16>(const __nv_bfloat16* p) {
+    __nv_bfloat162 v = __ldg(reinterpret_cast<const __nv_bfloat162*>(p));
+    return __bfloat1622float2(v);
+}
+
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t u) {
+    __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&u);
+    return __bfloat1622float2(v);
+}
+
+template <int K, typename TG>
+__global__ void __launch_bounds__(NTH, 1)
+k_fwd(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+      const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g,
+      const float* __restrict__ h0, float* __restrict__ final_state, float* __restrict__ ws, int T, int V) {
+    using Cfg = FwdCfg<K>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQT = sm + Cfg::OFF_QT;
+    uint8_t* sKB = sm + Cfg::OFF_KB;
+    uint8_t* sSB = sm + Cfg::OFF_SB;
+    uint8_t* sV = sm + Cfg::OFF_V;
+    uint8_t* sP = sm + Cfg::OFF_P;
+    float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
+    float* fy = fsb + K;
+    float* pend = fy + K;
+    float* gtot = pend + K;    // [RG][K]
+    __shared__ uint64_t bar_v, bar_m1, bar_m2;
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int vtile = blockIdx.x, bh = blockIdx.y;
+    const int v0 = vtile * VT;
+    const int NC = T / CH;
+    const int pj = tid % Cfg::NPAIR, rg = tid / Cfg::NPAIR;
+    const int ch0 = 2 * pj;                       // this thread's channels ch0, ch0+1
+    const int row0 = rg * Cfg::RPG;
+
+    if (warp == 0) tmem_alloc(&tmem_base, Cfg::TCOLS);
+    if (tid == 0) {
+        mbar_init(&bar_v, 1);
+        mbar_init(&bar_m1, 1);
+        mbar_init(&bar_m2, 1);
+        fence_mbar_init();
+        prefetch_tmap(&tmV);
+        prefetch_tmap(&tmO);
+    }
+    for (int m = tid; m < K; m += NTH) pend[m] = 0.f;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tm = tmem_base;
+    const uint32_t tS = tm + Cfg::COL_S, tO = tm + Cfg::COL_O, tP = tm + Cfg::COL_P;
+    const int lq = warp & 3, half = warp >> 2;
+    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
+    const int vrow = 32 * lq + lane;              // v index (TMEM lane) of this thread in TMEM passes
+
+    // ---- initial state Y_0 = h0 (or 0) into TMEM columns [0, K) ----
+    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+        uint32_t r[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            r[j] = __float_as_uint(h0 ? h0[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
+        tmem_st32(tS + lane_base + c0, r);
+    }
+    tmem_wait_st();
+
+    // ---- register prefetch of q, k, g for chunk 0 ----
+    const size_t head_row = (size_t)bh * T;
+    uint32_t qr[Cfg::RPG], kr[Cfg::RPG];
+    float2 gr[Cfg::RPG];
+    auto prefetch = [&](int i) {
+#pragma unroll
+        for (int r = 0; r < Cfg::RPG; ++r) {
+            const size_t off = (head_row + (size_t)i * CH + row0 + r) * K + ch0;
+            qr[r] = __ldg(reinterpret_cast<const uint32_t*>(q + off));
+            kr[r] = __ldg(reinterpret_cast<const uint32_t*>(k + off));
+            gr[r] = ld_g2<TG>(g + off);
+        }
+    };
+    prefetch(0);
+
+    const uint32_t idO = idesc_bf16(128, 64, 0, 0);      // O^T[v][t]: A = SB (K-major), B = Q~hi (K-major)
+    const uint32_t idP = idesc_bf16(128, 128, 0, 0);     // P blocks: A = Q~ hi|lo, B = K~ hi|lo
+    const uint32_t idS = idesc_bf16(128, K, 1, 1);       // Y[v][ch]: A = V^T (MN-major), B = K~hi (MN-major)
+    const uint32_t idPV = idesc_bf16(128, 64, 1, 0);     // O^T += V^T P^T: A = V (MN), B = P (K-major)
+    const uint32_t aQT = smem_u32(sQT), aKB = smem_u32(sKB), aSB = smem_u32(sSB), aV = smem_u32(sV),
+                   aP = smem_u32(sP);
+
+    for (int i = 0; i < NC; ++i) {
+        const uint32_t ph = i & 1;
+        const int trow = (int)(head_row + (size_t)i * CH);
+        if (tid == 0) {   // (TMA) V_i -> smem, two [64 t x 64 v] SW128 boxes
+            mbar_expect_tx(&bar_v, 16384);
+            tma_load_2d(sV, &tmV, &bar_v, v0, trow);
+            tma_load_2d(sV + 8192, &tmV, &bar_v, v0 + 64, trow);
+        }
+        // ---- (1) chunk-local cumsum, own rows ----
+        float2 run = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < Cfg::RPG; ++r) {
+            run.x += gr[r].x;
+            run.y += gr[r].y;
+            gr[r] = run;                      // local inclusive prefix
+        }
+        gtot[rg * K + ch0] = run.x;
+        gtot[rg * K + ch0 + 1] = run.y;
+        __syncthreads();
+        float2 off = make_float2(0.f, 0.f), rr = make_float2(0.f, 0.f), Gm = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r2 = 0; r2 < Cfg::RG; ++r2) {
+            const float a = gtot[r2 * K + ch0], b2 = gtot[r2 * K + ch0 + 1];
+            if (r2 < rg) { off.x += a; off.y += b2; }
+            if ((r2 + 1) * Cfg::RPG <= CH / 2) { rr.x += a; rr.y += b2; }
+            Gm.x += a; Gm.y += b2;
+        }
+        // guard: both half-chunk decays within GUARD for every channel
+        const bool bad_here = (rg == 0) && (-rr.x > GUARD || -rr.y > GUARD || rr.x - Gm.x > GUARD ||
+                                            rr.y - Gm.y > GUARD);
+        const bool slow = __syncthreads_or(bad_here) != 0;
+        // ---- factor exponents: Q~ = q e^{b - rq}, K~ = k e^{rk - b} ----
+        const float2 rq = slow ? make_float2(0.f, 0.f) : rr;
+        const float2 rk = slow ? Gm : rr;
+        if (rg == 0) {   // TMEM-pass factors + pending exponent (one owner per channel)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int m = ch0 + u;
+                const float p = pend[m];
+                const float r_ = u ? rr.y : rr.x, G_ = u ? Gm.y : Gm.x;
+                if (!slow) { fsb[m] = ex2f((p + r_) * L2E); fy[m] = fsb[m]; pend[m] = G_ - r_; }
+                else { fsb[m] = ex2f(p * L2E); fy[m] = ex2f((p + G_) * L2E); pend[m] = 0.f; }
+            }
+        }
+        const int blk = ch0 >> 6, col = ch0 & 63;
+        uint8_t* qbase = sQT + blk * 16384;
+        uint8_t* kbase = sKB + blk * 16384;
+#pragma unroll
+        for (int r = 0; r < Cfg::RPG; ++r) {
+            const int t = row0 + r;
+            const float bx = gr[r].x + off.x, by = gr[r].y + off.y;
+            const float2 qf = bf2_to_f2(qr[r]), kf = bf2_to_f2(kr[r]);
+            const float qx = qf.x * ex2f((bx - rq.x) * L2E), qy = qf.y * ex2f((by - rq.y) * L2E);
+            const float kx = kf.x * ex2f((rk.x - bx) * L2E), ky = kf.y * ex2f((rk.y - by) * L2E);
+            const uint32_t qh = pack_bf16(qx, qy), kh = pack_bf16(kx, ky);
+            const float2 qhf = bf2_to_f2(qh), khf = bf2_to_f2(kh);
+            *reinterpret_cast<uint32_t*>(qbase + sw128_off(t, col)) = qh;
+            *reinterpret_cast<uint32_t*>(qbase + sw128_off(64 + t, col)) = pack_bf16(qx - qhf.x, qy - qhf.y);
+            *reinterpret_cast<uint32_t*>(kbase + sw128_off(t, col)) = kh;
+            *reinterpret_cast<uint32_t*>(kbase + sw128_off(64 + t, col)) = pack_bf16(kx - khf.x, ky - khf.y);
+            if (slow) {   // exact path needs b in fp32
+                float* wb = ws + ((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * CH + t) * K + ch0;
+                *reinterpret_cast<float2*>(wb) = make_float2(bx, by);
+            }
+        }
+        if (i + 1 < NC) prefetch(i + 1);
+        if (tid == 0 && i > 0) tma_store_wait_read();   // O staging (in SB) of chunk i-1 consumed
+        __syncthreads();
+        // ---- TMEM pass: SB = bf16(Y * e^{sb}), Y <- Y * e^{y} ----
+        {
+            uint8_t* sbrow = sSB;
+            for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(tS + lane_base + c0, r);
+                tmem_wait_ld();
+                uint32_t pk[16];
+#pragma unroll
+                for (int j = 0; j < 32; j += 2) {
+                    const float y0 = __uint_as_float(r[j]), y1 = __uint_as_float(r[j + 1]);
+                    pk[j / 2] = pack_bf16(y0 * fsb[c0 + j], y1 * fsb[c0 + j + 1]);
+                    r[j] = __float_as_uint(y0 * fy[c0 + j]);
+                    r[j + 1] = __float_as_uint(y1 * fy[c0 + j + 1]);
+                }
+                tmem_st32(tS + lane_base + c0, r);
+                uint8_t* dst = sbrow + (c0 >> 6) * 16384;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int cc = (c0 & 63) + 8 * u;
+                    *reinterpret_cast<uint4*>(dst + sw128_off(vrow, cc)) =
+                        make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+                }
+            }
+            tmem_wait_st();
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        // ---- (2)+(3) MMAs ----
+        if (tid == 0) {
+            tc_fence_after();
+            mbar_wait(&bar_v, ph);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < K / 16; ++kk) {
+                const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                mma_bf16(tO, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aQT + o, 16, 1024), idO, kk > 0);
+            }
+            if (!slow) {
+#pragma unroll
+                for (int kk = 0; kk < K / 16; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    mma_bf16(tP, sdesc_sw128(aQT + o, 16, 1024), sdesc_sw128(aKB + o, 16, 1024), idP, kk > 0);
+                }
+            }
+#pragma unroll
+            for (int kk = 0; kk < CH / 16; ++kk)
+                mma_bf16(tS, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aKB + kk * 2048, 16384, 1024),
+                         idS, 1);
+            mma_commit(&bar_m1);
+        }
+        mbar_wait(&bar_m1, ph);
+        tc_fence_after();
+        // ---- P epilogue: P (bf16, causal) -> smem [t][s] ----
+        if (!slow) {
+            float* exch = reinterpret_cast<float*>(sSB);   // [64 t][64 s] fp32 (SB is free after the MMAs)
+            if (lq >= 2) {
+                uint32_t a[32], b[32];
+                tmem_ld32(tP + lane_base + 32 * half, a);
+                tmem_ld32(tP + lane_base + 64 + 32 * half, b);
+                tmem_wait_ld();
+                const int t = vrow - 64;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    exch[t * 64 + ((32 * half + j + t) & 63)] = __uint_as_float(a[j]) + __uint_as_float(b[j]);
+            }
+            __syncthreads();
+            if (lq < 2) {
+                uint32_t a[32], b[32];
+                tmem_ld32(tP + lane_base + 32 * half, a);
+                tmem_ld32(tP + lane_base + 64 + 32 * half, b);
+                tmem_wait_ld();
+                const int t = vrow;
+                uint32_t pk[16];
+#pragma unroll
+                for (int j = 0; j < 32; j += 2) {
+                    const int s = 32 * half + j;
+                    float p0 = __uint_as_float(a[j]) + __uint_as_float(b[j]) + exch[t * 64 + ((s + t) & 63)];
+                    float p1 = __uint_as_float(a[j + 1]) + __uint_as_float(b[j + 1]) +
+                               exch[t * 64 + ((s + 1 + t) & 63)];
+                    p0 = s <= t ? p0 : 0.f;
+                    p1 = s + 1 <= t ? p1 : 0.f;
+                    pk[j / 2] = pack_bf16(p0, p1);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    *reinterpret_cast<uint4*>(sP + sw128_off(t, 32 * half + 8 * u)) =
+                        make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+            }
+        } else {
+            // exact path: P[t][s] = sum_m q_tm k_sm e^{b_tm - b_sm}, s <= t, every exponent <= 0
+            const float* wb = ws + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * CH * K;
+            for (int e = tid; e < CH * CH; e += NTH) {
+                const int t = e >> 6, s = e & 63;
+                float a = 0.f;
+                if (s <= t) {
+                    const __nv_bfloat16* qt = q + (head_row + (size_t)i * CH + t) * K;
+                    const __nv_bfloat16* ks = k + (head_row + (size_t)i * CH + s) * K;
+                    for (int m = 0; m < K; ++m)
+                        a += __bfloat162float(qt[m]) * __bfloat162float(ks[m]) *
+                             ex2f((wb[t * K + m] - wb[s * K + m]) * L2E);
+                }
+                *reinterpret_cast<__nv_bfloat16*>(sP + sw128_off(t, s)) = __float2bfloat16_rn(a);
+            }
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < CH / 16; ++kk)
+                mma_bf16(tO, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aP + kk * 32, 16, 1024), idPV, 1);
+            mma_commit(&bar_m2);
+        }
+        mbar_wait(&bar_m2, ph);
+        tc_fence_after();
+        // ---- O epilogue: O^T (TMEM) -> bf16 staging [box][t][64 v] -> TMA store ----
+        {
+            uint8_t* stg = sm + Cfg::OFF_STG;
+            uint32_t r[32];
+            tmem_ld32(tO + lane_base + 32 * half, r);
+            tmem_wait_ld();
+            uint8_t* dst = stg + (vrow >> 6) * 8192 + (vrow & 63) * 2;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                *reinterpret_cast<__nv_bfloat16*>(dst + (32 * half + j) * 128) =
+                    __float2bfloat16_rn(__uint_as_float(r[j]));
+            fence_async_smem();
+            tc_fence_before();
+            __syncthreads();
+            if (tid == 0) {
+                tma_store_2d(&tmO, stg, v0, trow);
+                tma_store_2d(&tmO, stg + 8192, v0 + 64, trow);
+                tma_store_commit();
+            }
+        }
+    }
+    // ---- final state: H_T = Y (.) e^{pend} ----
+    if (final_state) {
+        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tS + lane_base + c0, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                final_state[((size_t)bh * K + c0 + j) * V + v0 + vrow] =
+                    __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E);
+        }
+    }
+    if (tid == 0) tma_store_wait_all();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tm, Cfg::TCOLS);
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encoder() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess)
+            fn = (EncodeFn)p;
+    }
+    return fn;
+}
+
+// 2-D bf16 map over a [rows][cols] row-major tensor with a {64 cols, 64 rows} box.
+cudaError_t make_map_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, bool swizzle) {
+    EncodeFn fn = encoder();
+    if (!fn) return cudaErrorNotSupported;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {64, 64};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int K, typename TG>
+static cudaError_t launch_fwd(const Problem& p, cudaStream_t st) {
+    CUtensorMap mV, mO;
+    const uint64_t rows = (uint64_t)p.B * p.H * p.T;
+    cudaError_t e = make_map_2d(&mV, p.v, rows, p.V, true);
+    if (e != cudaSuccess) return e;
+    e = make_map_2d(&mO, p.out, rows, p.V, false);
+    if (e != cudaSuccess) return e;
+    const uint32_t smem = FwdCfg<K>::SMEM;
+    e = cudaFuncSetAttribute(k_fwd<K, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid(p.V / VT, p.B * p.H);
+    {
+        GLA_PROF("tc::fwd", st);
+        k_fwd<K, TG><<<grid, NTH, smem, st>>>(mV, mO, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k,
+                                              (const TG*)p.g, p.h0, p.final_state, (float*)p.ws, p.T, p.V);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t fwd_tc(const Problem& p, cudaStream_t st) {
+    const bool gf = p.gate_dtype == 1;
+    switch (p.K) {
+        case 64: return gf ? launch_fwd<64, float>(p, st) : launch_fwd<64, __nv_bfloat16>(p, st);
+        case 128: return gf ? launch_fwd<128, float>(p, st) : launch_fwd<128, __nv_bfloat16>(p, st);
+        case 256: return gf ? launch_fwd<256, float>(p, st) : launch_fwd<256, __nv_bfloat16>(p, st);
+        default: return cudaErrorNotSupported;
+    }
+}
+
+size_t fwd_tc_ws(int B, int H, int T, int K, int V) {
+    return sizeof(float) * (size_t)B * H * (V / VT) * CH * K;   // fp32 b of the exact-path chunks
+}
+
+}  // namespace tc
+}  // namespace gla
