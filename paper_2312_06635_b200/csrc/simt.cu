@@ -36,7 +36,8 @@ constexpr int MAXC = 64;
 template <typename TQ, typename TG>
 __global__ void __launch_bounds__(NT) k_intra_P(const TQ* __restrict__ q, const TQ* __restrict__ k,
                                                 const TG* __restrict__ g, float* __restrict__ Pws,
-                                                int T, int K, int C, int c) {
+                                                int T, int K, int C, int c, const int* __restrict__ run_if) {
+    if (run_if && *run_if == 0) return;
     __shared__ float sq[MAXC][KS + 1], sk[MAXC][KS + 1], sb[MAXC][KS + 1];
     const int chunk = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
     const size_t base = ((size_t)bh * T + (size_t)chunk * C) * K;
@@ -91,7 +92,8 @@ __global__ void __launch_bounds__(NT) k_intra_P(const TQ* __restrict__ q, const 
 // dP[t][s] = sum_v dO[t][v] V[s][v] for s <= t.  grid (T/C, BH).
 template <typename TQ>
 __global__ void __launch_bounds__(NT) k_intra_dP(const TQ* __restrict__ dO, const TQ* __restrict__ v,
-                                                 float* __restrict__ dPws, int T, int V, int C) {
+                                                 float* __restrict__ dPws, int T, int V, int C, const int* __restrict__ run_if) {
+    if (run_if && *run_if == 0) return;
     __shared__ float sd[MAXC][KS + 1], sv[MAXC][KS + 1];
     const int chunk = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
     const size_t base = ((size_t)bh * T + (size_t)chunk * C) * V;
@@ -236,7 +238,8 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
                                                const TQ* __restrict__ dO, const float* __restrict__ h0,
                                                const float* __restrict__ dPws, TQ* __restrict__ dq,
                                                float* __restrict__ dq32, float* __restrict__ ST,
-                                               int T, int K, int V, int C) {
+                                               int T, int K, int V, int C, const int* __restrict__ run_if) {
+    if (run_if && *run_if == 0) return;
     extern __shared__ float smem[];
     float* Hs = smem;                          // [KT][V]
     float* sb = Hs + KT_BWD * V;               // [C][KT] b
@@ -333,7 +336,8 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
                                                const float* __restrict__ dPws, const float* __restrict__ dq32,
                                                const float* __restrict__ ST, TQ* __restrict__ dk,
                                                float* __restrict__ dg, float* __restrict__ dh0,
-                                               int T, int K, int V, int C) {
+                                               int T, int K, int V, int C, const int* __restrict__ run_if) {
+    if (run_if && *run_if == 0) return;
     extern __shared__ float smem[];
     float* dH = smem;                          // [KT][V]
     float* sb = dH + KT_BWD * V;               // [C][KT] b
@@ -445,7 +449,8 @@ __global__ void __launch_bounds__(NT) k_bwd_dv(const TQ* __restrict__ q, const T
                                                const TG* __restrict__ g, const TQ* __restrict__ dO,
                                                const float* __restrict__ dfinal, const float* __restrict__ Pws,
                                                TQ* __restrict__ dv, float* __restrict__ dh0,
-                                               int T, int K, int V, int C, int mode) {
+                                               int T, int K, int V, int C, int mode, const int* __restrict__ run_if) {
+    if (run_if && *run_if == 0) return;
     extern __shared__ float smem[];
     float* qe = smem;                          // [C][K] q e^{b}
     float* ke = qe + C * K;                    // [C][K] k e^{Gamma-b}
@@ -582,7 +587,7 @@ static cudaError_t fwd_impl(const Problem& p, cudaStream_t st) {
     if (p.mode == 0) {
         {
             GLA_PROF("simt::k_intra_P", st);
-            k_intra_P<TQ, TG><<<dim3(NC, BH), NT, 0, st>>>(q, k, g, Pws, p.T, p.K, p.C, p.c);
+            k_intra_P<TQ, TG><<<dim3(NC, BH), NT, 0, st>>>(q, k, g, Pws, p.T, p.K, p.C, p.c, nullptr);
         }
     }
     const size_t sm = fwd_state_smem(p.C, p.K);
@@ -614,17 +619,17 @@ static cudaError_t bwd_impl(const BwdProblem& p, cudaStream_t st) {
         {
             GLA_PROF("simt::k_bwd_dv", st);
             k_bwd_dv<TQ, TG><<<dim3(cdiv(p.V, VT_FWD), BH), NT, sm, st>>>(q, k, g, dO, nullptr, nullptr, nullptr,
-                                                                         p.dh0, p.T, p.K, p.V, p.C, 1);
+                                                                         p.dh0, p.T, p.K, p.V, p.C, 1, nullptr);
         }
         return cudaGetLastError();
     }
     {
         GLA_PROF("simt::k_intra_P", st);
-        k_intra_P<TQ, TG><<<dim3(NC, BH), NT, 0, st>>>(q, k, g, Pws, p.T, p.K, p.C, p.c);
+        k_intra_P<TQ, TG><<<dim3(NC, BH), NT, 0, st>>>(q, k, g, Pws, p.T, p.K, p.C, p.c, p.run_if);
     }
     {
         GLA_PROF("simt::k_intra_dP", st);
-        k_intra_dP<TQ><<<dim3(NC, BH), NT, 0, st>>>(dO, v, dPws, p.T, p.V, p.C);
+        k_intra_dP<TQ><<<dim3(NC, BH), NT, 0, st>>>(dO, v, dPws, p.T, p.V, p.C, p.run_if);
     }
     const size_t smk = bwd_k_smem(p.C, p.V);
     cudaError_t e = set_smem(k_bwd_dq<TQ, TG>, smk);
@@ -634,12 +639,12 @@ static cudaError_t bwd_impl(const BwdProblem& p, cudaStream_t st) {
     {
         GLA_PROF("simt::k_bwd_dq", st);
         k_bwd_dq<TQ, TG><<<dim3(cdiv(p.K, KT_BWD), BH), NT, smk, st>>>(q, k, v, g, dO, p.h0, dPws, (TQ*)p.dq, dq32,
-                                                                      ST, p.T, p.K, p.V, p.C);
+                                                                      ST, p.T, p.K, p.V, p.C, p.run_if);
     }
     {
         GLA_PROF("simt::k_bwd_dk", st);
         k_bwd_dk<TQ, TG><<<dim3(cdiv(p.K, KT_BWD), BH), NT, smk, st>>>(q, k, v, g, dO, p.dfinal, dPws, dq32, ST,
-                                                                      (TQ*)p.dk, p.dg, p.dh0, p.T, p.K, p.V, p.C);
+                                                                      (TQ*)p.dk, p.dg, p.dh0, p.T, p.K, p.V, p.C, p.run_if);
     }
     const size_t smv = fwd_state_smem(p.C, p.K);
     e = set_smem(k_bwd_dv<TQ, TG>, smv);
@@ -647,7 +652,7 @@ static cudaError_t bwd_impl(const BwdProblem& p, cudaStream_t st) {
     {
         GLA_PROF("simt::k_bwd_dv", st);
         k_bwd_dv<TQ, TG><<<dim3(cdiv(p.V, VT_FWD), BH), NT, smv, st>>>(q, k, g, dO, p.dfinal, Pws, (TQ*)p.dv,
-                                                                      nullptr, p.T, p.K, p.V, p.C, 0);
+                                                                      nullptr, p.T, p.K, p.V, p.C, 0, p.run_if);
     }
     return cudaGetLastError();
 }

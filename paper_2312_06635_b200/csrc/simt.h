@@ -24,6 +24,7 @@ struct BwdProblem {
     void *dq, *dk, *dv;
     float *dg, *dh0;
     void* ws;
+    const int* run_if;     // device flag: kernels return immediately when *run_if == 0 (nullptr = always run)
 };
 
 namespace simt {

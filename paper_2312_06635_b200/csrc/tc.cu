@@ -6,6 +6,9 @@ namespace tc {
 
 cudaError_t fwd_tc(const Problem& p, cudaStream_t st);
 size_t fwd_tc_ws(int B, int H, int T, int K, int V);
+cudaError_t bwd_tc(const BwdProblem& p, cudaStream_t st);
+size_t bwd_tc_ws(int B, int H, int T, int K, int V, int C);
+bool bwd_tc_supported(int K, int V);
 
 bool supported(int B, int H, int T, int K, int V, int C, int c, int qkv_dtype, int gate_dtype) {
     (void)B; (void)H; (void)T; (void)gate_dtype;
@@ -17,11 +20,16 @@ cudaError_t fwd(const Problem& p, cudaStream_t st) {
     return fwd_tc(p, st);
 }
 
-// Backward: the tcgen05 backward kernels are not in this build yet; the fp32 CUDA-core kernels run it.
-cudaError_t bwd(const BwdProblem& p, cudaStream_t st) { return simt::bwd(p, st); }
+// Backward: tcgen05 kernels for K in {128, 256}; K = 64 (and dstate summaries) run the CUDA-core kernels.
+cudaError_t bwd(const BwdProblem& p, cudaStream_t st) {
+    if (p.mode == 0 && bwd_tc_supported(p.K, p.V)) return bwd_tc(p, st);
+    return simt::bwd(p, st);
+}
 
 size_t fwd_ws(int B, int H, int T, int K, int V, int C) { return fwd_tc_ws(B, H, T, K, V); }
-size_t bwd_ws(int B, int H, int T, int K, int V, int C) { return simt::bwd_ws(B, H, T, K, V, C); }
+size_t bwd_ws(int B, int H, int T, int K, int V, int C) {
+    return bwd_tc_supported(K, V) ? bwd_tc_ws(B, H, T, K, V, C) : simt::bwd_ws(B, H, T, K, V, C);
+}
 
 }  // namespace tc
 }  // namespace gla

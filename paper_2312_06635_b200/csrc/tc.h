@@ -1,5 +1,6 @@
 // tc.h -- host-side interface of the tensor-core (tcgen05/TMEM/TMA, sm_100a) kernels.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 
@@ -12,5 +13,7 @@ cudaError_t fwd(const Problem& p, cudaStream_t st);
 cudaError_t bwd(const BwdProblem& p, cudaStream_t st);
 size_t fwd_ws(int B, int H, int T, int K, int V, int C);
 size_t bwd_ws(int B, int H, int T, int K, int V, int C);
+// 2-D bf16 TMA map over a [rows][cols] row-major tensor, box {64 cols, 64 rows}, optional 128B swizzle.
+cudaError_t make_map_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, bool swizzle);
 }  // namespace tc
 }  // namespace gla

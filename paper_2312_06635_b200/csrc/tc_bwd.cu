@@ -1,0 +1,722 @@
+// tc_bwd.cu -- chunk-wise GLA backward on sm_100a tensor cores (tcgen05 + TMEM + TMA).
+//
+// The paper gives no backward; the equations are DESIGN.md "Backward".
+// Per chunk i with b = chunk-local cumsum, r = b at the middle row, Gamma = b at the last row,
+// Q~ = q e^{b-r}, K~ = k e^{r-b}, E_q = e^{b-r}, E_k = e^{r-b} (per channel), dP = (dO V^T) (.) M:
+//   dq = E_q (.) [ dO (H_i e^r)^T + dP K~ ]                                   (inter + intra)
+//   dk = E_k (.) [ V (e^{Gamma-r} dH_{i+1})^T + dP^T Q~ ]
+//   dv = P^T dO + K~ (e^{Gamma-r} dH_{i+1})        P = (Q~ K~^T) (.) M
+//   dH_i = e^{r} (.) [ e^{Gamma-r} dH_{i+1} + Q~^T dO ]                      (reverse state pass)
+//   d log alpha_t = sum_{s>=t} (q dq - k dk)_s + rowsum(S_T (.) dS_T)
+// The d_k x d_v states are V-tiled (128 value columns per CTA, TMEM-resident), so the contractions over V
+// (dO H^T, V dH^T, dO V^T) are computed per V tile; dq and dk are linear in them, so each CTA emits its
+// per-tile partial (bf16) and k_bwd_reduce sums the V/128 partials in a fixed order (deterministic).
+//   k_bwd_dq  : forward walk, recomputes H in TMEM          -> dq partials, S_T . dS_T partials
+//   k_bwd_dkv : reverse walk, dH in TMEM                    -> dv (final), dk partials, dh0
+//   k_bwd_reduce: per (b,h, 32 channels), reverse over chunks -> dq, dk, d log alpha (carry across chunks)
+// If any chunk's half-chunk log decay exceeds the factorisation guard, k_bwd_dq raises a device flag; the
+// TC kernels that follow then do nothing and the exact fp32 CUDA-core kernels (simt.cu) produce every
+// gradient instead (no host synchronisation).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "prof.h"
+#include "tc.h"
+#include "tc_common.cuh"
+
+namespace gla {
+namespace tc {
+
+namespace {
+constexpr int CH = 64;
+constexpr int VT = 128;
+constexpr int NTH = 256;
+constexpr float L2E = 1.4426950408889634f;
+constexpr float GUARD = 60.f;
+}  // namespace
+
+template <int K>
+struct BwdCfg {
+    static constexpr int NPAIR = K / 2;
+    static constexpr int RG = NTH / NPAIR;
+    static constexpr int RPG = CH / RG;
+    static constexpr int KB = K / 64;
+    static constexpr int NH = K / 128;                 // 128-channel halves (M=128 MMAs over channels)
+    // shared memory (bytes, 1024-aligned blocks)
+    static constexpr uint32_t OP_BYTES = KB * 8192;    // [KB][64 t][128 B] bf16 operand (Q~ or K~, hi only)
+    static constexpr uint32_t SB_BYTES = KB * 16384;   // [KB][128 v][128 B]
+    static constexpr uint32_t OFF_Q = 0;
+    static constexpr uint32_t OFF_K = OFF_Q + OP_BYTES;
+    static constexpr uint32_t OFF_SB = OFF_K + OP_BYTES;
+    static constexpr uint32_t OFF_V = OFF_SB + SB_BYTES;    // [2][64 t][128 B]
+    static constexpr uint32_t OFF_DO = OFF_V + 16384;       // [2][64 t][128 B]
+    static constexpr uint32_t OFF_P = OFF_DO + 16384;       // [64 t][128 B]
+    static constexpr uint32_t OFF_DP = OFF_P + 8192;        // [64 t][128 B]
+    static constexpr uint32_t OFF_STG = OFF_DP + 8192;      // [2][64 s][128 B] dv staging
+    static constexpr uint32_t OFF_F = OFF_STG + 16384;      // fsb[K], fy[K], pend[K], gtot[RG][K], red[4][K]
+    static constexpr uint32_t SMEM = OFF_F + 4 * (3 * K + RG * K + 4 * K) + 1024;
+    // TMEM columns
+    static constexpr uint32_t COL_S = 0, COL_A = K, COL_B = K + 64, COL_C = K + 128;
+};
+
+// ---------------------------------------------------------------------------------------------------------------
+// Shared pieces: the TMEM state pass and the accumulator epilogues.
+template <int K>
+__device__ __forceinline__ void state_pass(uint32_t tS, uint32_t lane_base, int half, int vrow, const float* fsb,
+                                           const float* fy, uint8_t* sSB) {
+    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tS + lane_base + c0, r);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+            const float y0 = __uint_as_float(r[j]), y1 = __uint_as_float(r[j + 1]);
+            pk[j / 2] = pack_bf16(y0 * fsb[c0 + j], y1 * fsb[c0 + j + 1]);
+            r[j] = __float_as_uint(y0 * fy[c0 + j]);
+            r[j + 1] = __float_as_uint(y1 * fy[c0 + j + 1]);
+        }
+        tmem_st32(tS + lane_base + c0, r);
+        uint8_t* dst = sSB + (c0 >> 6) * 16384;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int cc = (c0 & 63) + 8 * u;
+            *reinterpret_cast<uint4*>(dst + sw128_off(vrow, cc)) =
+                make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+    }
+    tmem_wait_st();
+}
+
+// M=64 accumulator [64 t x 64 s] in TMEM -> causal-masked bf16 rows [t][s] (SW128) in smem.
+// M=64 layout: row t lives in TMEM lane 32*(t/16) + t%16 (lanes 0-15 of each quarter; probe-tested).
+__device__ __forceinline__ void m64_epilogue(uint32_t tcol, uint32_t lane_base, int lq, int lane, uint8_t* dst) {
+    uint32_t a[32], b[32];
+    tmem_ld32(tcol + lane_base, a);
+    tmem_ld32(tcol + lane_base + 32, b);
+    tmem_wait_ld();
+    if (lane < 16) {
+        const int t = 16 * lq + lane;
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 64; j += 2) {
+            const float x0 = __uint_as_float(j < 32 ? a[j] : b[j - 32]);
+            const float x1 = __uint_as_float(j + 1 < 32 ? a[j + 1] : b[j + 1 - 32]);
+            pk[j / 2] = pack_bf16(j <= t ? x0 : 0.f, j + 1 <= t ? x1 : 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            *reinterpret_cast<uint4*>(dst + sw128_off(t, 8 * u)) =
+                make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+    }
+}
+
+// [ch x t] accumulator halves (M=128 over channels) -> bf16 partial rows [t][ch] in global memory.
+template <int K>
+__device__ __forceinline__ void partial_epilogue(uint32_t tcol, uint32_t lane_base, int lq, int lane, int warp,
+                                                 __nv_bfloat16* out, size_t row0) {
+    constexpr int NH = K / 128;
+    // work items: (half hh, t-range); 8 warps -> lq quarter of channels, warp/4 -> item
+    for (int item = warp >> 2; item < NH * 2; item += 2) {
+        const int hh = item >> 1, tpart = item & 1;
+        uint32_t r[32];
+        tmem_ld32(tcol + 64 * hh + lane_base + 32 * tpart, r);
+        tmem_wait_ld();
+        const int ch = 128 * hh + 32 * lq + lane;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            out[(row0 + 32 * tpart + j) * K + ch] = __float2bfloat16_rn(__uint_as_float(r[j]));
+    }
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// k_bwd_dq: forward walk.  grid (V/128, BH).
+template <int K, typename TG>
+__global__ void __launch_bounds__(NTH, 1)
+k_bwd_dq(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
+         const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g, const float* __restrict__ h0,
+         const float* __restrict__ dfinal, __nv_bfloat16* __restrict__ dqp, float* __restrict__ stdot,
+         int* __restrict__ flag, int T, int V) {
+    using Cfg = BwdCfg<K>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = sm + Cfg::OFF_K;
+    uint8_t* sSB = sm + Cfg::OFF_SB;
+    uint8_t* sV = sm + Cfg::OFF_V;
+    uint8_t* sD = sm + Cfg::OFF_DO;
+    uint8_t* sdP = sm + Cfg::OFF_DP;
+    float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
+    float* fy = fsb + K;
+    float* pend = fy + K;
+    float* gtot = pend + K;
+    float* red = gtot + Cfg::RG * K;
+    __shared__ uint64_t bar_in, bar_m1, bar_m2;
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int vt = blockIdx.x, bh = blockIdx.y;
+    const int v0 = vt * VT;
+    const int NC = T / CH;
+    const int pj = tid % Cfg::NPAIR, rg = tid / Cfg::NPAIR;
+    const int ch0 = 2 * pj, row0 = rg * Cfg::RPG;
+
+    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    if (tid == 0) {
+        mbar_init(&bar_in, 1);
+        mbar_init(&bar_m1, 1);
+        mbar_init(&bar_m2, 1);
+        fence_mbar_init();
+        prefetch_tmap(&tmV);
+        prefetch_tmap(&tmD);
+    }
+    for (int m = tid; m < K; m += NTH) pend[m] = 0.f;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tm = tmem_base;
+    const uint32_t tS = tm + Cfg::COL_S, tdP = tm + Cfg::COL_A, tdq = tm + Cfg::COL_B;
+    const int lq = warp & 3, half = warp >> 2;
+    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
+    const int vrow = 32 * lq + lane;
+
+    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+        uint32_t r[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            r[j] = __float_as_uint(h0 ? h0[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
+        tmem_st32(tS + lane_base + c0, r);
+    }
+    tmem_wait_st();
+
+    const size_t head_row = (size_t)bh * T;
+    uint32_t kr[Cfg::RPG];
+    float2 gr[Cfg::RPG];
+    auto prefetch = [&](int i) {
+#pragma unroll
+        for (int r = 0; r < Cfg::RPG; ++r) {
+            const size_t off = (head_row + (size_t)i * CH + row0 + r) * K + ch0;
+            kr[r] = __ldg(reinterpret_cast<const uint32_t*>(k + off));
+            gr[r] = ld_g2<TG>(g + off);
+        }
+    };
+    prefetch(0);
+
+    const uint32_t idDP = idesc_bf16(64, 64, 0, 0);      // dP = dO V^T (K-major both, contraction over v)
+    const uint32_t idDQ = idesc_bf16(128, 64, 1, 0);     // dq^T: A = SB (MN-major [ch][v]) / K~ (MN [ch][s])
+    const uint32_t idS = idesc_bf16(128, K, 1, 1);       // Y[v][ch] += V^T K~
+    const uint32_t aK = smem_u32(sK), aSB = smem_u32(sSB), aV = smem_u32(sV), aD = smem_u32(sD),
+                   adP = smem_u32(sdP);
+    bool any_slow = false;
+
+    for (int i = 0; i < NC; ++i) {
+        const uint32_t ph = i & 1;
+        const int trow = (int)(head_row + (size_t)i * CH);
+        if (tid == 0) {
+            mbar_expect_tx(&bar_in, 32768);
+            tma_load_2d(sV, &tmV, &bar_in, v0, trow);
+            tma_load_2d(sV + 8192, &tmV, &bar_in, v0 + 64, trow);
+            tma_load_2d(sD, &tmD, &bar_in, v0, trow);
+            tma_load_2d(sD + 8192, &tmD, &bar_in, v0 + 64, trow);
+        }
+        float2 run = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < Cfg::RPG; ++r) {
+            run.x += gr[r].x;
+            run.y += gr[r].y;
+            gr[r] = run;
+        }
+        gtot[rg * K + ch0] = run.x;
+        gtot[rg * K + ch0 + 1] = run.y;
+        __syncthreads();
+        float2 off = make_float2(0.f, 0.f), rr = make_float2(0.f, 0.f), Gm = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r2 = 0; r2 < Cfg::RG; ++r2) {
+            const float a = gtot[r2 * K + ch0], b2 = gtot[r2 * K + ch0 + 1];
+            if (r2 < rg) { off.x += a; off.y += b2; }
+            if ((r2 + 1) * Cfg::RPG <= CH / 2) { rr.x += a; rr.y += b2; }
+            Gm.x += a; Gm.y += b2;
+        }
+        const bool bad_here = (rg == 0) && (-rr.x > GUARD || -rr.y > GUARD || rr.x - Gm.x > GUARD ||
+                                            rr.y - Gm.y > GUARD);
+        any_slow |= __syncthreads_or(bad_here) != 0;
+        if (rg == 0) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int m = ch0 + u;
+                const float r_ = u ? rr.y : rr.x, G_ = u ? Gm.y : Gm.x;
+                fsb[m] = ex2f((pend[m] + r_) * L2E);
+                fy[m] = fsb[m];
+                pend[m] = G_ - r_;
+            }
+        }
+        uint8_t* kbase = sK + (ch0 >> 6) * 8192;
+        const int col = ch0 & 63;
+#pragma unroll
+        for (int r = 0; r < Cfg::RPG; ++r) {
+            const int t = row0 + r;
+            const float bx = gr[r].x + off.x, by = gr[r].y + off.y;
+            const float2 kf = bf2_to_f2(kr[r]);
+            *reinterpret_cast<uint32_t*>(kbase + sw128_off(t, col)) =
+                pack_bf16(kf.x * ex2f((rr.x - bx) * L2E), kf.y * ex2f((rr.y - by) * L2E));
+        }
+        if (i + 1 < NC) prefetch(i + 1);
+        __syncthreads();
+        state_pass<K>(tS, lane_base, half, vrow, fsb, fy, sSB);   // SB = bf16(H_i e^r); Y <- H_i e^r
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            mbar_wait(&bar_in, ph);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < VT / 16; ++kk) {   // dP_j = dO_j V_j^T over this V tile
+                const uint32_t o = (kk >> 2) * 8192 + (kk & 3) * 32;
+                mma_bf16(tdP, sdesc_sw128(aD + o, 16, 1024), sdesc_sw128(aV + o, 16, 1024), idDP, kk > 0);
+            }
+#pragma unroll
+            for (int hh = 0; hh < Cfg::NH; ++hh)
+#pragma unroll
+                for (int kk = 0; kk < VT / 16; ++kk) {   // dq^T[ch][t] = SB^T dO^T (contraction over v)
+                    const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+                    mma_bf16(tdq + 64 * hh, sdesc_sw128(aSB + 2 * hh * 16384 + kk * 2048, 16384, 1024),
+                             sdesc_sw128(aD + ob, 16, 1024), idDQ, kk > 0);
+                }
+#pragma unroll
+            for (int kk = 0; kk < CH / 16; ++kk)       // Y += V^T K~   (state passing)
+                mma_bf16(tS, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aK + kk * 2048, 8192, 1024),
+                         idS, 1);
+            mma_commit(&bar_m1);
+        }
+        mbar_wait(&bar_m1, ph);
+        tc_fence_after();
+        if (half == 0) m64_epilogue(tdP, lane_base, lq, lane, sdP);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int hh = 0; hh < Cfg::NH; ++hh)
+#pragma unroll
+                for (int kk = 0; kk < CH / 16; ++kk)   // dq^T += K~^T dP^T (contraction over s)
+                    mma_bf16(tdq + 64 * hh, sdesc_sw128(aK + 2 * hh * 8192 + kk * 2048, 8192, 1024),
+                             sdesc_sw128(adP + kk * 32, 16, 1024), idDQ, 1);
+            mma_commit(&bar_m2);
+        }
+        mbar_wait(&bar_m2, ph);
+        tc_fence_after();
+        partial_epilogue<K>(tdq, lane_base, lq, lane, warp, dqp + (size_t)vt * gridDim.y * T * K, head_row + (size_t)i * CH);
+        tc_fence_before();
+        __syncthreads();
+    }
+    if (tid == 0 && any_slow) atomicOr(flag, 1);
+    // S_T . dS_T partial over this V tile: red[lq][ch] = sum over 32 lanes of S_T[ch][v] dfinal[ch][v]
+    if (dfinal) {
+        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tS + lane_base + c0, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                float x = __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E) *
+                          dfinal[((size_t)bh * K + c0 + j) * V + v0 + vrow];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                if (lane == 0) red[lq * K + c0 + j] = x;
+            }
+        }
+        __syncthreads();
+        for (int m = tid; m < K; m += NTH)
+            stdot[((size_t)vt * gridDim.y + bh) * K + m] = red[m] + red[K + m] + red[2 * K + m] + red[3 * K + m];
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tm, 512);
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// k_bwd_dkv: reverse walk.  grid (V/128, BH).
+template <int K, typename TG>
+__global__ void __launch_bounds__(NTH, 1)
+k_bwd_dkv(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
+          const __grid_constant__ CUtensorMap tmDV, const __nv_bfloat16* __restrict__ q,
+          const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g, const float* __restrict__ dfinal,
+          __nv_bfloat16* __restrict__ dkp, float* __restrict__ dh0, const int* __restrict__ flag, int T, int V) {
+    using Cfg = BwdCfg<K>;
+    if (*flag) return;   // exact CUDA-core path takes over
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = sm + Cfg::OFF_Q;
+    uint8_t* sK = sm + Cfg::OFF_K;
+    uint8_t* sSB = sm + Cfg::OFF_SB;
+    uint8_t* sV = sm + Cfg::OFF_V;
+    uint8_t* sD = sm + Cfg::OFF_DO;
+    uint8_t* sP = sm + Cfg::OFF_P;
+    uint8_t* sdP = sm + Cfg::OFF_DP;
+    uint8_t* stg = sm + Cfg::OFF_STG;
+    float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
+    float* fy = fsb + K;
+    float* pend = fy + K;
+    float* gtot = pend + K;
+    __shared__ uint64_t bar_in, bar_m1, bar_m2;
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int vt = blockIdx.x, bh = blockIdx.y;
+    const int v0 = vt * VT;
+    const int NC = T / CH;
+    const int pj = tid % Cfg::NPAIR, rg = tid / Cfg::NPAIR;
+    const int ch0 = 2 * pj, row0 = rg * Cfg::RPG;
+
+    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    if (tid == 0) {
+        mbar_init(&bar_in, 1);
+        mbar_init(&bar_m1, 1);
+        mbar_init(&bar_m2, 1);
+        fence_mbar_init();
+        prefetch_tmap(&tmV);
+        prefetch_tmap(&tmD);
+        prefetch_tmap(&tmDV);
+    }
+    for (int m = tid; m < K; m += NTH) pend[m] = 0.f;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tm = tmem_base;
+    const uint32_t tZ = tm + Cfg::COL_S, tP = tm + Cfg::COL_A, tdP = tm + Cfg::COL_B, tdk = tm + Cfg::COL_A,
+                   tdv = tm + Cfg::COL_C;
+    const int lq = warp & 3, half = warp >> 2;
+    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
+    const int vrow = 32 * lq + lane;
+
+    // Z = dH_T = d_final_state (or 0), pending exponent 0
+    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+        uint32_t r[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            r[j] = __float_as_uint(dfinal ? dfinal[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
+        tmem_st32(tZ + lane_base + c0, r);
+    }
+    tmem_wait_st();
+
+    const size_t head_row = (size_t)bh * T;
+    uint32_t qr[Cfg::RPG], kr[Cfg::RPG];
+    float2 gr[Cfg::RPG];
+    auto prefetch = [&](int i) {
+#pragma unroll
+        for (int r = 0; r < Cfg::RPG; ++r) {
+            const size_t off = (head_row + (size_t)i * CH + row0 + r) * K + ch0;
+            qr[r] = __ldg(reinterpret_cast<const uint32_t*>(q + off));
+            kr[r] = __ldg(reinterpret_cast<const uint32_t*>(k + off));
+            gr[r] = ld_g2<TG>(g + off);
+        }
+    };
+    prefetch(NC - 1);
+
+    const uint32_t idP = idesc_bf16(64, 64, 0, 0);        // P = Q~ K~^T ; dP = dO V^T
+    const uint32_t idZ = idesc_bf16(128, K, 1, 1);        // Z[v][ch] += dO^T Q~
+    const uint32_t idV1 = idesc_bf16(128, 64, 0, 0);      // dv^T[v][s] = dSB K~^T  (A K-major, B K-major)
+    const uint32_t idV2 = idesc_bf16(128, 64, 1, 1);      // dv^T += dO^T P          (A MN, B MN)
+    const uint32_t idK1 = idesc_bf16(128, 64, 1, 0);      // dk^T[ch][s] = dSB^T V^T (A MN, B K-major)
+    const uint32_t idK2 = idesc_bf16(128, 64, 1, 1);      // dk^T += Q~^T dP         (A MN, B MN)
+    const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aSB = smem_u32(sSB), aV = smem_u32(sV), aD = smem_u32(sD),
+                   aP = smem_u32(sP), adP = smem_u32(sdP);
+
+    for (int i = NC - 1; i >= 0; --i) {
+        const uint32_t ph = (NC - 1 - i) & 1;
+        const int trow = (int)(head_row + (size_t)i * CH);
+        if (tid == 0) {
+            mbar_expect_tx(&bar_in, 32768);
+            tma_load_2d(sV, &tmV, &bar_in, v0, trow);
+            tma_load_2d(sV + 8192, &tmV, &bar_in, v0 + 64, trow);
+            tma_load_2d(sD, &tmD, &bar_in, v0, trow);
+            tma_load_2d(sD + 8192, &tmD, &bar_in, v0 + 64, trow);
+        }
+        float2 run = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < Cfg::RPG; ++r) {
+            run.x += gr[r].x;
+            run.y += gr[r].y;
+            gr[r] = run;
+        }
+        gtot[rg * K + ch0] = run.x;
+        gtot[rg * K + ch0 + 1] = run.y;
+        __syncthreads();
+        float2 off = make_float2(0.f, 0.f), rr = make_float2(0.f, 0.f), Gm = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r2 = 0; r2 < Cfg::RG; ++r2) {
+            const float a = gtot[r2 * K + ch0], b2 = gtot[r2 * K + ch0 + 1];
+            if (r2 < rg) { off.x += a; off.y += b2; }
+            if ((r2 + 1) * Cfg::RPG <= CH / 2) { rr.x += a; rr.y += b2; }
+            Gm.x += a; Gm.y += b2;
+        }
+        if (rg == 0) {   // dSB = bf16(dH_{i+1} e^{Gamma - r}); Z <- same; next pending = r
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int m = ch0 + u;
+                const float r_ = u ? rr.y : rr.x, G_ = u ? Gm.y : Gm.x;
+                fsb[m] = ex2f((pend[m] + G_ - r_) * L2E);
+                fy[m] = fsb[m];
+                pend[m] = r_;
+            }
+        }
+        uint8_t* qbase = sQ + (ch0 >> 6) * 8192;
+        uint8_t* kbase = sK + (ch0 >> 6) * 8192;
+        const int col = ch0 & 63;
+#pragma unroll
+        for (int r = 0; r < Cfg::RPG; ++r) {
+            const int t = row0 + r;
+            const float bx = gr[r].x + off.x, by = gr[r].y + off.y;
+            const float2 qf = bf2_to_f2(qr[r]), kf = bf2_to_f2(kr[r]);
+            *reinterpret_cast<uint32_t*>(qbase + sw128_off(t, col)) =
+                pack_bf16(qf.x * ex2f((bx - rr.x) * L2E), qf.y * ex2f((by - rr.y) * L2E));
+            *reinterpret_cast<uint32_t*>(kbase + sw128_off(t, col)) =
+                pack_bf16(kf.x * ex2f((rr.x - bx) * L2E), kf.y * ex2f((rr.y - by) * L2E));
+        }
+        if (i > 0) prefetch(i - 1);
+        if (tid == 0 && i < NC - 1) tma_store_wait_read();   // dv staging of the previous chunk consumed
+        __syncthreads();
+        state_pass<K>(tZ, lane_base, half, vrow, fsb, fy, sSB);   // dSB = bf16(dH~), Z <- dH~
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            mbar_wait(&bar_in, ph);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < K / 16; ++kk) {   // P = Q~ K~^T
+                const uint32_t o = (kk >> 2) * 8192 + (kk & 3) * 32;
+                mma_bf16(tP, sdesc_sw128(aQ + o, 16, 1024), sdesc_sw128(aK + o, 16, 1024), idP, kk > 0);
+            }
+#pragma unroll
+            for (int kk = 0; kk < VT / 16; ++kk) {  // dP_j = dO_j V_j^T
+                const uint32_t o = (kk >> 2) * 8192 + (kk & 3) * 32;
+                mma_bf16(tdP, sdesc_sw128(aD + o, 16, 1024), sdesc_sw128(aV + o, 16, 1024), idP, kk > 0);
+            }
+#pragma unroll
+            for (int kk = 0; kk < K / 16; ++kk) {   // dv^T = dSB K~^T  (inter)
+                const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+                mma_bf16(tdv, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aK + ob, 16, 1024), idV1, kk > 0);
+            }
+#pragma unroll
+            for (int kk = 0; kk < CH / 16; ++kk)      // Z += dO^T Q~   (reverse state pass)
+                mma_bf16(tZ, sdesc_sw128(aD + kk * 2048, 8192, 1024), sdesc_sw128(aQ + kk * 2048, 8192, 1024), idZ,
+                         1);
+            mma_commit(&bar_m1);
+        }
+        mbar_wait(&bar_m1, ph);
+        tc_fence_after();
+        m64_epilogue(half == 0 ? tP : tdP, lane_base, lq, lane, half == 0 ? sP : sdP);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < CH / 16; ++kk)      // dv^T += dO^T P   (intra)
+                mma_bf16(tdv, sdesc_sw128(aD + kk * 2048, 8192, 1024), sdesc_sw128(aP + kk * 2048, 8192, 1024), idV2,
+                         1);
+#pragma unroll
+            for (int hh = 0; hh < Cfg::NH; ++hh) {
+#pragma unroll
+                for (int kk = 0; kk < VT / 16; ++kk) {   // dk^T = dSB^T V^T (inter, contraction over v)
+                    const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+                    mma_bf16(tdk + 64 * hh, sdesc_sw128(aSB + 2 * hh * 16384 + kk * 2048, 16384, 1024),
+                             sdesc_sw128(aV + ob, 16, 1024), idK1, kk > 0);
+                }
+#pragma unroll
+                for (int kk = 0; kk < CH / 16; ++kk)     // dk^T += Q~^T dP  (intra, contraction over t)
+                    mma_bf16(tdk + 64 * hh, sdesc_sw128(aQ + 2 * hh * 8192 + kk * 2048, 8192, 1024),
+                             sdesc_sw128(adP + kk * 2048, 8192, 1024), idK2, 1);
+            }
+            mma_commit(&bar_m2);
+        }
+        mbar_wait(&bar_m2, ph);
+        tc_fence_after();
+        // dv^T [v][s] -> bf16 staging [box][s][64 v] -> TMA store
+        {
+            uint32_t r[32];
+            tmem_ld32(tdv + lane_base + 32 * half, r);
+            tmem_wait_ld();
+            uint8_t* dst = stg + (vrow >> 6) * 8192 + (vrow & 63) * 2;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                *reinterpret_cast<__nv_bfloat16*>(dst + (32 * half + j) * 128) =
+                    __float2bfloat16_rn(__uint_as_float(r[j]));
+        }
+        partial_epilogue<K>(tdk, lane_base, lq, lane, warp, dkp + (size_t)vt * gridDim.y * T * K,
+                            head_row + (size_t)i * CH);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tma_store_2d(&tmDV, stg, v0, trow);
+            tma_store_2d(&tmDV, stg + 8192, v0 + 64, trow);
+            tma_store_commit();
+        }
+    }
+    if (dh0) {   // dH_0 = Z e^{pend}
+        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tZ + lane_base + c0, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                dh0[((size_t)bh * K + c0 + j) * V + v0 + vrow] = __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E);
+        }
+    }
+    if (tid == 0) tma_store_wait_all();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tm, 512);
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// k_bwd_reduce: grid (K/32, BH), 256 threads = 32 channels x 8 row groups of 8 rows.  Reverse over chunks:
+// dq = E_q sum_j dq_j, dk = E_k sum_j dk_j, d log alpha with the carry across chunks.
+template <int K, typename TG>
+__global__ void __launch_bounds__(256) k_bwd_reduce(const __nv_bfloat16* __restrict__ q,
+                                                    const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g,
+                                                    const __nv_bfloat16* __restrict__ dqp,
+                                                    const __nv_bfloat16* __restrict__ dkp,
+                                                    const float* __restrict__ stdot, __nv_bfloat16* __restrict__ dq,
+                                                    __nv_bfloat16* __restrict__ dk, float* __restrict__ dg,
+                                                    const int* __restrict__ flag, int T, int NVT, int BH) {
+    if (*flag) return;
+    __shared__ float tot[8][32], xt[8][32];
+    const int tid = threadIdx.x, c = tid & 31, rgp = tid >> 5;
+    const int m = blockIdx.x * 32 + c, bh = blockIdx.y;
+    const int NC = T / CH;
+    const size_t head_row = (size_t)bh * T;
+    const size_t plane = (size_t)BH * T * K;
+    float carry = 0.f;
+    if (stdot)
+        for (int j = 0; j < NVT; ++j) carry += stdot[((size_t)j * BH + bh) * K + m];
+    for (int i = NC - 1; i >= 0; --i) {
+        float bl[8];
+        float run = 0.f;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const size_t ix = (head_row + (size_t)i * CH + rgp * 8 + r) * K + m;
+            run += to_f(g[ix]);
+            bl[r] = run;
+        }
+        tot[rgp][c] = run;
+        __syncthreads();
+        float off = 0.f, rr = 0.f;
+#pragma unroll
+        for (int r2 = 0; r2 < 8; ++r2) {
+            if (r2 < rgp) off += tot[r2][c];
+            if (r2 < 4) rr += tot[r2][c];
+        }
+        float x[8];
+        float xs = 0.f;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const size_t ix = (head_row + (size_t)i * CH + rgp * 8 + r) * K + m;
+            float sq = 0.f, sk = 0.f;
+            for (int j = 0; j < NVT; ++j) {
+                sq += __bfloat162float(dqp[j * plane + ix]);
+                sk += __bfloat162float(dkp[j * plane + ix]);
+            }
+            const float b = bl[r] + off;
+            const float dqv = sq * ex2f((b - rr) * L2E), dkv = sk * ex2f((rr - b) * L2E);
+            dq[ix] = __float2bfloat16_rn(dqv);
+            dk[ix] = __float2bfloat16_rn(dkv);
+            x[r] = __bfloat162float(q[ix]) * dqv - __bfloat162float(k[ix]) * dkv;
+            xs += x[r];
+        }
+        xt[rgp][c] = xs;
+        __syncthreads();
+        float later = 0.f, ctot = 0.f;
+#pragma unroll
+        for (int r2 = 0; r2 < 8; ++r2) {
+            if (r2 > rgp) later += xt[r2][c];
+            ctot += xt[r2][c];
+        }
+        float acc = carry + later;
+#pragma unroll
+        for (int r = 7; r >= 0; --r) {
+            acc += x[r];
+            dg[(head_row + (size_t)i * CH + rgp * 8 + r) * K + m] = acc;
+        }
+        carry += ctot;
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+bool bwd_tc_supported(int K, int V) { return (K == 128 || K == 256) && V % 128 == 0; }
+
+size_t bwd_tc_ws(int B, int H, int T, int K, int V, int C) {
+    const size_t BH = (size_t)B * H, NVT = V / VT;
+    size_t bytes = 256;                                         // flag
+    bytes += 2 * NVT * BH * T * K * sizeof(__nv_bfloat16);       // dq, dk partials
+    bytes += NVT * BH * K * sizeof(float);                       // S_T . dS_T partials
+    bytes = (bytes + 255) & ~size_t(255);
+    return bytes + simt::bwd_ws(B, H, T, K, V, C);              // exact-path fallback scratch
+}
+
+template <int K, typename TG>
+static cudaError_t launch_bwd(const BwdProblem& p, cudaStream_t st) {
+    using Cfg = BwdCfg<K>;
+    const int BH = p.B * p.H, NVT = p.V / VT;
+    uint8_t* ws = (uint8_t*)p.ws;
+    int* flag = (int*)ws;
+    __nv_bfloat16* dqp = (__nv_bfloat16*)(ws + 256);
+    __nv_bfloat16* dkp = dqp + (size_t)NVT * BH * p.T * K;
+    float* stdot = (float*)(dkp + (size_t)NVT * BH * p.T * K);
+    size_t used = 256 + 2 * (size_t)NVT * BH * p.T * K * 2 + (size_t)NVT * BH * K * 4;
+    used = (used + 255) & ~size_t(255);
+    cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    CUtensorMap mV, mD, mDV;
+    const uint64_t rows = (uint64_t)BH * p.T;
+    if ((e = make_map_2d(&mV, p.v, rows, p.V, true)) != cudaSuccess) return e;
+    if ((e = make_map_2d(&mD, p.dO, rows, p.V, true)) != cudaSuccess) return e;
+    if ((e = make_map_2d(&mDV, p.dv, rows, p.V, false)) != cudaSuccess) return e;
+    const uint32_t smem = Cfg::SMEM;
+    if ((e = cudaFuncSetAttribute(k_bwd_dq<K, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_bwd_dkv<K, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+        return e;
+    dim3 grid(NVT, BH);
+    {
+        GLA_PROF("tc::bwd_dq", st);
+        k_bwd_dq<K, TG><<<grid, NTH, smem, st>>>(mV, mD, (const __nv_bfloat16*)p.k, (const TG*)p.g, p.h0, p.dfinal,
+                                                 dqp, p.dfinal ? stdot : nullptr, flag, p.T, p.V);
+    }
+    {
+        GLA_PROF("tc::bwd_dkv", st);
+        k_bwd_dkv<K, TG><<<grid, NTH, smem, st>>>(mV, mD, mDV, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k,
+                                                  (const TG*)p.g, p.dfinal, dkp, p.dh0, flag, p.T, p.V);
+    }
+    {
+        GLA_PROF("tc::bwd_reduce", st);
+        k_bwd_reduce<K, TG><<<dim3(K / 32, BH), 256, 0, st>>>(
+            (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k, (const TG*)p.g, dqp, dkp,
+            p.dfinal ? stdot : nullptr, (__nv_bfloat16*)p.dq, (__nv_bfloat16*)p.dk, p.dg, flag, p.T, NVT, BH);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // exact path: runs only when the guard flag was raised (kernels return immediately otherwise)
+    BwdProblem sp = p;
+    sp.ws = ws + used;
+    sp.run_if = flag;
+    return simt::bwd(sp, st);
+}
+
+cudaError_t bwd_tc(const BwdProblem& p, cudaStream_t st) {
+    const bool gf = p.gate_dtype == 1;
+    switch (p.K) {
+        case 128: return gf ? launch_bwd<128, float>(p, st) : launch_bwd<128, __nv_bfloat16>(p, st);
+        case 256: return gf ? launch_bwd<256, float>(p, st) : launch_bwd<256, __nv_bfloat16>(p, st);
+        default: return cudaErrorNotSupported;
+    }
+}
+
+}  // namespace tc
+}  // namespace gla

@@ -167,5 +167,22 @@ __device__ __forceinline__ float ex2f(float x) {
     return y;
 }
 
+template <typename TG>
+__device__ __forceinline__ float2 ld_g2(const TG* p);
+template <>
+__device__ __forceinline__ float2 ld_g2<float>(const float* p) {
+    return __ldg(reinterpret_cast<const float2*>(p));
+}
+template <>
+__device__ __forceinline__ float2 ld_g2<__nv_bfloat16>(const __nv_bfloat16* p) {
+    __nv_bfloat162 v = __ldg(reinterpret_cast<const __nv_bfloat162*>(p));
+    return __bfloat1622float2(v);
+}
+
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t u) {
+    __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&u);
+    return __bfloat1622float2(v);
+}
+
 }  // namespace tc
 }  // namespace gla

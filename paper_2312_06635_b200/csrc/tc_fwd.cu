@@ -56,23 +56,6 @@ struct FwdCfg {
     static constexpr uint32_t COL_S = 0, COL_O = K, COL_P = 2 * K >= 256 ? 384 : 2 * K;  // P needs 128 cols
 };
 
-template <typename TG>
-__device__ __forceinline__ float2 ld_g2(const TG* p);
-template <>
-__device__ __forceinline__ float2 ld_g2<float>(const float* p) {
-    return __ldg(reinterpret_cast<const float2*>(p));
-}
-template <>
-__device__ __forceinline__ float2 ld_g2<__nv_bfloat16>(const __nv_bfloat16* p) {
-    __nv_bfloat162 v = __ldg(reinterpret_cast<const __nv_bfloat162*>(p));
-    return __bfloat1622float2(v);
-}
-
-__device__ __forceinline__ float2 bf2_to_f2(uint32_t u) {
-    __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&u);
-    return __bfloat1622float2(v);
-}
-
 template <int K, typename TG>
 __global__ void __launch_bounds__(NTH, 1)
 k_fwd(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,

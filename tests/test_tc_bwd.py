@@ -1,0 +1,74 @@
+"""Tensor-core (tcgen05) backward vs the fp64 oracle: several chunks, both supported head shapes, gate
+distributions on the factorised path and on the guard-triggered exact path, h0 / d_final_state, bf16 gates,
+determinism and the full-size configuration (sampled slices)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2312_06635_b200 import binding as G
+from tests.helpers import cuda, nerr_slices, oracle_bwd, problem
+from tests.test_gpu_parity import check_bwd
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+@pytest.mark.parametrize("K,V", [(128, 256), (256, 512), (128, 128)])
+def test_tc_bwd_shapes(K, V):
+    p = problem(2, 2, 320, K, V, seed=K + V, h0=True, dfinal=True)
+    check_bwd(p, 64, 16, "tc", TOL)
+
+
+@pytest.mark.parametrize("gate", synth.GATES)
+def test_tc_bwd_gates(gate):
+    p = problem(1, 2, 256, 128, 256, seed=21, gate=gate, h0=True, dfinal=True)
+    p["gate_kind"] = gate
+    check_bwd(p, 64, 16, "tc", TOL)
+
+
+def test_tc_bwd_no_optional_states():
+    p = problem(2, 2, 192, 256, 256, seed=22)
+    errs = check_bwd(p, 64, 16, "tc", TOL)
+    assert errs["dlog_alpha_strict"] < TOL
+
+
+def test_tc_bwd_bf16_gates():
+    p = problem(1, 2, 128, 128, 128, seed=23)
+    p["g"] = p["g"].bfloat16()
+    check_bwd(p, 64, 16, "tc", TOL)
+
+
+def test_tc_bwd_matches_simt():
+    pc = cuda(problem(2, 2, 256, 128, 256, seed=24, h0=True, dfinal=True))
+    a = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, pc["h0"], pc["dfinal"], True, "tc")
+    b = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, pc["h0"], pc["dfinal"], True, "simt")
+    for x, y in zip(a, b):
+        d = (x.float() - y.float()).abs().max().item() / y.float().abs().max().item()
+        assert d < 2e-2
+
+
+def test_tc_bwd_deterministic():
+    pc = cuda(problem(2, 4, 256, 256, 512, seed=25, dfinal=True))
+    a = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, None, pc["dfinal"], True, "tc")
+    b = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, None, pc["dfinal"], True, "tc")
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+
+
+def test_tc_bwd_full_size_sampled():
+    """BASELINE.json configs[2] in the bench's launch configuration; oracle on 2 sampled (b,h) slices."""
+    B, H, T, K, V = 16, 4, 2048, 256, 512
+    p = synth.problem(B, H, T, K, V, seed=1)
+    pc = {n: t.cuda() for n, t in p.items()}
+    got = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, path="tc")
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    for _ in range(2):
+        b, h = int(rng.integers(B)), int(rng.integers(H))
+        sl = {n: p[n][b:b + 1, h:h + 1].double().numpy() for n in ("q", "k", "v", "g", "do")}
+        ref = oracle.bwd(sl["q"], sl["k"], sl["v"], sl["g"], sl["do"])
+        for name, x, y in zip(("dq", "dk", "dv", "dlog_alpha"), got[:4], ref[:4]):
+            e = nerr_slices(x[b:b + 1, h:h + 1].float().cpu().numpy(), y)
+            assert e < TOL, (name, e)
