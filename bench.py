@@ -19,7 +19,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -60,11 +59,17 @@ def flops_per_token_head(K, V, C, c):
 
 def kernel_algo(name, B, H, T, K, V, C, c, g_bytes=4, e=2):
     """(algorithmic HBM bytes per launch, algorithmic FLOPs per launch) for one kernel launch.
-    Bytes = unique inputs read once + outputs written once (no re-reads, no recompute)."""
+    Bytes = the unique tensors the kernel must read once + write once (DESIGN.md "Roofline accounting");
+    for the V-tiled backward kernels the per-V-tile dq/dk partials they exchange are counted as outputs/inputs.
+    FLOPs = the algorithmic FLOPs of the method assigned to that kernel (recompute excluded)."""
     u = B * H * T          # token-heads per launch
-    BH = B * H
+    nvt = max(1, V // 128)
     fwd_f, bwd_f = flops_per_token_head(K, V, C, c)
     table = {
+        "tc::bwd_dq": (u * (e * K + g_bytes * K + 2 * e * V + nvt * e * K), u * (2 * K * V + (C + 1) * K + C * V)),
+        "tc::bwd_dkv": (u * (2 * e * K + g_bytes * K + 3 * e * V + nvt * e * K),
+                        u * (6 * K * V + (C + 1) * K + (C + c) * V)),
+        "tc::bwd_reduce": (u * (2 * nvt * e * K + 2 * e * K + g_bytes * K + 2 * e * K + 4 * K), 0),
         # fused forward: q, k, v, g in; o out
         "tc::fwd": (u * (2 * e * K + e * V + g_bytes * K + e * V), u * fwd_f),
         "simt::k_fwd_state": (u * (2 * e * K + e * V + g_bytes * K + e * V + 4 * C), u * 4 * K * V + u * (C + 1) * V),
@@ -85,48 +90,47 @@ def kernel_algo(name, B, H, T, K, V, C, c, g_bytes=4, e=2):
 
 # ---- clocks sampler -------------------------------------------------------------------------------------------
 class Clocks:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """Samples SM clock and throttle reasons via NVML every ~2 ms during the timed region (the same fields as
+    the recipe's nvidia-smi clocks line: clocks.sm, clocks.max.sm, hw/sw slowdown, sw_power_cap)."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+               0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, gpu_index):
-        self.idx = str(gpu_index)
-        self.rows = []
-        self.proc = None
+        self.idx = gpu_index
+        self.sm, self.reasons, self.max = [], set(), None
+        self.stop = threading.Event()
+
+    def _run(self):
+        import pynvml as N
+        N.nvmlInit()
+        h = N.nvmlDeviceGetHandleByIndex(self.idx)
+        self.max = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            self.sm.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.reasons |= {n for bit, n in self.REASONS.items() if r & bit}
+            time.sleep(0.002)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml  # noqa: F401
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            time.sleep(0.01)
         except Exception:
-            self.proc = None
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 8 and parts[0] == self.idx:
-                self.rows.append(parts)
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.t:
+            self.t.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+                "samples": len(self.sm)}
 
 
 # ---- CPU oracle baseline -------------------------------------------------------------------------------------
@@ -139,7 +143,7 @@ def cpu_oracle_sample(cfg, seed=0, n_slices=None, T_sample=None):
         cores = len(os.sched_getaffinity(0))
     except Exception:
         cores = os.cpu_count() or 1
-    n = n_slices or max(1, min(cores, 16))
+    n = n_slices or max(1, 2 * min(cores, 32))
     Ts = T_sample or T
     p = synth.problem(1, n, Ts, K, V, seed=seed)
     f = {k: v.double().numpy() for k, v in p.items()}
@@ -157,7 +161,7 @@ def cpu_oracle_sample(cfg, seed=0, n_slices=None, T_sample=None):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="1p3b")

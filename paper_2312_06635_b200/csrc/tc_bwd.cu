@@ -576,81 +576,120 @@ k_bwd_dkv(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUten
 }
 
 // ---------------------------------------------------------------------------------------------------------------
-// k_bwd_reduce: grid (K/32, BH), 256 threads = 32 channels x 8 row groups of 8 rows.  Reverse over chunks:
-// dq = E_q sum_j dq_j, dk = E_k sum_j dk_j, d log alpha with the carry across chunks.
-template <int K, typename TG>
+// k_bwd_reduce: grid (K/64, BH), 256 threads = 64 rows x 4 groups of 16 channels (16-byte vector loads).
+// Reverse over chunks: dq = E_q (.) sum_j dq_j, dk = E_k (.) sum_j dk_j (fixed j order), and
+// d log alpha_t = carry + sum_{s >= t in chunk} (q dq - k dk)_s, the carry summing every later chunk plus
+// rowsum(S_T (.) dS_T).  The next chunk's inputs are prefetched into registers while this one is scanned.
+template <int K, int NVT, typename TG>
 __global__ void __launch_bounds__(256) k_bwd_reduce(const __nv_bfloat16* __restrict__ q,
                                                     const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g,
                                                     const __nv_bfloat16* __restrict__ dqp,
                                                     const __nv_bfloat16* __restrict__ dkp,
                                                     const float* __restrict__ stdot, __nv_bfloat16* __restrict__ dq,
                                                     __nv_bfloat16* __restrict__ dk, float* __restrict__ dg,
-                                                    const int* __restrict__ flag, int T, int NVT, int BH) {
+                                                    const int* __restrict__ flag, int T, int BH) {
     if (*flag) return;
-    __shared__ float tot[8][32], xt[8][32];
-    const int tid = threadIdx.x, c = tid & 31, rgp = tid >> 5;
-    const int m = blockIdx.x * 32 + c, bh = blockIdx.y;
+    __shared__ float sb[64][65];      // g -> b (chunk-local cumsum), then x -> suffix sums
+    __shared__ float carry_s[64];
+    const int tid = threadIdx.x, t = tid >> 2, cg = tid & 3;
+    const int m0 = blockIdx.x * 64, bh = blockIdx.y;
+    const int mc = m0 + 16 * cg;      // this thread's 16 channels [mc, mc+16)
     const int NC = T / CH;
     const size_t head_row = (size_t)bh * T;
     const size_t plane = (size_t)BH * T * K;
-    float carry = 0.f;
-    if (stdot)
-        for (int j = 0; j < NVT; ++j) carry += stdot[((size_t)j * BH + bh) * K + m];
-    for (int i = NC - 1; i >= 0; --i) {
-        float bl[8];
-        float run = 0.f;
+    if (tid < 64) {
+        float c0 = 0.f;
+        if (stdot)
+            for (int j = 0; j < NVT; ++j) c0 += stdot[((size_t)j * BH + bh) * K + m0 + tid];
+        carry_s[tid] = c0;
+    }
+    uint4 pq[NVT][2], pk[NVT][2], qv[2], kv[2];
+    float gv[16];
+    auto load = [&](int i) {
+        const size_t ix = (head_row + (size_t)i * CH + t) * K + mc;
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const size_t ix = (head_row + (size_t)i * CH + rgp * 8 + r) * K + m;
-            run += to_f(g[ix]);
-            bl[r] = run;
-        }
-        tot[rgp][c] = run;
-        __syncthreads();
-        float off = 0.f, rr = 0.f;
+        for (int j = 0; j < NVT; ++j)
 #pragma unroll
-        for (int r2 = 0; r2 < 8; ++r2) {
-            if (r2 < rgp) off += tot[r2][c];
-            if (r2 < 4) rr += tot[r2][c];
-        }
-        float x[8];
-        float xs = 0.f;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const size_t ix = (head_row + (size_t)i * CH + rgp * 8 + r) * K + m;
-            float sq = 0.f, sk = 0.f;
-            for (int j = 0; j < NVT; ++j) {
-                sq += __bfloat162float(dqp[j * plane + ix]);
-                sk += __bfloat162float(dkp[j * plane + ix]);
+            for (int u = 0; u < 2; ++u) {
+                pq[j][u] = __ldg(reinterpret_cast<const uint4*>(dqp + j * plane + ix + 8 * u));
+                pk[j][u] = __ldg(reinterpret_cast<const uint4*>(dkp + j * plane + ix + 8 * u));
             }
-            const float b = bl[r] + off;
-            const float dqv = sq * ex2f((b - rr) * L2E), dkv = sk * ex2f((rr - b) * L2E);
-            dq[ix] = __float2bfloat16_rn(dqv);
-            dk[ix] = __float2bfloat16_rn(dkv);
-            x[r] = __bfloat162float(q[ix]) * dqv - __bfloat162float(k[ix]) * dkv;
-            xs += x[r];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            qv[u] = __ldg(reinterpret_cast<const uint4*>(q + ix + 8 * u));
+            kv[u] = __ldg(reinterpret_cast<const uint4*>(k + ix + 8 * u));
         }
-        xt[rgp][c] = xs;
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) {
+            const float2 x = ld_g2<TG>(g + ix + u);
+            gv[u] = x.x;
+            gv[u + 1] = x.y;
+        }
+    };
+    load(NC - 1);
+    for (int i = NC - 1; i >= 0; --i) {
+        // (a1) chunk-local cumsum: stage g, one thread per channel scans the 64 rows
+#pragma unroll
+        for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = gv[u];
         __syncthreads();
-        float later = 0.f, ctot = 0.f;
-#pragma unroll
-        for (int r2 = 0; r2 < 8; ++r2) {
-            if (r2 > rgp) later += xt[r2][c];
-            ctot += xt[r2][c];
+        if (tid < 64) {
+            float run = 0.f;
+            for (int r = 0; r < CH; ++r) { run += sb[r][tid]; sb[r][tid] = run; }
         }
-        float acc = carry + later;
+        __syncthreads();
+        float x[16], dqv[16], dkv[16];
 #pragma unroll
-        for (int r = 7; r >= 0; --r) {
-            acc += x[r];
-            dg[(head_row + (size_t)i * CH + rgp * 8 + r) * K + m] = acc;
+        for (int u = 0; u < 16; ++u) {
+            const float b = sb[t][16 * cg + u], r = sb[CH / 2 - 1][16 * cg + u];
+            float sq = 0.f, sk = 0.f;
+#pragma unroll
+            for (int j = 0; j < NVT; ++j) {
+                const __nv_bfloat16* a = reinterpret_cast<const __nv_bfloat16*>(&pq[j][u >> 3]);
+                const __nv_bfloat16* c = reinterpret_cast<const __nv_bfloat16*>(&pk[j][u >> 3]);
+                sq += __bfloat162float(a[u & 7]);
+                sk += __bfloat162float(c[u & 7]);
+            }
+            dqv[u] = sq * ex2f((b - r) * L2E);
+            dkv[u] = sk * ex2f((r - b) * L2E);
+            const float qf = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(&qv[u >> 3])[u & 7]);
+            const float kf = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(&kv[u >> 3])[u & 7]);
+            x[u] = qf * dqv[u] - kf * dkv[u];
         }
-        carry += ctot;
+        const size_t ix = (head_row + (size_t)i * CH + t) * K + mc;
+        uint4 oq[2], ok[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            oq[u] = make_uint4(pack_bf16(dqv[8 * u], dqv[8 * u + 1]), pack_bf16(dqv[8 * u + 2], dqv[8 * u + 3]),
+                               pack_bf16(dqv[8 * u + 4], dqv[8 * u + 5]), pack_bf16(dqv[8 * u + 6], dqv[8 * u + 7]));
+            ok[u] = make_uint4(pack_bf16(dkv[8 * u], dkv[8 * u + 1]), pack_bf16(dkv[8 * u + 2], dkv[8 * u + 3]),
+                               pack_bf16(dkv[8 * u + 4], dkv[8 * u + 5]), pack_bf16(dkv[8 * u + 6], dkv[8 * u + 7]));
+            *reinterpret_cast<uint4*>(dq + ix + 8 * u) = oq[u];
+            *reinterpret_cast<uint4*>(dk + ix + 8 * u) = ok[u];
+        }
+        if (i > 0) load(i - 1);
+        __syncthreads();                   // everyone has read b
+#pragma unroll
+        for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = x[u];
+        __syncthreads();
+        if (tid < 64) {                    // reverse cumsum with the carry of all later chunks
+            float run = carry_s[tid];
+            for (int r = CH - 1; r >= 0; --r) { run += sb[r][tid]; sb[r][tid] = run; }
+            carry_s[tid] = run;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 16; u += 4)
+            *reinterpret_cast<float4*>(dg + ix + u) =
+                make_float4(sb[t][16 * cg + u], sb[t][16 * cg + u + 1], sb[t][16 * cg + u + 2], sb[t][16 * cg + u + 3]);
         __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------------------------------------------------------
-bool bwd_tc_supported(int K, int V) { return (K == 128 || K == 256) && V % 128 == 0; }
+bool bwd_tc_supported(int K, int V) {
+    const int nvt = V / 128;
+    return (K == 128 || K == 256) && V % 128 == 0 && (nvt == 1 || nvt == 2 || nvt == 4 || nvt == 8);
+}
 
 size_t bwd_tc_ws(int B, int H, int T, int K, int V, int C) {
     const size_t BH = (size_t)B * H, NVT = V / VT;
@@ -697,9 +736,17 @@ static cudaError_t launch_bwd(const BwdProblem& p, cudaStream_t st) {
     }
     {
         GLA_PROF("tc::bwd_reduce", st);
-        k_bwd_reduce<K, TG><<<dim3(K / 32, BH), 256, 0, st>>>(
-            (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k, (const TG*)p.g, dqp, dkp,
-            p.dfinal ? stdot : nullptr, (__nv_bfloat16*)p.dq, (__nv_bfloat16*)p.dk, p.dg, flag, p.T, NVT, BH);
+        const __nv_bfloat16 *q_ = (const __nv_bfloat16*)p.q, *k_ = (const __nv_bfloat16*)p.k;
+        const float* sd = p.dfinal ? stdot : nullptr;
+        __nv_bfloat16 *dq_ = (__nv_bfloat16*)p.dq, *dk_ = (__nv_bfloat16*)p.dk;
+        const dim3 rg(K / 64, BH);
+        switch (NVT) {
+            case 1: k_bwd_reduce<K, 1, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, flag, p.T, BH); break;
+            case 2: k_bwd_reduce<K, 2, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, flag, p.T, BH); break;
+            case 4: k_bwd_reduce<K, 4, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, flag, p.T, BH); break;
+            case 8: k_bwd_reduce<K, 8, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, flag, p.T, BH); break;
+            default: return cudaErrorNotSupported;
+        }
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // exact path: runs only when the guard flag was raised (kernels return immediately otherwise)
