@@ -20,11 +20,13 @@
 // Thread roles (256 threads): every thread builds operands for 2 channels x 64/RG rows; all 8 warps run the
 // TMEM passes (warp w -> TMEM lanes 32(w%4).., column half w/4); thread 0 issues TMA and tcgen05.mma.
 #include <cuda.h>
+#include <cstdio>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
 #include "prof.h"
 #include "tc.h"
+#include "tc_build.cuh"
 #include "tc_common.cuh"
 
 namespace gla {
@@ -38,9 +40,7 @@ constexpr float GUARD = 60.f;   // max half-chunk |log decay| for the factorised
 
 template <int K>
 struct FwdCfg {
-    static constexpr int NPAIR = K / 2;             // channel pairs = threads per row group
-    static constexpr int RG = NTH / NPAIR;          // row groups
-    static constexpr int RPG = CH / RG;             // rows per group
+    static constexpr int RG = Tile<K>::RG;          // row groups of the operand build (tc_build.cuh)
     static constexpr int KB = K / 64;               // 64-channel blocks
     static constexpr uint32_t QT_BYTES = KB * 16384;  // [KB][128 rows: hi 0-63, lo 64-127][128 B]
     static constexpr uint32_t SB_BYTES = KB * 16384;  // [KB][128 rows v][128 B]
@@ -50,8 +50,10 @@ struct FwdCfg {
     static constexpr uint32_t OFF_V = OFF_SB + SB_BYTES;       // [2 boxes][64 t][128 B]
     static constexpr uint32_t OFF_P = OFF_V + 16384;           // [64 t][128 B]
     static constexpr uint32_t OFF_STG = K >= 128 ? OFF_SB + 16384 : OFF_P + 8192;   // O staging [2][64 t][128 B]
-    static constexpr uint32_t OFF_F = K >= 128 ? OFF_P + 8192 : OFF_STG + 16384;     // fsb, fy, pend, gtot[RG]
-    static constexpr uint32_t SMEM = OFF_F + 4 * (3 * K + RG * K) + 1024;
+    static constexpr uint32_t OFF_F = K >= 128 ? OFF_P + 8192 : OFF_STG + 16384;     // fsb, fy, pend
+    static constexpr uint32_t SMEM = OFF_F + 4 * 3 * K + 1024;
+    static_assert(RG * K * 4 <= 8192, "gtot aliases the 8 KB P buffer");
+    static_assert(SMEM <= 232448, "dynamic shared memory");
     static constexpr uint32_t TCOLS = 512;
     static constexpr uint32_t COL_S = 0, COL_O = K, COL_P = 2 * K >= 256 ? 384 : 2 * K;  // P needs 128 cols
 };
@@ -72,21 +74,22 @@ k_fwd(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorM
     float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
     float* fy = fsb + K;
     float* pend = fy + K;
-    float* gtot = pend + K;    // [RG][K]
-    __shared__ uint64_t bar_v, bar_m1, bar_m2;
+    float* gtot = reinterpret_cast<float*>(sP);   // [RG][K] cumsum exchange; aliases P (free at chunk start)
+    __shared__ uint64_t bar_v, bar_p, bar_m1, bar_m2;
     __shared__ uint32_t tmem_base;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int vtile = blockIdx.x, bh = blockIdx.y;
     const int v0 = vtile * VT;
     const int NC = T / CH;
-    const int pj = tid % Cfg::NPAIR, rg = tid / Cfg::NPAIR;
-    const int ch0 = 2 * pj;                       // this thread's channels ch0, ch0+1
-    const int row0 = rg * Cfg::RPG;
+    const int oc = tid % Tile<K>::NOCT, rg = tid / Tile<K>::NOCT;
+    const int ch0 = 8 * oc;                       // this thread's channels [ch0, ch0 + 8)
+    const int row0 = rg * Tile<K>::RPG;
 
     if (warp == 0) tmem_alloc(&tmem_base, Cfg::TCOLS);
     if (tid == 0) {
         mbar_init(&bar_v, 1);
+        mbar_init(&bar_p, 1);
         mbar_init(&bar_m1, 1);
         mbar_init(&bar_m2, 1);
         fence_mbar_init();
@@ -115,18 +118,8 @@ k_fwd(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorM
 
     // ---- register prefetch of q, k, g for chunk 0 ----
     const size_t head_row = (size_t)bh * T;
-    uint32_t qr[Cfg::RPG], kr[Cfg::RPG];
-    float2 gr[Cfg::RPG];
-    auto prefetch = [&](int i) {
-#pragma unroll
-        for (int r = 0; r < Cfg::RPG; ++r) {
-            const size_t off = (head_row + (size_t)i * CH + row0 + r) * K + ch0;
-            qr[r] = __ldg(reinterpret_cast<const uint32_t*>(q + off));
-            kr[r] = __ldg(reinterpret_cast<const uint32_t*>(k + off));
-            gr[r] = ld_g2<TG>(g + off);
-        }
-    };
-    prefetch(0);
+    ChunkRegs<K> R;
+    load_chunk<K, TG, true, true>(R, q, k, g, head_row, row0, ch0);
 
     const uint32_t idO = idesc_bf16(128, 64, 0, 0);      // O^T[v][t]: A = SB (K-major), B = Q~hi (K-major)
     const uint32_t idP = idesc_bf16(128, 128, 0, 0);     // P blocks: A = Q~ hi|lo, B = K~ hi|lo
@@ -135,6 +128,13 @@ k_fwd(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorM
     const uint32_t aQT = smem_u32(sQT), aKB = smem_u32(sKB), aSB = smem_u32(sSB), aV = smem_u32(sV),
                    aP = smem_u32(sP);
 
+#ifdef GLA_PHASE_TIMING
+    long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tlast = clock64();
+#define PHASE(n) do { long long _t = clock64(); tph[n] += _t - tlast; tlast = _t; } while (0)
+#else
+#define PHASE(n) do {} while (0)
+#endif
     for (int i = 0; i < NC; ++i) {
         const uint32_t ph = i & 1;
         const int trow = (int)(head_row + (size_t)i * CH);
@@ -143,38 +143,31 @@ k_fwd(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorM
             tma_load_2d(sV, &tmV, &bar_v, v0, trow);
             tma_load_2d(sV + 8192, &tmV, &bar_v, v0 + 64, trow);
         }
-        // ---- (1) chunk-local cumsum, own rows ----
-        float2 run = make_float2(0.f, 0.f);
+        // ---- (1) chunk-local cumsum; r = b at row 31, Gamma = b at row 63 ----
+        float2 off[4], rr[4], Gm[4];
+        chunk_cumsum<K>(R, gtot, rg, ch0, off, rr, Gm);
+        bool bad_here = false;
+        if (rg == 0)   // guard: both half-chunk decays within GUARD for every channel
 #pragma unroll
-        for (int r = 0; r < Cfg::RPG; ++r) {
-            run.x += gr[r].x;
-            run.y += gr[r].y;
-            gr[r] = run;                      // local inclusive prefix
-        }
-        gtot[rg * K + ch0] = run.x;
-        gtot[rg * K + ch0 + 1] = run.y;
-        __syncthreads();
-        float2 off = make_float2(0.f, 0.f), rr = make_float2(0.f, 0.f), Gm = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int r2 = 0; r2 < Cfg::RG; ++r2) {
-            const float a = gtot[r2 * K + ch0], b2 = gtot[r2 * K + ch0 + 1];
-            if (r2 < rg) { off.x += a; off.y += b2; }
-            if ((r2 + 1) * Cfg::RPG <= CH / 2) { rr.x += a; rr.y += b2; }
-            Gm.x += a; Gm.y += b2;
-        }
-        // guard: both half-chunk decays within GUARD for every channel
-        const bool bad_here = (rg == 0) && (-rr.x > GUARD || -rr.y > GUARD || rr.x - Gm.x > GUARD ||
-                                            rr.y - Gm.y > GUARD);
+            for (int p = 0; p < 4; ++p)
+                bad_here |= (-rr[p].x > GUARD) | (-rr[p].y > GUARD) | (rr[p].x - Gm[p].x > GUARD) |
+                            (rr[p].y - Gm[p].y > GUARD);
         const bool slow = __syncthreads_or(bad_here) != 0;
-        // ---- factor exponents: Q~ = q e^{b - rq}, K~ = k e^{rk - b} ----
-        const float2 rq = slow ? make_float2(0.f, 0.f) : rr;
-        const float2 rk = slow ? Gm : rr;
+        PHASE(0);
+        // ---- factor references: Q~ = q e^{b - rq}, K~ = k e^{rk - b} ----
+        float2 refq[4], refk[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const float2 rq = slow ? make_float2(0.f, 0.f) : rr[p], rk = slow ? Gm[p] : rr[p];
+            refq[p] = make_float2(-L2E * rq.x, -L2E * rq.y);
+            refk[p] = make_float2(L2E * rk.x, L2E * rk.y);
+        }
         if (rg == 0) {   // TMEM-pass factors + pending exponent (one owner per channel)
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 const int m = ch0 + u;
                 const float p = pend[m];
-                const float r_ = u ? rr.y : rr.x, G_ = u ? Gm.y : Gm.x;
+                const float r_ = (u & 1) ? rr[u >> 1].y : rr[u >> 1].x, G_ = (u & 1) ? Gm[u >> 1].y : Gm[u >> 1].x;
                 if (!slow) { fsb[m] = ex2f((p + r_) * L2E); fy[m] = fsb[m]; pend[m] = G_ - r_; }
                 else { fsb[m] = ex2f(p * L2E); fy[m] = ex2f((p + G_) * L2E); pend[m] = 0.f; }
             }
@@ -183,65 +176,33 @@ k_fwd(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorM
         uint8_t* qbase = sQT + blk * 16384;
         uint8_t* kbase = sKB + blk * 16384;
 #pragma unroll
-        for (int r = 0; r < Cfg::RPG; ++r) {
+        for (int r = 0; r < Tile<K>::RPG; ++r) {
             const int t = row0 + r;
-            const float bx = gr[r].x + off.x, by = gr[r].y + off.y;
-            const float2 qf = bf2_to_f2(qr[r]), kf = bf2_to_f2(kr[r]);
-            const float qx = qf.x * ex2f((bx - rq.x) * L2E), qy = qf.y * ex2f((by - rq.y) * L2E);
-            const float kx = kf.x * ex2f((rk.x - bx) * L2E), ky = kf.y * ex2f((rk.y - by) * L2E);
-            const uint32_t qh = pack_bf16(qx, qy), kh = pack_bf16(kx, ky);
-            const float2 qhf = bf2_to_f2(qh), khf = bf2_to_f2(kh);
-            *reinterpret_cast<uint32_t*>(qbase + sw128_off(t, col)) = qh;
-            *reinterpret_cast<uint32_t*>(qbase + sw128_off(64 + t, col)) = pack_bf16(qx - qhf.x, qy - qhf.y);
-            *reinterpret_cast<uint32_t*>(kbase + sw128_off(t, col)) = kh;
-            *reinterpret_cast<uint32_t*>(kbase + sw128_off(64 + t, col)) = pack_bf16(kx - khf.x, ky - khf.y);
+            float2 b[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) b[p] = add2(R.g[r][p], off[p]);
+            scaled_row(R.q[r], b, refq, 1.f, qbase + sw128_off(t, col), qbase + sw128_off(64 + t, col));
+            scaled_row(R.k[r], b, refk, -1.f, kbase + sw128_off(t, col), kbase + sw128_off(64 + t, col));
             if (slow) {   // exact path needs b in fp32
-                float* wb = ws + ((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * CH + t) * K + ch0;
-                *reinterpret_cast<float2*>(wb) = make_float2(bx, by);
+                float4* wb = reinterpret_cast<float4*>(ws + ((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * CH + t) * K + ch0);
+                wb[0] = make_float4(b[0].x, b[0].y, b[1].x, b[1].y);
+                wb[1] = make_float4(b[2].x, b[2].y, b[3].x, b[3].y);
             }
         }
-        if (i + 1 < NC) prefetch(i + 1);
+        PHASE(1);
+        if (i + 1 < NC) load_chunk<K, TG, true, true>(R, q, k, g, head_row + (size_t)(i + 1) * CH, row0, ch0);
         if (tid == 0 && i > 0) tma_store_wait_read();   // O staging (in SB) of chunk i-1 consumed
         __syncthreads();
+        PHASE(2);
         // ---- TMEM pass: SB = bf16(Y * e^{sb}), Y <- Y * e^{y} ----
-        {
-            uint8_t* sbrow = sSB;
-            for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
-                uint32_t r[32];
-                tmem_ld32(tS + lane_base + c0, r);
-                tmem_wait_ld();
-                uint32_t pk[16];
-#pragma unroll
-                for (int j = 0; j < 32; j += 2) {
-                    const float y0 = __uint_as_float(r[j]), y1 = __uint_as_float(r[j + 1]);
-                    pk[j / 2] = pack_bf16(y0 * fsb[c0 + j], y1 * fsb[c0 + j + 1]);
-                    r[j] = __float_as_uint(y0 * fy[c0 + j]);
-                    r[j + 1] = __float_as_uint(y1 * fy[c0 + j + 1]);
-                }
-                tmem_st32(tS + lane_base + c0, r);
-                uint8_t* dst = sbrow + (c0 >> 6) * 16384;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int cc = (c0 & 63) + 8 * u;
-                    *reinterpret_cast<uint4*>(dst + sw128_off(vrow, cc)) =
-                        make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-                }
-            }
-            tmem_wait_st();
-        }
+        state_pass2<K>(tS, lane_base, half, vrow, fsb, fy, sSB);
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
+        PHASE(3);
         // ---- (2)+(3) MMAs ----
-        if (tid == 0) {
+        if (tid == 0) {   // P first: its epilogue overlaps the O_inter / state MMAs
             tc_fence_after();
-            mbar_wait(&bar_v, ph);
-            tc_fence_after();
-#pragma unroll
-            for (int kk = 0; kk < K / 16; ++kk) {
-                const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                mma_bf16(tO, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aQT + o, 16, 1024), idO, kk > 0);
-            }
             if (!slow) {
 #pragma unroll
                 for (int kk = 0; kk < K / 16; ++kk) {
@@ -249,17 +210,31 @@ k_fwd(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorM
                     mma_bf16(tP, sdesc_sw128(aQT + o, 16, 1024), sdesc_sw128(aKB + o, 16, 1024), idP, kk > 0);
                 }
             }
+            mma_commit(&bar_p);
+#pragma unroll
+            for (int kk = 0; kk < K / 16; ++kk) {
+                const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                mma_bf16(tO, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aQT + o, 16, 1024), idO, kk > 0);
+            }
+            mbar_wait(&bar_v, ph);
+            tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < CH / 16; ++kk)
                 mma_bf16(tS, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aKB + kk * 2048, 16384, 1024),
                          idS, 1);
             mma_commit(&bar_m1);
         }
-        mbar_wait(&bar_m1, ph);
+        mbar_wait(&bar_p, ph);
         tc_fence_after();
+        PHASE(4);
         // ---- P epilogue: P (bf16, causal) -> smem [t][s] ----
         if (!slow) {
-            float* exch = reinterpret_cast<float*>(sSB);   // [64 t][64 s] fp32 (SB is free after the MMAs)
+            // fp32 exchange [64 t][64 s] in the lo rows of Q~ / K~ block 0: only the finished P MMA read them
+            // (the O_inter / state MMAs still in flight read the hi rows, SB and V).
+            auto exch_at = [&](int t, int s) -> float* {
+                uint8_t* base = (t < 32 ? sQT : sKB) + 8192 + (t & 31) * 256;
+                return reinterpret_cast<float*>(base) + ((s + t) & 63);
+            };
             if (lq >= 2) {
                 uint32_t a[32], b[32];
                 tmem_ld32(tP + lane_base + 32 * half, a);
@@ -268,7 +243,7 @@ k_fwd(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorM
                 const int t = vrow - 64;
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
-                    exch[t * 64 + ((32 * half + j + t) & 63)] = __uint_as_float(a[j]) + __uint_as_float(b[j]);
+                    *exch_at(t, 32 * half + j) = __uint_as_float(a[j]) + __uint_as_float(b[j]);
             }
             __syncthreads();
             if (lq < 2) {
@@ -281,9 +256,8 @@ k_fwd(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorM
 #pragma unroll
                 for (int j = 0; j < 32; j += 2) {
                     const int s = 32 * half + j;
-                    float p0 = __uint_as_float(a[j]) + __uint_as_float(b[j]) + exch[t * 64 + ((s + t) & 63)];
-                    float p1 = __uint_as_float(a[j + 1]) + __uint_as_float(b[j + 1]) +
-                               exch[t * 64 + ((s + 1 + t) & 63)];
+                    float p0 = __uint_as_float(a[j]) + __uint_as_float(b[j]) + *exch_at(t, s);
+                    float p1 = __uint_as_float(a[j + 1]) + __uint_as_float(b[j + 1]) + *exch_at(t, s + 1);
                     p0 = s <= t ? p0 : 0.f;
                     p1 = s + 1 <= t ? p1 : 0.f;
                     pk[j / 2] = pack_bf16(p0, p1);
@@ -319,8 +293,11 @@ k_fwd(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorM
                 mma_bf16(tO, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aP + kk * 32, 16, 1024), idPV, 1);
             mma_commit(&bar_m2);
         }
+        PHASE(5);
+        mbar_wait(&bar_m1, ph);
         mbar_wait(&bar_m2, ph);
         tc_fence_after();
+        PHASE(6);
         // ---- O epilogue: O^T (TMEM) -> bf16 staging [box][t][64 v] -> TMA store ----
         {
             uint8_t* stg = sm + Cfg::OFF_STG;
@@ -341,7 +318,13 @@ k_fwd(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorM
                 tma_store_commit();
             }
         }
+        PHASE(7);
     }
+#ifdef GLA_PHASE_TIMING
+    if ((tid == 0 || tid == 255) && blockIdx.x == 0 && blockIdx.y == 0)
+        printf("tid %d phases/chunk: cumsum+guard %lld build %lld prefetch+sync %lld statepass %lld mma1 %lld pepi+issue %lld pv %lld oepi %lld\n", tid,
+               tph[0] / NC, tph[1] / NC, tph[2] / NC, tph[3] / NC, tph[4] / NC, tph[5] / NC, tph[6] / NC, tph[7] / NC);
+#endif
     // ---- final state: H_T = Y (.) e^{pend} ----
     if (final_state) {
         for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
