@@ -145,41 +145,49 @@ __device__ __forceinline__ void scaled_row(const uint4& x, const float2 (&b)[4],
 
 // TMEM state pass over this thread's columns: SB <- bf16(Y * fsb), Y <- Y * fy (fsb, fy per channel, smem).
 // Warp w handles TMEM lanes 32 (w%4) + [0,32) (one v per thread) and column half w/4.
+template <int NL>
+__device__ __forceinline__ void state_pass_cols(uint32_t tS, uint32_t lane_base, int c0, int vrow, const float* fsb,
+                                                const float* fy, uint8_t* sSB) {
+    // NL 32-column TMEM loads in flight (tcgen05.ld is latency-bound, ~150 cycles per x32)
+    uint32_t r[NL][32];
+#pragma unroll
+    for (int h = 0; h < NL; ++h) tmem_ld32(tS + lane_base + c0 + 32 * h, r[h]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int h = 0; h < NL; ++h) {
+        const int cb = c0 + 32 * h;
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+            const float4 fs = *reinterpret_cast<const float4*>(fsb + cb + j);
+            const float4 fyv = *reinterpret_cast<const float4*>(fy + cb + j);
+            const float2 y0 = make_float2(__uint_as_float(r[h][j]), __uint_as_float(r[h][j + 1]));
+            const float2 y1 = make_float2(__uint_as_float(r[h][j + 2]), __uint_as_float(r[h][j + 3]));
+            pk[j / 2] = pack2(mul2(y0, make_float2(fs.x, fs.y)));
+            pk[j / 2 + 1] = pack2(mul2(y1, make_float2(fs.z, fs.w)));
+            const float2 z0 = mul2(y0, make_float2(fyv.x, fyv.y)), z1 = mul2(y1, make_float2(fyv.z, fyv.w));
+            r[h][j] = __float_as_uint(z0.x); r[h][j + 1] = __float_as_uint(z0.y);
+            r[h][j + 2] = __float_as_uint(z1.x); r[h][j + 3] = __float_as_uint(z1.y);
+        }
+        tmem_st32(tS + lane_base + cb, r[h]);
+        uint8_t* dst = sSB + (cb >> 6) * 16384;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int cc = (cb & 63) + 8 * u;
+            *reinterpret_cast<uint4*>(dst + sw128_off(vrow, cc)) =
+                make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+    }
+}
+
+// TMEM state pass over this thread's columns: SB <- bf16(Y * fsb), Y <- Y * fy (fsb, fy per channel, smem).
+// Warp w handles TMEM lanes 32 (w%4) + [0,32) (one v per thread) and column half w/4 (K/2 columns).
 template <int K>
 __device__ __forceinline__ void state_pass2(uint32_t tS, uint32_t lane_base, int half, int vrow, const float* fsb,
                                             const float* fy, uint8_t* sSB) {
-    // two 32-column TMEM loads in flight per step (tcgen05.ld is latency-bound, ~150 cycles per x32)
-    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 64) {
-        uint32_t r[2][32];
-        tmem_ld32(tS + lane_base + c0, r[0]);
-        tmem_ld32(tS + lane_base + c0 + 32, r[1]);
-        tmem_wait_ld();
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int cb = c0 + 32 * h;
-            uint32_t pk[16];
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-                const float4 fs = *reinterpret_cast<const float4*>(fsb + cb + j);
-                const float4 fyv = *reinterpret_cast<const float4*>(fy + cb + j);
-                const float2 y0 = make_float2(__uint_as_float(r[h][j]), __uint_as_float(r[h][j + 1]));
-                const float2 y1 = make_float2(__uint_as_float(r[h][j + 2]), __uint_as_float(r[h][j + 3]));
-                pk[j / 2] = pack2(mul2(y0, make_float2(fs.x, fs.y)));
-                pk[j / 2 + 1] = pack2(mul2(y1, make_float2(fs.z, fs.w)));
-                const float2 z0 = mul2(y0, make_float2(fyv.x, fyv.y)), z1 = mul2(y1, make_float2(fyv.z, fyv.w));
-                r[h][j] = __float_as_uint(z0.x); r[h][j + 1] = __float_as_uint(z0.y);
-                r[h][j + 2] = __float_as_uint(z1.x); r[h][j + 3] = __float_as_uint(z1.y);
-            }
-            tmem_st32(tS + lane_base + cb, r[h]);
-            uint8_t* dst = sSB + (cb >> 6) * 16384;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int cc = (cb & 63) + 8 * u;
-                *reinterpret_cast<uint4*>(dst + sw128_off(vrow, cc)) =
-                    make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-            }
-        }
-    }
+    constexpr int NL = 1;   // two loads in flight spill at 255 registers (measured slower)
+    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32 * NL)
+        state_pass_cols<NL>(tS, lane_base, c0, vrow, fsb, fy, sSB);
     tmem_wait_st();
 }
 
