@@ -147,7 +147,7 @@ __device__ __forceinline__ void scaled_row(const uint4& x, const float2 (&b)[4],
 // Warp w handles TMEM lanes 32 (w%4) + [0,32) (one v per thread) and column half w/4.
 template <int NL>
 __device__ __forceinline__ void state_pass_cols(uint32_t tS, uint32_t lane_base, int c0, int vrow, const float* fsb,
-                                                const float* fy, uint8_t* sSB) {
+                                                const float* fy, uint8_t* sSB, __nv_bfloat16* anch_row) {
     // NL 32-column TMEM loads in flight (tcgen05.ld is latency-bound, ~150 cycles per x32)
     uint32_t r[NL][32];
 #pragma unroll
@@ -174,8 +174,9 @@ __device__ __forceinline__ void state_pass_cols(uint32_t tS, uint32_t lane_base,
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int cc = (cb & 63) + 8 * u;
-            *reinterpret_cast<uint4*>(dst + sw128_off(vrow, cc)) =
-                make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+            const uint4 w = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+            *reinterpret_cast<uint4*>(dst + sw128_off(vrow, cc)) = w;
+            if (anch_row) *reinterpret_cast<uint4*>(anch_row + cb + 8 * u) = w;   // checkpoint copy (bwd anchors)
         }
     }
 }
@@ -184,10 +185,10 @@ __device__ __forceinline__ void state_pass_cols(uint32_t tS, uint32_t lane_base,
 // Warp w handles TMEM lanes 32 (w%4) + [0,32) (one v per thread) and column half w/4 (K/2 columns).
 template <int K>
 __device__ __forceinline__ void state_pass2(uint32_t tS, uint32_t lane_base, int half, int vrow, const float* fsb,
-                                            const float* fy, uint8_t* sSB) {
+                                            const float* fy, uint8_t* sSB, __nv_bfloat16* anch_row = nullptr) {
     constexpr int NL = 1;   // two loads in flight spill at 255 registers (measured slower)
     for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32 * NL)
-        state_pass_cols<NL>(tS, lane_base, c0, vrow, fsb, fy, sSB);
+        state_pass_cols<NL>(tS, lane_base, c0, vrow, fsb, fy, sSB, anch_row);
     tmem_wait_st();
 }
 

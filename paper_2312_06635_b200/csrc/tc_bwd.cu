@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "prof.h"
 #include "tc.h"
+#include "tc_build.cuh"
 #include "tc_common.cuh"
 
 namespace gla {
@@ -34,13 +35,12 @@ constexpr int VT = 128;
 constexpr int NTH = 256;
 constexpr float L2E = 1.4426950408889634f;
 constexpr float GUARD = 60.f;
+constexpr int ANCH = 4;   // d log alpha carry re-anchored from exact states every ANCH chunks
 }  // namespace
 
 template <int K>
 struct BwdCfg {
-    static constexpr int NPAIR = K / 2;
-    static constexpr int RG = NTH / NPAIR;
-    static constexpr int RPG = CH / RG;
+    using Tl = Tile<K>;                                // operand-build thread mapping (tc_build.cuh)
     static constexpr int KB = K / 64;
     static constexpr int NH = K / 128;                 // 128-channel halves (M=128 MMAs over channels)
     // shared memory (bytes, 1024-aligned blocks)
@@ -54,41 +54,16 @@ struct BwdCfg {
     static constexpr uint32_t OFF_P = OFF_DO + 16384;       // [64 t][128 B]
     static constexpr uint32_t OFF_DP = OFF_P + 8192;        // [64 t][128 B]
     static constexpr uint32_t OFF_STG = OFF_DP + 8192;      // [2][64 s][128 B] dv staging
-    static constexpr uint32_t OFF_F = OFF_STG + 16384;      // fsb[K], fy[K], pend[K], gtot[RG][K], red[4][K]
-    static constexpr uint32_t SMEM = OFF_F + 4 * (3 * K + RG * K + 4 * K) + 1024;
+    static constexpr uint32_t OFF_F = OFF_STG + 16384;      // fsb[K], fy[K], pend[K], red[4][K]
+    static constexpr uint32_t SMEM = OFF_F + 4 * (3 * K + 4 * K) + 1024;
+    static_assert(Tl::RG * K * 4 <= 8192, "gtot aliases the 8 KB P buffer");
+    static_assert(SMEM <= 232448, "dynamic shared memory");
     // TMEM columns
     static constexpr uint32_t COL_S = 0, COL_A = K, COL_B = K + 64, COL_C = K + 128;
 };
 
 // ---------------------------------------------------------------------------------------------------------------
 // Shared pieces: the TMEM state pass and the accumulator epilogues.
-template <int K>
-__device__ __forceinline__ void state_pass(uint32_t tS, uint32_t lane_base, int half, int vrow, const float* fsb,
-                                           const float* fy, uint8_t* sSB) {
-    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
-        uint32_t r[32];
-        tmem_ld32(tS + lane_base + c0, r);
-        tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-            const float y0 = __uint_as_float(r[j]), y1 = __uint_as_float(r[j + 1]);
-            pk[j / 2] = pack_bf16(y0 * fsb[c0 + j], y1 * fsb[c0 + j + 1]);
-            r[j] = __float_as_uint(y0 * fy[c0 + j]);
-            r[j + 1] = __float_as_uint(y1 * fy[c0 + j + 1]);
-        }
-        tmem_st32(tS + lane_base + c0, r);
-        uint8_t* dst = sSB + (c0 >> 6) * 16384;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int cc = (c0 & 63) + 8 * u;
-            *reinterpret_cast<uint4*>(dst + sw128_off(vrow, cc)) =
-                make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-        }
-    }
-    tmem_wait_st();
-}
-
 // M=64 accumulator [64 t x 64 s] in TMEM -> causal-masked bf16 rows [t][s] (SW128) in smem.
 // M=64 layout: row t lives in TMEM lane 32*(t/16) + t%16 (lanes 0-15 of each quarter; probe-tested).
 __device__ __forceinline__ void m64_epilogue(uint32_t tcol, uint32_t lane_base, int lq, int lane, uint8_t* dst) {
@@ -137,7 +112,7 @@ __global__ void __launch_bounds__(NTH, 1)
 k_bwd_dq(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
          const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g, const float* __restrict__ h0,
          const float* __restrict__ dfinal, __nv_bfloat16* __restrict__ dqp, float* __restrict__ stdot,
-         int* __restrict__ flag, int T, int V) {
+         __nv_bfloat16* __restrict__ anch, int* __restrict__ flag, int T, int V) {
     using Cfg = BwdCfg<K>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -149,8 +124,8 @@ k_bwd_dq(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtens
     float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
     float* fy = fsb + K;
     float* pend = fy + K;
-    float* gtot = pend + K;
-    float* red = gtot + Cfg::RG * K;
+    float* red = pend + K;
+    float* gtot = reinterpret_cast<float*>(sm + Cfg::OFF_P);   // cumsum exchange (P is unused here)
     __shared__ uint64_t bar_in, bar_m1, bar_m2;
     __shared__ uint32_t tmem_base;
 
@@ -158,8 +133,8 @@ k_bwd_dq(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtens
     const int vt = blockIdx.x, bh = blockIdx.y;
     const int v0 = vt * VT;
     const int NC = T / CH;
-    const int pj = tid % Cfg::NPAIR, rg = tid / Cfg::NPAIR;
-    const int ch0 = 2 * pj, row0 = rg * Cfg::RPG;
+    const int oc = tid % Cfg::Tl::NOCT, rg = tid / Cfg::Tl::NOCT;
+    const int ch0 = 8 * oc, row0 = rg * Cfg::Tl::RPG;
 
     if (warp == 0) tmem_alloc(&tmem_base, 512);
     if (tid == 0) {
@@ -190,17 +165,8 @@ k_bwd_dq(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtens
     tmem_wait_st();
 
     const size_t head_row = (size_t)bh * T;
-    uint32_t kr[Cfg::RPG];
-    float2 gr[Cfg::RPG];
-    auto prefetch = [&](int i) {
-#pragma unroll
-        for (int r = 0; r < Cfg::RPG; ++r) {
-            const size_t off = (head_row + (size_t)i * CH + row0 + r) * K + ch0;
-            kr[r] = __ldg(reinterpret_cast<const uint32_t*>(k + off));
-            gr[r] = ld_g2<TG>(g + off);
-        }
-    };
-    prefetch(0);
+    ChunkRegs<K> R;
+    load_chunk<K, TG, false, true>(R, nullptr, k, g, head_row, row0, ch0);
 
     const uint32_t idDP = idesc_bf16(64, 64, 0, 0);      // dP = dO V^T (K-major both, contraction over v)
     const uint32_t idDQ = idesc_bf16(128, 64, 1, 0);     // dq^T: A = SB (MN-major [ch][v]) / K~ (MN [ch][s])
@@ -219,50 +185,44 @@ k_bwd_dq(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtens
             tma_load_2d(sD, &tmD, &bar_in, v0, trow);
             tma_load_2d(sD + 8192, &tmD, &bar_in, v0 + 64, trow);
         }
-        float2 run = make_float2(0.f, 0.f);
+        float2 off[4], rr[4], Gm[4];
+        chunk_cumsum<K>(R, gtot, rg, ch0, off, rr, Gm);
+        bool bad_here = false;
+        if (rg == 0)
 #pragma unroll
-        for (int r = 0; r < Cfg::RPG; ++r) {
-            run.x += gr[r].x;
-            run.y += gr[r].y;
-            gr[r] = run;
-        }
-        gtot[rg * K + ch0] = run.x;
-        gtot[rg * K + ch0 + 1] = run.y;
-        __syncthreads();
-        float2 off = make_float2(0.f, 0.f), rr = make_float2(0.f, 0.f), Gm = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int r2 = 0; r2 < Cfg::RG; ++r2) {
-            const float a = gtot[r2 * K + ch0], b2 = gtot[r2 * K + ch0 + 1];
-            if (r2 < rg) { off.x += a; off.y += b2; }
-            if ((r2 + 1) * Cfg::RPG <= CH / 2) { rr.x += a; rr.y += b2; }
-            Gm.x += a; Gm.y += b2;
-        }
-        const bool bad_here = (rg == 0) && (-rr.x > GUARD || -rr.y > GUARD || rr.x - Gm.x > GUARD ||
-                                            rr.y - Gm.y > GUARD);
+            for (int p = 0; p < 4; ++p)
+                bad_here |= (-rr[p].x > GUARD) | (-rr[p].y > GUARD) | (rr[p].x - Gm[p].x > GUARD) |
+                            (rr[p].y - Gm[p].y > GUARD);
         any_slow |= __syncthreads_or(bad_here) != 0;
-        if (rg == 0) {
+        if (rg == 0) {   // SB = bf16(H_i e^{r}); Y <- H_i e^{r}; next pending = Gamma - r
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 const int m = ch0 + u;
-                const float r_ = u ? rr.y : rr.x, G_ = u ? Gm.y : Gm.x;
+                const float r_ = (u & 1) ? rr[u >> 1].y : rr[u >> 1].x, G_ = (u & 1) ? Gm[u >> 1].y : Gm[u >> 1].x;
                 fsb[m] = ex2f((pend[m] + r_) * L2E);
                 fy[m] = fsb[m];
                 pend[m] = G_ - r_;
             }
         }
+        float2 refk[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) refk[p] = make_float2(L2E * rr[p].x, L2E * rr[p].y);
         uint8_t* kbase = sK + (ch0 >> 6) * 8192;
         const int col = ch0 & 63;
 #pragma unroll
-        for (int r = 0; r < Cfg::RPG; ++r) {
-            const int t = row0 + r;
-            const float bx = gr[r].x + off.x, by = gr[r].y + off.y;
-            const float2 kf = bf2_to_f2(kr[r]);
-            *reinterpret_cast<uint32_t*>(kbase + sw128_off(t, col)) =
-                pack_bf16(kf.x * ex2f((rr.x - bx) * L2E), kf.y * ex2f((rr.y - by) * L2E));
+        for (int r = 0; r < Cfg::Tl::RPG; ++r) {
+            float2 b[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) b[p] = add2(R.g[r][p], off[p]);
+            scaled_row(R.k[r], b, refk, -1.f, kbase + sw128_off(row0 + r, col), nullptr);
         }
-        if (i + 1 < NC) prefetch(i + 1);
+        if (i + 1 < NC) load_chunk<K, TG, false, true>(R, nullptr, k, g, head_row + (size_t)(i + 1) * CH, row0, ch0);
         __syncthreads();
-        state_pass<K>(tS, lane_base, half, vrow, fsb, fy, sSB);   // SB = bf16(H_i e^r); Y <- H_i e^r
+        // SB = bf16(H_i e^r); Y <- H_i e^r.  Every ANCH chunks SB is also kept in HBM: k_bwd_dkv forms
+        // rowsum(H_i (.) dH_i) from it, the exact d log alpha carry at that boundary (R12).
+        __nv_bfloat16* arow = (i > 0 && i % ANCH == 0)
+            ? anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K : nullptr;
+        state_pass2<K>(tS, lane_base, half, vrow, fsb, fy, sSB, arow);
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
@@ -343,7 +303,8 @@ __global__ void __launch_bounds__(NTH, 1)
 k_bwd_dkv(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
           const __grid_constant__ CUtensorMap tmDV, const __nv_bfloat16* __restrict__ q,
           const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g, const float* __restrict__ dfinal,
-          __nv_bfloat16* __restrict__ dkp, float* __restrict__ dh0, const int* __restrict__ flag, int T, int V) {
+          __nv_bfloat16* __restrict__ dkp, float* __restrict__ dh0, const __nv_bfloat16* __restrict__ anch,
+          float* __restrict__ cpart, const int* __restrict__ flag, int T, int V) {
     using Cfg = BwdCfg<K>;
     if (*flag) return;   // exact CUDA-core path takes over
     extern __shared__ uint8_t smem_raw[];
@@ -359,7 +320,8 @@ k_bwd_dkv(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUten
     float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
     float* fy = fsb + K;
     float* pend = fy + K;
-    float* gtot = pend + K;
+    float* red = pend + K;                         // [4][K] anchor row-sum partials
+    float* gtot = reinterpret_cast<float*>(sP);   // cumsum exchange; P is free at chunk start
     __shared__ uint64_t bar_in, bar_m1, bar_m2;
     __shared__ uint32_t tmem_base;
 
@@ -367,8 +329,8 @@ k_bwd_dkv(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUten
     const int vt = blockIdx.x, bh = blockIdx.y;
     const int v0 = vt * VT;
     const int NC = T / CH;
-    const int pj = tid % Cfg::NPAIR, rg = tid / Cfg::NPAIR;
-    const int ch0 = 2 * pj, row0 = rg * Cfg::RPG;
+    const int oc = tid % Cfg::Tl::NOCT, rg = tid / Cfg::Tl::NOCT;
+    const int ch0 = 8 * oc, row0 = rg * Cfg::Tl::RPG;
 
     if (warp == 0) tmem_alloc(&tmem_base, 512);
     if (tid == 0) {
@@ -402,18 +364,8 @@ k_bwd_dkv(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUten
     tmem_wait_st();
 
     const size_t head_row = (size_t)bh * T;
-    uint32_t qr[Cfg::RPG], kr[Cfg::RPG];
-    float2 gr[Cfg::RPG];
-    auto prefetch = [&](int i) {
-#pragma unroll
-        for (int r = 0; r < Cfg::RPG; ++r) {
-            const size_t off = (head_row + (size_t)i * CH + row0 + r) * K + ch0;
-            qr[r] = __ldg(reinterpret_cast<const uint32_t*>(q + off));
-            kr[r] = __ldg(reinterpret_cast<const uint32_t*>(k + off));
-            gr[r] = ld_g2<TG>(g + off);
-        }
-    };
-    prefetch(NC - 1);
+    ChunkRegs<K> R;
+    load_chunk<K, TG, true, true>(R, q, k, g, head_row + (size_t)(NC - 1) * CH, row0, ch0);
 
     const uint32_t idP = idesc_bf16(64, 64, 0, 0);        // P = Q~ K~^T ; dP = dO V^T
     const uint32_t idZ = idesc_bf16(128, K, 1, 1);        // Z[v][ch] += dO^T Q~
@@ -434,51 +386,40 @@ k_bwd_dkv(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUten
             tma_load_2d(sD, &tmD, &bar_in, v0, trow);
             tma_load_2d(sD + 8192, &tmD, &bar_in, v0 + 64, trow);
         }
-        float2 run = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int r = 0; r < Cfg::RPG; ++r) {
-            run.x += gr[r].x;
-            run.y += gr[r].y;
-            gr[r] = run;
-        }
-        gtot[rg * K + ch0] = run.x;
-        gtot[rg * K + ch0 + 1] = run.y;
-        __syncthreads();
-        float2 off = make_float2(0.f, 0.f), rr = make_float2(0.f, 0.f), Gm = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int r2 = 0; r2 < Cfg::RG; ++r2) {
-            const float a = gtot[r2 * K + ch0], b2 = gtot[r2 * K + ch0 + 1];
-            if (r2 < rg) { off.x += a; off.y += b2; }
-            if ((r2 + 1) * Cfg::RPG <= CH / 2) { rr.x += a; rr.y += b2; }
-            Gm.x += a; Gm.y += b2;
-        }
+        float2 off[4], rr[4], Gm[4];
+        chunk_cumsum<K>(R, gtot, rg, ch0, off, rr, Gm);
         if (rg == 0) {   // dSB = bf16(dH_{i+1} e^{Gamma - r}); Z <- same; next pending = r
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 const int m = ch0 + u;
-                const float r_ = u ? rr.y : rr.x, G_ = u ? Gm.y : Gm.x;
+                const float r_ = (u & 1) ? rr[u >> 1].y : rr[u >> 1].x, G_ = (u & 1) ? Gm[u >> 1].y : Gm[u >> 1].x;
                 fsb[m] = ex2f((pend[m] + G_ - r_) * L2E);
                 fy[m] = fsb[m];
                 pend[m] = r_;
             }
         }
+        float2 refq[4], refk[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            refq[p] = make_float2(-L2E * rr[p].x, -L2E * rr[p].y);
+            refk[p] = make_float2(L2E * rr[p].x, L2E * rr[p].y);
+        }
         uint8_t* qbase = sQ + (ch0 >> 6) * 8192;
         uint8_t* kbase = sK + (ch0 >> 6) * 8192;
         const int col = ch0 & 63;
 #pragma unroll
-        for (int r = 0; r < Cfg::RPG; ++r) {
+        for (int r = 0; r < Cfg::Tl::RPG; ++r) {
             const int t = row0 + r;
-            const float bx = gr[r].x + off.x, by = gr[r].y + off.y;
-            const float2 qf = bf2_to_f2(qr[r]), kf = bf2_to_f2(kr[r]);
-            *reinterpret_cast<uint32_t*>(qbase + sw128_off(t, col)) =
-                pack_bf16(qf.x * ex2f((bx - rr.x) * L2E), qf.y * ex2f((by - rr.y) * L2E));
-            *reinterpret_cast<uint32_t*>(kbase + sw128_off(t, col)) =
-                pack_bf16(kf.x * ex2f((rr.x - bx) * L2E), kf.y * ex2f((rr.y - by) * L2E));
+            float2 b[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) b[p] = add2(R.g[r][p], off[p]);
+            scaled_row(R.q[r], b, refq, 1.f, qbase + sw128_off(t, col), nullptr);
+            scaled_row(R.k[r], b, refk, -1.f, kbase + sw128_off(t, col), nullptr);
         }
-        if (i > 0) prefetch(i - 1);
+        if (i > 0) load_chunk<K, TG, true, true>(R, q, k, g, head_row + (size_t)(i - 1) * CH, row0, ch0);
         if (tid == 0 && i < NC - 1) tma_store_wait_read();   // dv staging of the previous chunk consumed
         __syncthreads();
-        state_pass<K>(tZ, lane_base, half, vrow, fsb, fy, sSB);   // dSB = bf16(dH~), Z <- dH~
+        state_pass2<K>(tZ, lane_base, half, vrow, fsb, fy, sSB);   // dSB = bf16(dH~), Z <- dH~
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
@@ -558,6 +499,42 @@ k_bwd_dkv(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUten
             tma_store_2d(&tmDV, stg + 8192, v0 + 64, trow);
             tma_store_commit();
         }
+        if (i > 0 && i % ANCH == 0) {
+            // exact carry at boundary i over this V tile: sum_v H_i[ch][v] dH_i[ch][v]
+            //   = sum_v SB_anchor[v][ch] * Z[v][ch]   (SB = bf16(H_i e^{r_i}), dH_i = e^{r_i} Z)
+            const __nv_bfloat16* arow = anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K;
+            for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(tZ + lane_base + c0, r);
+                uint4 hv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) hv[u] = __ldg(reinterpret_cast<const uint4*>(arow + c0 + 8 * u));
+                tmem_wait_ld();
+                float x[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t w = word(hv[j >> 3], (j & 7) >> 1);
+                    x[j] = ((j & 1) ? bf16hi(w) : bf16lo(w)) * __uint_as_float(r[j]);
+                }
+                // butterfly transpose-reduce over the 32 lanes (31 shuffles): lane l ends with column l's sum
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) {
+                    const bool up = (lane & o) != 0;
+#pragma unroll
+                    for (int j = 0; j < o; ++j) {
+                        const float send = up ? x[j] : x[j + o];
+                        const float keep = up ? x[j + o] : x[j];
+                        x[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                    }
+                }
+                red[lq * K + c0 + lane] = x[0];
+            }
+            __syncthreads();
+            for (int m = tid; m < K; m += NTH)
+                cpart[(((size_t)(i / ANCH - 1) * gridDim.x + vt) * gridDim.y + bh) * K + m] =
+                    red[m] + red[K + m] + red[2 * K + m] + red[3 * K + m];
+            __syncthreads();
+        }
     }
     if (dh0) {   // dH_0 = Z e^{pend}
         for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
@@ -587,7 +564,8 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(const __nv_bfloat16* __restr
                                                     const __nv_bfloat16* __restrict__ dkp,
                                                     const float* __restrict__ stdot, __nv_bfloat16* __restrict__ dq,
                                                     __nv_bfloat16* __restrict__ dk, float* __restrict__ dg,
-                                                    const int* __restrict__ flag, int T, int BH) {
+                                                    const float* __restrict__ cpart, const int* __restrict__ flag,
+                                                    int T, int BH) {
     if (*flag) return;
     __shared__ float sb[64][65];      // g -> b (chunk-local cumsum), then x -> suffix sums
     __shared__ float carry_s[64];
@@ -628,6 +606,12 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(const __nv_bfloat16* __restr
     };
     load(NC - 1);
     for (int i = NC - 1; i >= 0; --i) {
+        if (tid < 64 && i + 1 < NC && (i + 1) % ANCH == 0) {   // exact carry rowsum(H_{i+1} (.) dH_{i+1})
+            float c0 = 0.f;
+            const size_t a = (i + 1) / ANCH - 1;
+            for (int j = 0; j < NVT; ++j) c0 += cpart[((a * NVT + j) * BH + bh) * K + m0 + tid];
+            carry_s[tid] = c0;
+        }
         // (a1) chunk-local cumsum: stage g, one thread per channel scans the 64 rows
 #pragma unroll
         for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = gv[u];
@@ -697,6 +681,10 @@ size_t bwd_tc_ws(int B, int H, int T, int K, int V, int C) {
     bytes += 2 * NVT * BH * T * K * sizeof(__nv_bfloat16);       // dq, dk partials
     bytes += NVT * BH * K * sizeof(float);                       // S_T . dS_T partials
     bytes = (bytes + 255) & ~size_t(255);
+    const size_t NA = (T / C > 1) ? (size_t)(T / C - 1) / ANCH : 0;
+    bytes += NA * BH * V * K * sizeof(__nv_bfloat16);           // state anchors (bf16)
+    bytes += NA * NVT * BH * K * sizeof(float);                 // anchor row-sum partials
+    bytes = (bytes + 255) & ~size_t(255);
     return bytes + simt::bwd_ws(B, H, T, K, V, C);              // exact-path fallback scratch
 }
 
@@ -710,6 +698,11 @@ static cudaError_t launch_bwd(const BwdProblem& p, cudaStream_t st) {
     __nv_bfloat16* dkp = dqp + (size_t)NVT * BH * p.T * K;
     float* stdot = (float*)(dkp + (size_t)NVT * BH * p.T * K);
     size_t used = 256 + 2 * (size_t)NVT * BH * p.T * K * 2 + (size_t)NVT * BH * K * 4;
+    used = (used + 255) & ~size_t(255);
+    const size_t NA = (p.T / CH > 1) ? (size_t)(p.T / CH - 1) / ANCH : 0;
+    __nv_bfloat16* anch = (__nv_bfloat16*)(ws + used);
+    float* cpart = (float*)(ws + used + NA * BH * p.V * K * 2);
+    used += NA * BH * p.V * K * 2 + NA * NVT * BH * K * 4;
     used = (used + 255) & ~size_t(255);
     cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
@@ -727,12 +720,12 @@ static cudaError_t launch_bwd(const BwdProblem& p, cudaStream_t st) {
     {
         GLA_PROF("tc::bwd_dq", st);
         k_bwd_dq<K, TG><<<grid, NTH, smem, st>>>(mV, mD, (const __nv_bfloat16*)p.k, (const TG*)p.g, p.h0, p.dfinal,
-                                                 dqp, p.dfinal ? stdot : nullptr, flag, p.T, p.V);
+                                                 dqp, p.dfinal ? stdot : nullptr, anch, flag, p.T, p.V);
     }
     {
         GLA_PROF("tc::bwd_dkv", st);
         k_bwd_dkv<K, TG><<<grid, NTH, smem, st>>>(mV, mD, mDV, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k,
-                                                  (const TG*)p.g, p.dfinal, dkp, p.dh0, flag, p.T, p.V);
+                                                  (const TG*)p.g, p.dfinal, dkp, p.dh0, anch, cpart, flag, p.T, p.V);
     }
     {
         GLA_PROF("tc::bwd_reduce", st);
@@ -741,10 +734,10 @@ static cudaError_t launch_bwd(const BwdProblem& p, cudaStream_t st) {
         __nv_bfloat16 *dq_ = (__nv_bfloat16*)p.dq, *dk_ = (__nv_bfloat16*)p.dk;
         const dim3 rg(K / 64, BH);
         switch (NVT) {
-            case 1: k_bwd_reduce<K, 1, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, flag, p.T, BH); break;
-            case 2: k_bwd_reduce<K, 2, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, flag, p.T, BH); break;
-            case 4: k_bwd_reduce<K, 4, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, flag, p.T, BH); break;
-            case 8: k_bwd_reduce<K, 8, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, flag, p.T, BH); break;
+            case 1: k_bwd_reduce<K, 1, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
+            case 2: k_bwd_reduce<K, 2, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
+            case 4: k_bwd_reduce<K, 4, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
+            case 8: k_bwd_reduce<K, 8, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
             default: return cudaErrorNotSupported;
         }
     }

@@ -72,3 +72,19 @@ def test_tc_bwd_full_size_sampled():
         for name, x, y in zip(("dq", "dk", "dv", "dlog_alpha"), got[:4], ref[:4]):
             e = nerr_slices(x[b:b + 1, h:h + 1].float().cpu().numpy(), y)
             assert e < TOL, (name, e)
+
+
+@pytest.mark.parametrize("T", [4096, 16384])
+def test_tc_bwd_long_sequence_dlog_alpha(T):
+    """BASELINE.json configs[3] lengths: the d log alpha carry is re-anchored from exact states every 4 chunks,
+    so its error does not grow with T (plain normwise metric, std gates)."""
+    B, H, K, V = 1, 2, 256, 512
+    p = synth.problem(B, H, T, K, V, seed=3)
+    pc = {n: t.cuda() for n, t in p.items()}
+    got = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, path="tc")
+    torch.cuda.synchronize()
+    f = {n: p[n].double().numpy() for n in ("q", "k", "v", "g", "do")}
+    ref = oracle.bwd(f["q"], f["k"], f["v"], f["g"], f["do"])
+    for name, x, y in zip(("dq", "dk", "dv", "dlog_alpha"), got[:4], ref[:4]):
+        e = nerr_slices(x.float().cpu().numpy(), y)
+        assert e < 1.2e-2, (name, e)
