@@ -318,6 +318,19 @@ def main():
         return
 
     hbm, tf_burst, tf_sus, peak_src = load_peaks()
+    ncu = {}
+    try:   # per-launch DRAM bytes of each kernel from the committed `ncu --set full` capture (profiles/)
+        ncu = json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_summary.json")))
+    except Exception:
+        pass
+
+    def traffic_of(name):
+        key = {"tc::fwd": "k_fwd<", "tc::bwd_dq": "k_bwd_dq<", "tc::bwd_dkv": "k_bwd_dkv<",
+               "tc::bwd_reduce": "k_bwd_reduce<"}.get(name)
+        for n, v in ncu.items():
+            if key and key in n and n.startswith("tc::") and f"<{K}," in n:
+                return v.get("traffic_bytes")
+        return None
     roof = None
     if prof:
         top = max(prof, key=lambda n: prof[n][0])
@@ -327,7 +340,7 @@ def main():
         if algo:
             by, fl = algo
             roof = {"kernel": top, "bound": "hbm", "achieved": by / per_launch_s / 1e9, "peak": hbm, "unit": "GB/s",
-                    "frac": by / per_launch_s / 1e9 / hbm, "traffic": None, "peak_source": peak_src,
+                    "frac": by / per_launch_s / 1e9 / hbm, "traffic": traffic_of(top), "peak_source": peak_src,
                     "algo_bytes_per_launch": by, "algo_flops_per_launch": fl,
                     "tensor_tflops": fl / per_launch_s / 1e12,
                     "share_of_step": tot / total_ms if total_ms else None, "ms_per_launch": per_launch_s * 1e3}
