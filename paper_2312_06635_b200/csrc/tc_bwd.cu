@@ -17,6 +17,7 @@
 // If any chunk's half-chunk log decay exceeds the factorisation guard, k_bwd_dq raises a device flag; the
 // TC kernels that follow then do nothing and the exact fp32 CUDA-core kernels (simt.cu) produce every
 // gradient instead (no host synchronisation).
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -669,15 +670,547 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(const __nv_bfloat16* __restr
     }
 }
 
+// ===============================================================================================================
+// Split backward (default): k_bwd_prep (chunk-parallel) computes, once per (b,h, chunk), the chunk-local cumsum
+// statistics, Q~hi, K~hi, P = (Q~ K~^T) (.) M (stacked hi/lo MMA) and dP = (dO V^T) (.) M over the full V
+// (TMA-streamed in 256-wide rounds); the two V-tiled walks are then fed entirely by TMA, and the intra-chunk terms
+// K~^T dP^T and Q~^T dP are added by the V tile 0 CTA only (dq, dk are sums over V tiles).
+template <int K>
+struct BPrepCfg {
+    using Tl = Tile<K>;
+    static constexpr int KB = K / 64;
+    static constexpr uint32_t OP = KB * 16384;            // [KB][128 rows: hi | lo][128 B]
+    static constexpr uint32_t OFF_Q = 0, OFF_K = OP;
+    static constexpr uint32_t OFF_D = 2 * OP;             // dO round: [4][64 t][128 B]
+    static constexpr uint32_t OFF_V = OFF_D + 32768;      // V round:  [4][64 t][128 B]
+    static constexpr uint32_t OFF_P = OFF_V + 32768;      // P  [64 t][128 B]
+    static constexpr uint32_t OFF_DP = OFF_P + 8192;      // dP [64 t][128 B]
+    static constexpr uint32_t OFF_X = OFF_DP + 8192;      // fp32 exchange [64][64] / cumsum exchange
+    static constexpr uint32_t SMEM = OFF_X + 16384 + 1024;
+    static_assert(SMEM <= 232448, "dynamic shared memory");
+};
+
+template <int K, typename TG>
+__global__ void __launch_bounds__(NTH, 1)
+k_bwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+           const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmDP,
+           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
+           const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g,
+           float* __restrict__ stats, int* __restrict__ flag, int T, int V) {
+    using Cfg = BPrepCfg<K>;
+    using Tl = typename Cfg::Tl;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = sm + Cfg::OFF_Q;
+    uint8_t* sK = sm + Cfg::OFF_K;
+    uint8_t* sD = sm + Cfg::OFF_D;
+    uint8_t* sV = sm + Cfg::OFF_V;
+    uint8_t* sP = sm + Cfg::OFF_P;
+    uint8_t* sdP = sm + Cfg::OFF_DP;
+    float* exch = reinterpret_cast<float*>(sm + Cfg::OFF_X);
+    __shared__ uint64_t bar_in, bar_m, bar_done;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int chunk = blockIdx.x, bh = blockIdx.y, NC = gridDim.x;
+    const int oc = tid % Tl::NOCT, rg = tid / Tl::NOCT;
+    const int ch0 = 8 * oc, row0 = rg * Tl::RPG;
+    const size_t crow = (size_t)bh * T + (size_t)chunk * CH;
+    const int VR = V < 256 ? V : 256, NR = V / VR, NBX = VR / 64;   // V rounds of VR columns (NBX boxes)
+
+    if (warp == 0) tmem_alloc(&tmem_base, 256);
+    if (tid == 0) {
+        mbar_init(&bar_in, 1);
+        mbar_init(&bar_m, 1);
+        mbar_init(&bar_done, 1);
+        fence_mbar_init();
+        mbar_expect_tx(&bar_in, 2 * NBX * 8192);
+        for (int b = 0; b < NBX; ++b) {
+            tma_load_2d(sD + b * 8192, &tmD, &bar_in, 64 * b, (int)crow);
+            tma_load_2d(sV + b * 8192, &tmV, &bar_in, 64 * b, (int)crow);
+        }
+    }
+    ChunkRegs<K> R;
+    load_chunk<K, TG, true, true>(R, q, k, g, crow, row0, ch0);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tP = tmem_base, tdP = tmem_base + 128;
+
+    float2 off[4], rr[4], Gm[4];
+    chunk_cumsum<K>(R, exch, rg, ch0, off, rr, Gm);
+    bool bad = false;
+    if (rg == 0)
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+            bad |= (-rr[p].x > GUARD) | (-rr[p].y > GUARD) | (rr[p].x - Gm[p].x > GUARD) | (rr[p].y - Gm[p].y > GUARD);
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(flag, 1);   // whole call -> exact CUDA-core kernels
+    if (rg == 0) {
+        float* st = stats + ((size_t)bh * NC + chunk) * 2 * K + ch0;
+        reinterpret_cast<float4*>(st)[0] = make_float4(rr[0].x, rr[0].y, rr[1].x, rr[1].y);
+        reinterpret_cast<float4*>(st)[1] = make_float4(rr[2].x, rr[2].y, rr[3].x, rr[3].y);
+        reinterpret_cast<float4*>(st + K)[0] = make_float4(Gm[0].x, Gm[0].y, Gm[1].x, Gm[1].y);
+        reinterpret_cast<float4*>(st + K)[1] = make_float4(Gm[2].x, Gm[2].y, Gm[3].x, Gm[3].y);
+    }
+    float2 refq[4], refk[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        refq[p] = make_float2(-L2E * rr[p].x, -L2E * rr[p].y);
+        refk[p] = make_float2(L2E * rr[p].x, L2E * rr[p].y);
+    }
+    const int blk = ch0 >> 6, col = ch0 & 63;
+    uint8_t* qb = sQ + blk * 16384;
+    uint8_t* kb = sK + blk * 16384;
+#pragma unroll
+    for (int r = 0; r < Tl::RPG; ++r) {
+        const int t = row0 + r;
+        float2 b[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) b[p] = add2(R.g[r][p], off[p]);
+        scaled_row(R.q[r], b, refq, 1.f, qb + sw128_off(t, col), qb + sw128_off(64 + t, col));
+        scaled_row(R.k[r], b, refk, -1.f, kb + sw128_off(t, col), kb + sw128_off(64 + t, col));
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+        tc_fence_after();
+        const uint32_t idPs = idesc_bf16(128, 128, 0, 0), idDP = idesc_bf16(64, 64, 0, 0);
+        const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aD = smem_u32(sD), aV = smem_u32(sV);
+#pragma unroll
+        for (int kk = 0; kk < K / 16; ++kk) {   // P: [Q~hi; Q~lo] [K~hi; K~lo]^T
+            const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+            mma_bf16(tP, sdesc_sw128(aQ + o, 16, 1024), sdesc_sw128(aK + o, 16, 1024), idPs, kk > 0);
+        }
+        for (int c = 0; c < K / 64; ++c) {     // Q~hi, K~hi -> HBM for the V-tiled walks
+            tma_store_2d(&tmQ, sQ + c * 16384, 64 * c, (int)crow);
+            tma_store_2d(&tmK, sK + c * 16384, 64 * c, (int)crow);
+        }
+        tma_store_commit();
+        for (int rd = 0; rd < NR; ++rd) {      // dP = dO V^T over the full V, VR columns per round
+            mbar_wait(&bar_in, rd & 1);
+            tc_fence_after();
+            for (int kk = 0; kk < VR / 16; ++kk) {
+                const uint32_t o = (kk >> 2) * 8192 + (kk & 3) * 32;
+                mma_bf16(tdP, sdesc_sw128(aD + o, 16, 1024), sdesc_sw128(aV + o, 16, 1024), idDP, (rd | kk) > 0);
+            }
+            if (rd + 1 < NR) {
+                mma_commit(&bar_m);
+                mbar_wait(&bar_m, rd & 1);   // the MMAs have consumed this round's tiles
+                mbar_expect_tx(&bar_in, 2 * NBX * 8192);
+                for (int b = 0; b < NBX; ++b) {
+                    tma_load_2d(sD + b * 8192, &tmD, &bar_in, (rd + 1) * VR + 64 * b, (int)crow);
+                    tma_load_2d(sV + b * 8192, &tmV, &bar_in, (rd + 1) * VR + 64 * b, (int)crow);
+                }
+            }
+        }
+        mma_commit(&bar_done);
+    }
+    mbar_wait(&bar_done, 0);   // one-shot barrier: every MMA of this CTA has completed
+    tc_fence_after();
+    const int lq = warp & 3, half = warp >> 2;
+    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
+    const int vrow = 32 * lq + lane;
+    // dP (M=64 layout) -> causal bf16 [t][s]; the lo-row warps of P run the P exchange meanwhile
+    if (half == 1) m64_epilogue(tdP, lane_base, lq, lane, sdP);
+    if (lq >= 2 && half == 0) {
+        for (int hc = 0; hc < 2; ++hc) {
+            uint32_t a[32], b[32];
+            tmem_ld32(tP + lane_base + 32 * hc, a);
+            tmem_ld32(tP + lane_base + 64 + 32 * hc, b);
+            tmem_wait_ld();
+            const int t = vrow - 64;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                exch[t * 64 + ((32 * hc + j + t) & 63)] = __uint_as_float(a[j]) + __uint_as_float(b[j]);
+        }
+    }
+    __syncthreads();
+    if (lq < 2) {
+        uint32_t a[32], b[32];
+        tmem_ld32(tP + lane_base + 32 * half, a);
+        tmem_ld32(tP + lane_base + 64 + 32 * half, b);
+        tmem_wait_ld();
+        const int t = vrow;
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+            const int s = 32 * half + j;
+            float p0 = __uint_as_float(a[j]) + __uint_as_float(b[j]) + exch[t * 64 + ((s + t) & 63)];
+            float p1 = __uint_as_float(a[j + 1]) + __uint_as_float(b[j + 1]) + exch[t * 64 + ((s + 1 + t) & 63)];
+            pk[j / 2] = pack_bf16(s <= t ? p0 : 0.f, s + 1 <= t ? p1 : 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<uint4*>(sP + sw128_off(t, 32 * half + 8 * u)) =
+                make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+        tma_store_2d(&tmP, sP, 0, (int)crow);
+        tma_store_2d(&tmDP, sdP, 0, (int)crow);
+        tma_store_commit();
+        tma_store_wait_all();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tP, 256);
+}
+
+template <int K>
+struct BWalkCfg {
+    static constexpr int KB = K / 64;
+    static constexpr uint32_t OP = KB * 8192;             // [KB][64 t][128 B]
+    static constexpr uint32_t OFF_Q = 0, OFF_K = OP, OFF_SB = 2 * OP;
+    static constexpr uint32_t OFF_V = OFF_SB + KB * 16384;   // [2][64 t][128 B]
+    static constexpr uint32_t OFF_D = OFF_V + 16384;         // [2][64 t][128 B]
+    static constexpr uint32_t OFF_P = OFF_D + 16384;         // [64 t][128 B]
+    static constexpr uint32_t OFF_DP = OFF_P + 8192;         // [64 t][128 B]
+    static constexpr uint32_t OFF_STG = OFF_DP + 8192;       // dv staging [2][64 s][128 B]
+    static constexpr uint32_t OFF_F = OFF_STG + 16384;       // fsb, fy, pend, red[4][K]
+    static constexpr uint32_t SMEM = OFF_F + 4 * 7 * K + 1024;
+    static_assert(SMEM <= 232448, "dynamic shared memory");
+};
+
+// Forward walk over chunks (recomputes H in TMEM): dq partial of this V tile (+ the intra term on V tile 0).
+template <int K>
+__global__ void __launch_bounds__(NTH, 1)
+k_bwd_dq2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmDP,
+          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
+          const float* __restrict__ stats, const float* __restrict__ h0, const float* __restrict__ dfinal,
+          __nv_bfloat16* __restrict__ dqp, float* __restrict__ stdot, __nv_bfloat16* __restrict__ anch,
+          const int* __restrict__ flag, int T, int V) {
+    using Cfg = BWalkCfg<K>;
+    if (*flag) return;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = sm + Cfg::OFF_K;
+    uint8_t* sSB = sm + Cfg::OFF_SB;
+    uint8_t* sV = sm + Cfg::OFF_V;
+    uint8_t* sD = sm + Cfg::OFF_D;
+    uint8_t* sdP = sm + Cfg::OFF_DP;
+    float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
+    float* fy = fsb + K;
+    float* pend = fy + K;
+    float* red = pend + K;
+    __shared__ uint64_t bar_in, bar_m;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int vt = blockIdx.x, bh = blockIdx.y, v0 = vt * VT, NC = T / CH;
+    const int rowb = bh * T;
+    const bool intra = vt == 0;
+    const uint32_t in_bytes = Cfg::OP + 32768 + (intra ? 8192 : 0);
+    auto load_inputs = [&](int i) {
+        const int row = rowb + i * CH;
+        mbar_expect_tx(&bar_in, in_bytes);
+        for (int c = 0; c < K / 64; ++c) tma_load_2d(sK + c * 8192, &tmK, &bar_in, 64 * c, row);
+        tma_load_2d(sV, &tmV, &bar_in, v0, row);
+        tma_load_2d(sV + 8192, &tmV, &bar_in, v0 + 64, row);
+        tma_load_2d(sD, &tmD, &bar_in, v0, row);
+        tma_load_2d(sD + 8192, &tmD, &bar_in, v0 + 64, row);
+        if (intra) tma_load_2d(sdP, &tmDP, &bar_in, 0, row);
+    };
+    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    if (tid == 0) {
+        mbar_init(&bar_in, 1);
+        mbar_init(&bar_m, 1);
+        fence_mbar_init();
+        load_inputs(0);
+    }
+    for (int m = tid; m < K; m += NTH) pend[m] = 0.f;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tS = tmem_base, tdq = tmem_base + K;
+    const int lq = warp & 3, half = warp >> 2;
+    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
+    const int vrow = 32 * lq + lane;
+    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+        uint32_t r[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(h0 ? h0[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
+        tmem_st32(tS + lane_base + c0, r);
+    }
+    tmem_wait_st();
+    const uint32_t idDQ = idesc_bf16(128, 64, 1, 0), idS = idesc_bf16(128, K, 1, 1);
+    const uint32_t aK = smem_u32(sK), aSB = smem_u32(sSB), aV = smem_u32(sV), aD = smem_u32(sD), adP = smem_u32(sdP);
+    for (int i = 0; i < NC; ++i) {
+        if (tid < K) {   // SB = bf16(H_i e^{r}); Y <- H_i e^{r}; next pending = Gamma - r
+            const float r_ = stats[((size_t)bh * NC + i) * 2 * K + tid], G_ = stats[((size_t)bh * NC + i) * 2 * K + K + tid];
+            fsb[tid] = ex2f((pend[tid] + r_) * L2E);
+            fy[tid] = fsb[tid];
+            pend[tid] = G_ - r_;
+        }
+        __syncthreads();
+        __nv_bfloat16* arow = (i > 0 && i % ANCH == 0)
+            ? anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K : nullptr;
+        state_pass2<K>(tS, lane_base, half, vrow, fsb, fy, sSB, arow);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            mbar_wait(&bar_in, i & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int hh = 0; hh < K / 128; ++hh) {
+#pragma unroll
+                for (int kk = 0; kk < VT / 16; ++kk) {   // dq^T[ch][t] = SB^T dO^T (this V tile)
+                    const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+                    mma_bf16(tdq + 64 * hh, sdesc_sw128(aSB + 2 * hh * 16384 + kk * 2048, 16384, 1024),
+                             sdesc_sw128(aD + ob, 16, 1024), idDQ, kk > 0);
+                }
+                if (intra)
+#pragma unroll
+                    for (int kk = 0; kk < CH / 16; ++kk)   // + K~^T dP^T (the full intra term, V tile 0 only)
+                        mma_bf16(tdq + 64 * hh, sdesc_sw128(aK + 2 * hh * 8192 + kk * 2048, 8192, 1024),
+                                 sdesc_sw128(adP + kk * 32, 16, 1024), idDQ, 1);
+            }
+#pragma unroll
+            for (int kk = 0; kk < CH / 16; ++kk)
+                mma_bf16(tS, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aK + kk * 2048, 8192, 1024), idS, 1);
+            mma_commit(&bar_m);
+        }
+        mbar_wait(&bar_m, i & 1);
+        tc_fence_after();
+        if (tid == 0 && i + 1 < NC) load_inputs(i + 1);   // every reader of the input tiles is done
+        partial_epilogue<K>(tdq, lane_base, lq, lane, warp, dqp + (size_t)vt * gridDim.y * T * K,
+                            (size_t)rowb + (size_t)i * CH);
+        tc_fence_before();
+        __syncthreads();
+    }
+    if (dfinal) {   // S_T . dS_T partial over this V tile
+        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tS + lane_base + c0, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                float x = __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E) * dfinal[((size_t)bh * K + c0 + j) * V + v0 + vrow];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                if (lane == 0) red[lq * K + c0 + j] = x;
+            }
+        }
+        __syncthreads();
+        for (int m = tid; m < K; m += NTH)
+            stdot[((size_t)vt * gridDim.y + bh) * K + m] = red[m] + red[K + m] + red[2 * K + m] + red[3 * K + m];
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem_base, 512);
+}
+
+// Reverse walk with dH in TMEM: dv (final) and the dk partial of this V tile (+ intra term on V tile 0), dh0.
+template <int K>
+__global__ void __launch_bounds__(NTH, 1)
+k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+           const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmDP,
+           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
+           const __grid_constant__ CUtensorMap tmDV, const float* __restrict__ stats,
+           const float* __restrict__ dfinal, __nv_bfloat16* __restrict__ dkp, float* __restrict__ dh0,
+           const __nv_bfloat16* __restrict__ anch, float* __restrict__ cpart, const int* __restrict__ flag, int T,
+           int V) {
+    using Cfg = BWalkCfg<K>;
+    if (*flag) return;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = sm + Cfg::OFF_Q;
+    uint8_t* sK = sm + Cfg::OFF_K;
+    uint8_t* sSB = sm + Cfg::OFF_SB;
+    uint8_t* sV = sm + Cfg::OFF_V;
+    uint8_t* sD = sm + Cfg::OFF_D;
+    uint8_t* sP = sm + Cfg::OFF_P;
+    uint8_t* sdP = sm + Cfg::OFF_DP;
+    uint8_t* stg = sm + Cfg::OFF_STG;
+    float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
+    float* fy = fsb + K;
+    float* pend = fy + K;
+    float* red = pend + K;
+    __shared__ uint64_t bar_in, bar_m;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int vt = blockIdx.x, bh = blockIdx.y, v0 = vt * VT, NC = T / CH;
+    const int rowb = bh * T;
+    const bool intra = vt == 0;
+    const uint32_t in_bytes = 2 * Cfg::OP + 32768 + 8192 + (intra ? 8192 : 0);
+    auto load_inputs = [&](int i) {
+        const int row = rowb + i * CH;
+        mbar_expect_tx(&bar_in, in_bytes);
+        for (int c = 0; c < K / 64; ++c) {
+            tma_load_2d(sQ + c * 8192, &tmQ, &bar_in, 64 * c, row);
+            tma_load_2d(sK + c * 8192, &tmK, &bar_in, 64 * c, row);
+        }
+        tma_load_2d(sV, &tmV, &bar_in, v0, row);
+        tma_load_2d(sV + 8192, &tmV, &bar_in, v0 + 64, row);
+        tma_load_2d(sD, &tmD, &bar_in, v0, row);
+        tma_load_2d(sD + 8192, &tmD, &bar_in, v0 + 64, row);
+        tma_load_2d(sP, &tmP, &bar_in, 0, row);
+        if (intra) tma_load_2d(sdP, &tmDP, &bar_in, 0, row);
+    };
+    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    if (tid == 0) {
+        mbar_init(&bar_in, 1);
+        mbar_init(&bar_m, 1);
+        fence_mbar_init();
+        load_inputs(NC - 1);
+    }
+    for (int m = tid; m < K; m += NTH) pend[m] = 0.f;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tZ = tmem_base, tdk = tmem_base + K, tdv = tmem_base + K + 128;
+    const int lq = warp & 3, half = warp >> 2;
+    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
+    const int vrow = 32 * lq + lane;
+    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+        uint32_t r[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            r[j] = __float_as_uint(dfinal ? dfinal[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
+        tmem_st32(tZ + lane_base + c0, r);
+    }
+    tmem_wait_st();
+    const uint32_t idZ = idesc_bf16(128, K, 1, 1);      // Z[v][ch] += dO^T Q~
+    const uint32_t idV1 = idesc_bf16(128, 64, 0, 0);    // dv^T = dSB K~^T
+    const uint32_t idV2 = idesc_bf16(128, 64, 1, 1);    // dv^T += dO^T P
+    const uint32_t idK1 = idesc_bf16(128, 64, 1, 0);    // dk^T = dSB^T V^T
+    const uint32_t idK2 = idesc_bf16(128, 64, 1, 1);    // dk^T += Q~^T dP
+    const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aSB = smem_u32(sSB), aV = smem_u32(sV), aD = smem_u32(sD),
+                   aP = smem_u32(sP), adP = smem_u32(sdP);
+    for (int i = NC - 1; i >= 0; --i) {
+        const uint32_t ph = (NC - 1 - i) & 1;
+        const int trow = rowb + i * CH;
+        if (tid < K) {   // dSB = bf16(dH_{i+1} e^{Gamma - r}); Z <- same; next pending = r
+            const float r_ = stats[((size_t)bh * NC + i) * 2 * K + tid], G_ = stats[((size_t)bh * NC + i) * 2 * K + K + tid];
+            fsb[tid] = ex2f((pend[tid] + G_ - r_) * L2E);
+            fy[tid] = fsb[tid];
+            pend[tid] = r_;
+        }
+        if (tid == 0 && i < NC - 1) tma_store_wait_read();   // dv staging of the previous chunk consumed
+        __syncthreads();
+        state_pass2<K>(tZ, lane_base, half, vrow, fsb, fy, sSB);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            mbar_wait(&bar_in, ph);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < K / 16; ++kk) {   // dv^T = dSB K~^T (inter)
+                const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+                mma_bf16(tdv, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aK + ob, 16, 1024), idV1, kk > 0);
+            }
+#pragma unroll
+            for (int kk = 0; kk < CH / 16; ++kk)      // dv^T += dO^T P (intra)
+                mma_bf16(tdv, sdesc_sw128(aD + kk * 2048, 8192, 1024), sdesc_sw128(aP + kk * 2048, 8192, 1024), idV2, 1);
+#pragma unroll
+            for (int hh = 0; hh < K / 128; ++hh) {
+#pragma unroll
+                for (int kk = 0; kk < VT / 16; ++kk) {   // dk^T = dSB^T V^T (inter, this V tile)
+                    const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+                    mma_bf16(tdk + 64 * hh, sdesc_sw128(aSB + 2 * hh * 16384 + kk * 2048, 16384, 1024),
+                             sdesc_sw128(aV + ob, 16, 1024), idK1, kk > 0);
+                }
+                if (intra)
+#pragma unroll
+                    for (int kk = 0; kk < CH / 16; ++kk)   // + Q~^T dP (the full intra term, V tile 0 only)
+                        mma_bf16(tdk + 64 * hh, sdesc_sw128(aQ + 2 * hh * 8192 + kk * 2048, 8192, 1024),
+                                 sdesc_sw128(adP + kk * 2048, 8192, 1024), idK2, 1);
+            }
+#pragma unroll
+            for (int kk = 0; kk < CH / 16; ++kk)      // Z += dO^T Q~ (reverse state pass)
+                mma_bf16(tZ, sdesc_sw128(aD + kk * 2048, 8192, 1024), sdesc_sw128(aQ + kk * 2048, 8192, 1024), idZ, 1);
+            mma_commit(&bar_m);
+        }
+        mbar_wait(&bar_m, ph);
+        tc_fence_after();
+        if (tid == 0 && i > 0) load_inputs(i - 1);
+        {
+            uint32_t r[32];
+            tmem_ld32(tdv + lane_base + 32 * half, r);
+            tmem_wait_ld();
+            uint8_t* dst = stg + (vrow >> 6) * 8192 + (vrow & 63) * 2;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                *reinterpret_cast<__nv_bfloat16*>(dst + (32 * half + j) * 128) = __float2bfloat16_rn(__uint_as_float(r[j]));
+        }
+        partial_epilogue<K>(tdk, lane_base, lq, lane, warp, dkp + (size_t)vt * gridDim.y * T * K, (size_t)trow);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tma_store_2d(&tmDV, stg, v0, trow);
+            tma_store_2d(&tmDV, stg + 8192, v0 + 64, trow);
+            tma_store_commit();
+        }
+        if (i > 0 && i % ANCH == 0) {   // exact carry at boundary i over this V tile (see k_bwd_dkv)
+            const __nv_bfloat16* arow = anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K;
+            for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(tZ + lane_base + c0, r);
+                uint4 hv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) hv[u] = __ldg(reinterpret_cast<const uint4*>(arow + c0 + 8 * u));
+                tmem_wait_ld();
+                float x[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t w = word(hv[j >> 3], (j & 7) >> 1);
+                    x[j] = ((j & 1) ? bf16hi(w) : bf16lo(w)) * __uint_as_float(r[j]);
+                }
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) {
+                    const bool up = (lane & o) != 0;
+#pragma unroll
+                    for (int j = 0; j < o; ++j) {
+                        const float send = up ? x[j] : x[j + o];
+                        const float keep = up ? x[j + o] : x[j];
+                        x[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                    }
+                }
+                red[lq * K + c0 + lane] = x[0];
+            }
+            __syncthreads();
+            for (int m = tid; m < K; m += NTH)
+                cpart[(((size_t)(i / ANCH - 1) * gridDim.x + vt) * gridDim.y + bh) * K + m] =
+                    red[m] + red[K + m] + red[2 * K + m] + red[3 * K + m];
+            __syncthreads();
+        }
+    }
+    if (dh0) {
+        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tZ + lane_base + c0, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                dh0[((size_t)bh * K + c0 + j) * V + v0 + vrow] = __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E);
+        }
+    }
+    if (tid == 0) tma_store_wait_all();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem_base, 512);
+}
+
 // ---------------------------------------------------------------------------------------------------------------
 bool bwd_tc_supported(int K, int V) {
     const int nvt = V / 128;
     return (K == 128 || K == 256) && V % 128 == 0 && (nvt == 1 || nvt == 2 || nvt == 4 || nvt == 8);
 }
 
+static size_t al1k(size_t x) { return (x + 1023) & ~size_t(1023); }
+// extra scratch of the split backward: Q~hi, K~hi, P, dP (bf16) and per-chunk (r, Gamma) statistics
+static size_t split_ws(int B, int H, int T, int K) {
+    const size_t BH = (size_t)B * H, rows = BH * T, NC = T / CH;
+    return 2 * al1k(rows * K * 2) + 2 * al1k(rows * 64 * 2) + al1k(BH * NC * 2 * K * 4);
+}
+
 size_t bwd_tc_ws(int B, int H, int T, int K, int V, int C) {
     const size_t BH = (size_t)B * H, NVT = V / VT;
-    size_t bytes = 256;                                         // flag
+    size_t bytes = 256 + split_ws(B, H, T, K);                  // flag + split-backward scratch
     bytes += 2 * NVT * BH * T * K * sizeof(__nv_bfloat16);       // dq, dk partials
     bytes += NVT * BH * K * sizeof(float);                       // S_T . dS_T partials
     bytes = (bytes + 255) & ~size_t(255);
@@ -692,7 +1225,7 @@ template <int K, typename TG>
 static cudaError_t launch_bwd(const BwdProblem& p, cudaStream_t st) {
     using Cfg = BwdCfg<K>;
     const int BH = p.B * p.H, NVT = p.V / VT;
-    uint8_t* ws = (uint8_t*)p.ws;
+    uint8_t* ws = (uint8_t*)p.ws + split_ws(p.B, p.H, p.T, K);   // (the split path uses the front part)
     int* flag = (int*)ws;
     __nv_bfloat16* dqp = (__nv_bfloat16*)(ws + 256);
     __nv_bfloat16* dkp = dqp + (size_t)NVT * BH * p.T * K;
@@ -749,11 +1282,101 @@ static cudaError_t launch_bwd(const BwdProblem& p, cudaStream_t st) {
     return simt::bwd(sp, st);
 }
 
+// Split backward: prep + TMA-fed walks + reduce (+ exact CUDA-core fallback behind the guard flag).
+template <int K, typename TG>
+static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
+    const int BH = p.B * p.H, NVT = p.V / VT, NC = p.T / CH;
+    const size_t rows = (size_t)BH * p.T;
+    uint8_t* w = (uint8_t*)p.ws;
+    __nv_bfloat16* Qt = (__nv_bfloat16*)w; w += al1k(rows * K * 2);
+    __nv_bfloat16* Kt = (__nv_bfloat16*)w; w += al1k(rows * K * 2);
+    __nv_bfloat16* Pm = (__nv_bfloat16*)w; w += al1k(rows * 64 * 2);
+    __nv_bfloat16* dPm = (__nv_bfloat16*)w; w += al1k(rows * 64 * 2);
+    float* stats = (float*)w; w += al1k((size_t)BH * NC * 2 * K * 4);
+    uint8_t* ws = w;
+    int* flag = (int*)ws;
+    __nv_bfloat16* dqp = (__nv_bfloat16*)(ws + 256);
+    __nv_bfloat16* dkp = dqp + (size_t)NVT * BH * p.T * K;
+    float* stdot = (float*)(dkp + (size_t)NVT * BH * p.T * K);
+    size_t used = 256 + 2 * (size_t)NVT * BH * p.T * K * 2 + (size_t)NVT * BH * K * 4;
+    used = (used + 255) & ~size_t(255);
+    const size_t NA = (NC > 1) ? (size_t)(NC - 1) / ANCH : 0;
+    __nv_bfloat16* anch = (__nv_bfloat16*)(ws + used);
+    float* cpart = (float*)(ws + used + NA * BH * p.V * K * 2);
+    used += NA * BH * p.V * K * 2 + NA * NVT * BH * K * 4;
+    used = (used + 255) & ~size_t(255);
+    cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    CUtensorMap mQ, mK, mP, mDP, mV, mD, mDV;
+    if ((e = make_map_2d(&mQ, Qt, rows, K, true)) != cudaSuccess) return e;
+    if ((e = make_map_2d(&mK, Kt, rows, K, true)) != cudaSuccess) return e;
+    if ((e = make_map_2d(&mP, Pm, rows, 64, true)) != cudaSuccess) return e;
+    if ((e = make_map_2d(&mDP, dPm, rows, 64, true)) != cudaSuccess) return e;
+    if ((e = make_map_2d(&mV, p.v, rows, p.V, true)) != cudaSuccess) return e;
+    if ((e = make_map_2d(&mD, p.dO, rows, p.V, true)) != cudaSuccess) return e;
+    if ((e = make_map_2d(&mDV, p.dv, rows, p.V, false)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_bwd_prep<K, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BPrepCfg<K>::SMEM)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_bwd_dq2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWalkCfg<K>::SMEM)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_bwd_dkv2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWalkCfg<K>::SMEM)))
+        return e;
+    {
+        GLA_PROF("tc::bwd_prep", st);
+        k_bwd_prep<K, TG><<<dim3(NC, BH), NTH, BPrepCfg<K>::SMEM, st>>>(
+            mQ, mK, mP, mDP, mV, mD, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k, (const TG*)p.g, stats, flag,
+            p.T, p.V);
+    }
+    const dim3 grid(NVT, BH);
+    {
+        GLA_PROF("tc::bwd_dq", st);
+        k_bwd_dq2<K><<<grid, NTH, BWalkCfg<K>::SMEM, st>>>(mK, mDP, mV, mD, stats, p.h0, p.dfinal, dqp,
+                                                            p.dfinal ? stdot : nullptr, anch, flag, p.T, p.V);
+    }
+    {
+        GLA_PROF("tc::bwd_dkv", st);
+        k_bwd_dkv2<K><<<grid, NTH, BWalkCfg<K>::SMEM, st>>>(mQ, mK, mP, mDP, mV, mD, mDV, stats, p.dfinal, dkp, p.dh0,
+                                                             anch, cpart, flag, p.T, p.V);
+    }
+    {
+        GLA_PROF("tc::bwd_reduce", st);
+        const __nv_bfloat16 *q_ = (const __nv_bfloat16*)p.q, *k_ = (const __nv_bfloat16*)p.k;
+        const float* sd = p.dfinal ? stdot : nullptr;
+        __nv_bfloat16 *dq_ = (__nv_bfloat16*)p.dq, *dk_ = (__nv_bfloat16*)p.dk;
+        const dim3 rg(K / 64, BH);
+        switch (NVT) {
+            case 1: k_bwd_reduce<K, 1, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
+            case 2: k_bwd_reduce<K, 2, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
+            case 4: k_bwd_reduce<K, 4, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
+            case 8: k_bwd_reduce<K, 8, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
+            default: return cudaErrorNotSupported;
+        }
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    BwdProblem sp = p;
+    sp.ws = ws + used;
+    sp.run_if = flag;
+    return simt::bwd(sp, st);
+}
+
+static bool bwd_fused() {   // GLA_BWD_FUSED=1: the earlier per-V-tile-build backward (A/B measurements)
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("GLA_BWD_FUSED");
+        v = (s && s[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 cudaError_t bwd_tc(const BwdProblem& p, cudaStream_t st) {
     const bool gf = p.gate_dtype == 1;
     switch (p.K) {
-        case 128: return gf ? launch_bwd<128, float>(p, st) : launch_bwd<128, __nv_bfloat16>(p, st);
-        case 256: return gf ? launch_bwd<256, float>(p, st) : launch_bwd<256, __nv_bfloat16>(p, st);
+        case 128:
+            if (bwd_fused()) return gf ? launch_bwd<128, float>(p, st) : launch_bwd<128, __nv_bfloat16>(p, st);
+            return gf ? launch_bwd2<128, float>(p, st) : launch_bwd2<128, __nv_bfloat16>(p, st);
+        case 256:
+            if (bwd_fused()) return gf ? launch_bwd<256, float>(p, st) : launch_bwd<256, __nv_bfloat16>(p, st);
+            return gf ? launch_bwd2<256, float>(p, st) : launch_bwd2<256, __nv_bfloat16>(p, st);
         default: return cudaErrorNotSupported;
     }
 }
