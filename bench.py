@@ -65,22 +65,28 @@ def kernel_algo(name, B, H, T, K, V, C, c, g_bytes=4, e=2):
     u = B * H * T          # token-heads per launch
     nvt = max(1, V // 128)
     fwd_f, bwd_f = flops_per_token_head(K, V, C, c)
+    P = 2 * C                   # one bf16 row of the C x C score matrix per token
+    st = 2 * 4 * K // C         # per-chunk (r, Gamma) statistics per token
     table = {
-        "tc::bwd_dq": (u * (e * K + g_bytes * K + 2 * e * V + nvt * e * K), u * (2 * K * V + (C + 1) * K + C * V)),
-        "tc::bwd_dkv": (u * (2 * e * K + g_bytes * K + 3 * e * V + nvt * e * K),
+        # split forward: prep reads q, k, log alpha and writes Q~hi, K~hi, P, stats; state reads those + v, writes o
+        "tc::fwd_prep": (u * (2 * e * K + g_bytes * K + 2 * e * K + P + st), u * 2 * (C + 1) * K),
+        "tc::fwd_state": (u * (2 * e * K + e * V + P + st + e * V), u * (4 * K * V + (C + c) * V)),
+        # split backward
+        "tc::bwd_prep": (u * (2 * e * K + g_bytes * K + 2 * e * V + 2 * e * K + 2 * P + st),
+                         u * (2 * (C + 1) * K + 2 * (C + 1) * V)),
+        "tc::bwd_dq": (u * (e * K + 2 * e * V + P + st + nvt * e * K), u * (2 * K * V + (C + 1) * K)),
+        "tc::bwd_dkv": (u * (2 * e * K + 2 * e * V + 2 * P + st + e * V + nvt * e * K),
                         u * (6 * K * V + (C + 1) * K + (C + c) * V)),
         "tc::bwd_reduce": (u * (2 * nvt * e * K + 2 * e * K + g_bytes * K + 2 * e * K + 4 * K), 0),
-        # fused forward: q, k, v, g in; o out
+        # fused single-kernel forward (GLA_FWD_FUSED=1): q, k, v, g in; o out
         "tc::fwd": (u * (2 * e * K + e * V + g_bytes * K + e * V), u * fwd_f),
+        # fp32 CUDA-core kernels
         "simt::k_fwd_state": (u * (2 * e * K + e * V + g_bytes * K + e * V + 4 * C), u * 4 * K * V + u * (C + 1) * V),
         "simt::k_intra_P": (u * (2 * e * K + g_bytes * K + 4 * C), u * (C + 1) * K),
         "simt::k_intra_dP": (u * (2 * e * V + 4 * C), u * (C + 1) * V),
-        # dq kernel: q?, k, v, g, dO, dP in; dq (+fp32 copy) out
         "simt::k_bwd_dq": (u * (e * K + e * V + g_bytes * K + e * V + 4 * C + e * K + 4 * K), u * 4 * K * V),
-        "simt::k_bwd_dk": (u * (2 * e * K + e * V + g_bytes * K + e * V + 4 * C + 4 * K + e * K + 4 * K),
-                           u * 4 * K * V),
+        "simt::k_bwd_dk": (u * (2 * e * K + e * V + g_bytes * K + e * V + 4 * C + 4 * K + e * K + 4 * K), u * 4 * K * V),
         "simt::k_bwd_dv": (u * (2 * e * K + g_bytes * K + e * V + 4 * C + e * V), u * 4 * K * V),
-        "tc::bwd": (u * (2 * e * K + e * V + g_bytes * K + e * V + 2 * e * K + e * V + 4 * K), u * bwd_f),
     }
     for key, val in table.items():
         if name.endswith(key) or name == key:
@@ -325,10 +331,11 @@ def main():
         pass
 
     def traffic_of(name):
-        key = {"tc::fwd": "k_fwd<", "tc::bwd_dq": "k_bwd_dq<", "tc::bwd_dkv": "k_bwd_dkv<",
+        key = {"tc::fwd": "k_fwd<", "tc::fwd_prep": "k_fwd_prep<", "tc::fwd_state": "k_fwd_state<",
+               "tc::bwd_prep": "k_bwd_prep<", "tc::bwd_dq": "k_bwd_dq2<", "tc::bwd_dkv": "k_bwd_dkv2<",
                "tc::bwd_reduce": "k_bwd_reduce<"}.get(name)
         for n, v in ncu.items():
-            if key and key in n and n.startswith("tc::") and f"<{K}," in n:
+            if key and key in n.split("::")[-1] and (f"<{K}," in n or f"<{K}>" in n):
                 return v.get("traffic_bytes")
         return None
     roof = None
