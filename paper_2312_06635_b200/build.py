@@ -14,6 +14,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"]
+FLAGS_C = [f for f in FLAGS if f != "-shared"]
+OBJ = os.path.join(HERE, "build")
 
 
 def sources():
@@ -29,24 +31,63 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+def _headers():
+    return glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+        [os.path.join(HERE, "..", "include", "gla.h")]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """One object per .cu (compiled in parallel, rebuilt when the source or any header is newer), then one
+    shared-library link.  ptxas resource usage of every kernel goes to ptxas_info.txt."""
     if not force and not stale():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(HERE, "..", "include"), "-o", LIB, *sources()]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    os.makedirs(OBJ, exist_ok=True)
+    hdr_t = max(os.path.getmtime(h) for h in _headers())
+    jobs = []
+    for src in sources():
+        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), hdr_t):
+            cmd = [NVCC, *ARCH, *FLAGS_C, "-I", os.path.join(HERE, "..", "include"), "-c", "-o", obj, src]
+            jobs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    info = {}
+    for src, pr in jobs:
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            sys.stderr.write(out + err)
+            raise RuntimeError(f"nvcc failed compiling {os.path.basename(src)}")
+        info[src] = err
+        with open(os.path.join(OBJ, os.path.basename(src)[:-3] + ".ptxas"), "w") as f:
+            f.write(err)
+    objs = [os.path.join(OBJ, os.path.basename(s)[:-3] + ".o") for s in sources()]
+    res = subprocess.run([NVCC, *ARCH, "-shared", "-o", LIB, *objs], capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libgla.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc failed linking libgla.so")
     with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
-        f.write(res.stderr)
+        for s in sources():
+            pf = os.path.join(OBJ, os.path.basename(s)[:-3] + ".ptxas")
+            if os.path.exists(pf):
+                f.write(open(pf).read())
+    if verbose:
+        sys.stderr.write("".join(info.values()))
     probe = [NVCC, *ARCH, *FLAGS, "-o", PROBE, os.path.join(CSRC, "probe", "tc_probe.cu")]
     res = subprocess.run(probe, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libgla_probe.so")
     return LIB
+
+
+def build_timing() -> str:
+    """libgla_timing.so: the same sources with -DGLA_PHASE_TIMING (kernels print per-chunk phase traces)."""
+    out = os.path.join(HERE, "libgla_timing.so")
+    cmd = [NVCC, *ARCH, *FLAGS, "-DGLA_PHASE_TIMING", "-I", os.path.join(HERE, "..", "include"), "-o", out,
+           *sources()]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libgla_timing.so")
+    return out
 
 
 if __name__ == "__main__":

@@ -12,7 +12,7 @@ using namespace gla::tc;
 
 __global__ void __launch_bounds__(128) k_probe(const __nv_bfloat16* __restrict__ A, const __nv_bfloat16* __restrict__ B,
                                                float* __restrict__ D, int M, int N, int K, int a_mn, int b_mn,
-                                               int use_tma, const __grid_constant__ CUtensorMap tmapA) {
+                                               int use_tma, int a_tmem, const __grid_constant__ CUtensorMap tmapA) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* sA = smem;                       // up to 64 KB
@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(128) k_probe(const __nv_bfloat16* __restrict__
     __shared__ uint64_t bar_mma, bar_tma;
     __shared__ uint32_t tbase;
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-    if (warp == 0) tmem_alloc(&tbase, N < 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256)));
+    if (warp == 0) tmem_alloc(&tbase, 512);
     if (tid == 0) {
         mbar_init(&bar_mma, 1);
         mbar_init(&bar_tma, 1);
@@ -48,12 +48,32 @@ __global__ void __launch_bounds__(128) k_probe(const __nv_bfloat16* __restrict__
         uint32_t off = b_mn ? (n / 64) * (K * 128) + sw128_off(k, n % 64) : (k / 64) * (N * 128) + sw128_off(n, k % 64);
         *reinterpret_cast<__nv_bfloat16*>(sB + off) = B[(size_t)k * N + n];
     }
+    const uint32_t tA = tbase + 256;          // A in TMEM (M = 128): row m = lane m, bf16 pairs per column
+    if (a_tmem) {
+        for (int c0 = 0; c0 < K / 2; c0 += 32) {
+            uint32_t r[32];
+            const int m = 32 * warp + lane;
+            for (int j = 0; j < 32; ++j)
+                r[j] = pack_bf16(__bfloat162float(A[(size_t)m * K + 2 * (c0 + j)]),
+                                 __bfloat162float(A[(size_t)m * K + 2 * (c0 + j) + 1]));
+            tmem_st32(taddr(tA, 32 * warp, c0), r);
+        }
+        tmem_wait_st();
+    }
     fence_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tbase;
-    if (tid == 0) {
+    if (tid == 0 && a_tmem) {
+        const uint32_t id = idesc_bf16(M, N, 0, b_mn);
+        for (int kk = 0; kk < K / 16; ++kk) {
+            uint64_t bd = b_mn ? sdesc_sw128(smem_u32(sB) + kk * 2048, K * 128, 1024)
+                               : sdesc_sw128(smem_u32(sB) + (kk / 4) * (N * 128) + (kk % 4) * 32, 16, 1024);
+            mma_bf16_ta(tmem, tA + kk * 8, bd, id, kk > 0);
+        }
+        mma_commit(&bar_mma);
+    } else if (tid == 0) {
         const uint32_t id = idesc_bf16(M, N, a_mn, b_mn);
         for (int kk = 0; kk < K / 16; ++kk) {
             uint64_t ad = a_mn ? sdesc_sw128(smem_u32(sA) + kk * 2048, K * 128, 1024)
@@ -78,7 +98,7 @@ __global__ void __launch_bounds__(128) k_probe(const __nv_bfloat16* __restrict__
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem, N < 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256)));
+    if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
@@ -86,7 +106,7 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 extern "C" int probe_gemm(const void* A, const void* At, const void* B, float* D, int M, int N, int K, int a_mn,
-                          int b_mn, int use_tma) {
+                          int b_mn, int use_tma, int a_tmem) {
     CUtensorMap map{};
     if (use_tma) {
         void* fn = nullptr;
@@ -103,7 +123,7 @@ extern "C" int probe_gemm(const void* A, const void* At, const void* B, float* D
     }
     const int smem = 65536 + 131072 + 1024;
     cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_probe<<<1, 128, smem>>>((const __nv_bfloat16*)A, (const __nv_bfloat16*)B, D, M, N, K, a_mn, b_mn, use_tma, map);
+    k_probe<<<1, 128, smem>>>((const __nv_bfloat16*)A, (const __nv_bfloat16*)B, D, M, N, K, a_mn, b_mn, use_tma, a_tmem, map);
     cudaError_t e = cudaDeviceSynchronize();
     return e == cudaSuccess ? 0 : 1000 + (int)e;
 }

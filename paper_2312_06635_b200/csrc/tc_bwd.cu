@@ -116,7 +116,7 @@ k_bwd_dq(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtens
          __nv_bfloat16* __restrict__ anch, int* __restrict__ flag, int T, int V) {
     using Cfg = BwdCfg<K>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_align1k(smem_raw);
     uint8_t* sK = sm + Cfg::OFF_K;
     uint8_t* sSB = sm + Cfg::OFF_SB;
     uint8_t* sV = sm + Cfg::OFF_V;
@@ -309,7 +309,7 @@ k_bwd_dkv(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUten
     using Cfg = BwdCfg<K>;
     if (*flag) return;   // exact CUDA-core path takes over
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_align1k(smem_raw);
     uint8_t* sQ = sm + Cfg::OFF_Q;
     uint8_t* sK = sm + Cfg::OFF_K;
     uint8_t* sSB = sm + Cfg::OFF_SB;
@@ -700,7 +700,7 @@ k_bwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     using Cfg = BPrepCfg<K>;
     using Tl = typename Cfg::Tl;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_align1k(smem_raw);
     uint8_t* sQ = sm + Cfg::OFF_Q;
     uint8_t* sK = sm + Cfg::OFF_K;
     uint8_t* sD = sm + Cfg::OFF_D;
@@ -883,7 +883,7 @@ k_bwd_dq2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUten
     using Cfg = BWalkCfg<K>;
     if (*flag) return;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_align1k(smem_raw);
     uint8_t* sK = sm + Cfg::OFF_K;
     uint8_t* sSB = sm + Cfg::OFF_SB;
     uint8_t* sV = sm + Cfg::OFF_V;
@@ -1014,7 +1014,7 @@ k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     using Cfg = BWalkCfg<K>;
     if (*flag) return;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_align1k(smem_raw);
     uint8_t* sQ = sm + Cfg::OFF_Q;
     uint8_t* sK = sm + Cfg::OFF_K;
     uint8_t* sSB = sm + Cfg::OFF_SB;

@@ -65,7 +65,7 @@ k_fwd(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorM
       const float* __restrict__ h0, float* __restrict__ final_state, float* __restrict__ ws, int T, int V) {
     using Cfg = FwdCfg<K>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_align1k(smem_raw);
     uint8_t* sQT = sm + Cfg::OFF_QT;
     uint8_t* sKB = sm + Cfg::OFF_KB;
     uint8_t* sSB = sm + Cfg::OFF_SB;

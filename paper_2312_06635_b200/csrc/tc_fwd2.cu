@@ -16,6 +16,7 @@
 // (prep computes P in fp32 log space with factors <= 1; the state kernel applies the decay before the update).
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cstdio>
 
 #include "common.cuh"
 #include "prof.h"
@@ -55,7 +56,7 @@ k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     using Cfg = PrepCfg<K>;
     using Tl = typename Cfg::Tl;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_align1k(smem_raw);
     uint8_t* sQ = sm + Cfg::OFF_Q;
     uint8_t* sK = sm + Cfg::OFF_K;
     uint8_t* sP = sm + Cfg::OFF_P;
@@ -210,185 +211,304 @@ k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
 }
 
 // ---------------------------------------------------------------------------------------------------------------
+// k_fwd_state: warp-specialised walk over the chunks of one (b,h) unit x 128-wide V tile.
+//   warps 0-7   ("state"):    per chunk, the TMEM state pass: Y <- H_i e^{r} (in place, fp32) and
+//                             SB = bf16(H_i e^{r}) written to TMEM as the A operand of the O MMAs;
+//                             the next chunks' K~ / V / P loads; at the end final_state.
+//   warp 8      ("mma S"):    the state update Y += V^T K~hi (N = K MMAs), commit bar_s.
+//   warps 9, 10 ("mma O"):    O^T = SB Q~hi^T split by channel range into two TMEM partials O_a, O_b, plus
+//                             V^T P^T (intra-chunk) into O_a; commits bar_oa / bar_ob.
+//   warps 11-14 ("epilogue"): O^T = O_a + O_b (TMEM) -> bf16 staging -> TMA store; the Q~ loads.
+// Three issuing warps because one thread issues at most one tcgen05.mma per ~110 cycles whatever N is
+// (profiles/r1_microbench.md): the N = 64 output MMAs need several issuers in parallel to approach the
+// tensor pipe's rate.  Serial chain per chunk: state MMA -> state pass -> state MMA; the O MMAs overlap the
+// next pass; epilogue, TMA loads and stores overlap everything.  SB never touches shared memory.
 template <int K>
 struct StateCfg {
     static constexpr int KB = K / 64;
     static constexpr uint32_t OP = KB * 8192;            // [KB][64 t][128 B]  Q~hi or K~hi
-    static constexpr uint32_t OFF_Q = 0, OFF_K = OP, OFF_SB = 2 * OP;
-    static constexpr uint32_t OFF_V = OFF_SB + KB * 16384;      // 2 buffers x [2][64 t][128 B]
+    static constexpr uint32_t OFF_Q = 0, OFF_K = 2 * OP;        // 2 buffers each
+    static constexpr uint32_t OFF_V = 4 * OP;                   // 2 buffers x [2][64 t][128 B]
     static constexpr uint32_t OFF_P = OFF_V + 2 * 16384;        // 2 buffers x [64 t][128 B]
-    static constexpr uint32_t OFF_STG = OFF_P + 2 * 8192;       // O staging [2][64 t][128 B]
-    static constexpr uint32_t OFF_F = OFF_STG + 16384;          // fsb, fy, pend [K]
+    static constexpr uint32_t OFF_STG = OFF_P + 2 * 8192;       // O staging 2 buffers x [2][64 t][128 B]
+    static constexpr uint32_t OFF_F = OFF_STG + 2 * 16384;      // fsb, fy, pend [K]
     static constexpr uint32_t SMEM = OFF_F + 4 * 3 * K + 1024;
     static_assert(SMEM <= 232448, "dynamic shared memory");
-    static constexpr uint32_t TCOLS = 2 * K >= 256 ? 512 : 256;
+    // TMEM: Y [K] | SB bf16 pairs [K/2] | O_a [64] | O_b [64]   (O partials 64-column aligned)
+    static constexpr uint32_t COL_SB = K, COL_OA = (K + K / 2 + 63) / 64 * 64, COL_OB = COL_OA + 64;
+    static constexpr uint32_t TCOLS = COL_OB + 64 > 256 ? 512 : 256;
+    static constexpr int NST = 256, NTHR = NST + 3 * 32 + 128;  // state, 3 MMA issuers, epilogue
+    static constexpr int NSB = K / 16;                           // K-steps of the SB Q~^T product
+    static constexpr int NSB_B = (NSB + 4) / 2, NSB_A = NSB - NSB_B;   // O_a also takes the 4 P V^T steps
 };
 
 template <int K>
-__global__ void __launch_bounds__(NTH, 1)
+__global__ void __launch_bounds__(StateCfg<K>::NTHR, 1)
 k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmV,
             const __grid_constant__ CUtensorMap tmO, const float* __restrict__ stats, const int* __restrict__ flags,
             const float* __restrict__ h0, float* __restrict__ final_state, int T, int V) {
     using Cfg = StateCfg<K>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_align1k(smem_raw);
     uint8_t* sQ = sm + Cfg::OFF_Q;
     uint8_t* sK = sm + Cfg::OFF_K;
-    uint8_t* sSB = sm + Cfg::OFF_SB;
     uint8_t* sV = sm + Cfg::OFF_V;
     uint8_t* sP = sm + Cfg::OFF_P;
     uint8_t* stg = sm + Cfg::OFF_STG;
     float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
     float* fy = fsb + K;
     float* pend = fy + K;
-    __shared__ uint64_t bar_qk, bar_vp[2], bar_m;
+    __shared__ uint64_t bar_q[2], bar_k[2], bar_vp[2], bar_sb, bar_s, bar_oa, bar_ob, bar_ofree;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int vt = blockIdx.x, bh = blockIdx.y;
     const int v0 = vt * VT, NC = T / CH;
     const int rowb = bh * T;
+#ifdef GLA_PHASE_TIMING
+    __shared__ long long trc[8][16];
+#define TR(ev, i) do { if ((i) < 16) trc[ev][i] = clock64(); } while (0)
+#else
+#define TR(ev, i) do {} while (0)
+#endif
+    auto load_q = [&](int i) {
+        const int b = i & 1;
+        mbar_expect_tx(&bar_q[b], Cfg::OP);
+        for (int c = 0; c < K / 64; ++c)
+            tma_load_2d(sQ + b * Cfg::OP + c * 8192, &tmQ, &bar_q[b], 64 * c, rowb + i * CH);
+    };
+    auto load_k = [&](int i) {
+        const int b = i & 1;
+        mbar_expect_tx(&bar_k[b], Cfg::OP);
+        for (int c = 0; c < K / 64; ++c)
+            tma_load_2d(sK + b * Cfg::OP + c * 8192, &tmK, &bar_k[b], 64 * c, rowb + i * CH);
+    };
+    auto load_vp = [&](int i) {
+        const int b = i & 1;
+        mbar_expect_tx(&bar_vp[b], 16384 + 8192);
+        tma_load_2d(sV + b * 16384, &tmV, &bar_vp[b], v0, rowb + i * CH);
+        tma_load_2d(sV + b * 16384 + 8192, &tmV, &bar_vp[b], v0 + 64, rowb + i * CH);
+        tma_load_2d(sP + b * 8192, &tmP, &bar_vp[b], 0, rowb + i * CH);
+    };
 
     if (warp == 0) tmem_alloc(&tmem_base, Cfg::TCOLS);
     if (tid == 0) {
-        mbar_init(&bar_qk, 1);
-        mbar_init(&bar_vp[0], 1);
-        mbar_init(&bar_vp[1], 1);
-        mbar_init(&bar_m, 1);
+        mbar_init(&bar_q[0], 1); mbar_init(&bar_q[1], 1); mbar_init(&bar_k[0], 1); mbar_init(&bar_k[1], 1);
+        mbar_init(&bar_vp[0], 1); mbar_init(&bar_vp[1], 1);
+        mbar_init(&bar_sb, 1); mbar_init(&bar_s, 1);
+        mbar_init(&bar_oa, 1); mbar_init(&bar_ob, 1); mbar_init(&bar_ofree, 1);
         fence_mbar_init();
         prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmP); prefetch_tmap(&tmV); prefetch_tmap(&tmO);
-        // chunk 0 inputs
-        mbar_expect_tx(&bar_qk, 2 * Cfg::OP);
-        for (int c = 0; c < K / 64; ++c) {
-            tma_load_2d(sQ + c * 8192, &tmQ, &bar_qk, 64 * c, rowb);
-            tma_load_2d(sK + c * 8192, &tmK, &bar_qk, 64 * c, rowb);
-        }
-        mbar_expect_tx(&bar_vp[0], 16384 + 8192);
-        tma_load_2d(sV, &tmV, &bar_vp[0], v0, rowb);
-        tma_load_2d(sV + 8192, &tmV, &bar_vp[0], v0 + 64, rowb);
-        tma_load_2d(sP, &tmP, &bar_vp[0], 0, rowb);
+        load_q(0);
+        load_k(0);
+        load_vp(0);
+        if (NC > 1) { load_q(1); load_k(1); load_vp(1); }
     }
-    for (int m = tid; m < K; m += NTH) pend[m] = 0.f;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tm = tmem_base;
-    const uint32_t tS = tm, tO = tm + K;
-    const int lq = warp & 3, half = warp >> 2;
-    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
-    const int vrow = 32 * lq + lane;
-    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
-        uint32_t r[32];
+    const uint32_t tS = tmem_base, tSB = tmem_base + Cfg::COL_SB;
+    const uint32_t tOa = tmem_base + Cfg::COL_OA, tOb = tmem_base + Cfg::COL_OB;
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    const int vrow = 32 * (warp & 3) + lane;
+
+    if (warp < 8) {
+        // ------------------------------------------------------------------ state warps
+        const int half = warp >> 2;
+        const int cbeg = half * (K / 2);
+        for (int m = tid; m < K; m += Cfg::NST) pend[m] = 0.f;
+        for (int c0 = cbeg; c0 < cbeg + K / 2; c0 += 32) {
+            uint32_t r[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-            r[j] = __float_as_uint(h0 ? h0[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
-        tmem_st32(tS + lane_base + c0, r);
-    }
-    tmem_wait_st();
-
-    const uint32_t idO = idesc_bf16(128, 64, 0, 0);      // O^T[v][t] = SB . Q~hi^T
-    const uint32_t idS = idesc_bf16(128, K, 1, 1);       // Y[v][ch] += V^T K~hi
-    const uint32_t idPV = idesc_bf16(128, 64, 1, 0);     // O^T += V^T P^T
-    const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aSB = smem_u32(sSB);
-    // per-chunk statistics (r, Gamma) for this thread's channel, one chunk ahead
-    float st_r = 0.f, st_G = 0.f;
-    int st_slow = 0;
-    if (tid < K) {
-        st_r = stats[((size_t)bh * NC) * 2 * K + tid];
-        st_G = stats[((size_t)bh * NC) * 2 * K + K + tid];
-    }
-    st_slow = flags[(size_t)bh * NC];
-
-    for (int i = 0; i < NC; ++i) {
-        const int buf = i & 1;
-        const int trow = rowb + i * CH;
-        const float r_ = st_r, G_ = st_G;
-        const bool slow = st_slow != 0;
-        if (i + 1 < NC) {   // next chunk's statistics
-            if (tid < K) {
-                st_r = stats[((size_t)bh * NC + i + 1) * 2 * K + tid];
-                st_G = stats[((size_t)bh * NC + i + 1) * 2 * K + K + tid];
-            }
-            st_slow = flags[(size_t)bh * NC + i + 1];
+            for (int j = 0; j < 32; ++j)
+                r[j] = __float_as_uint(h0 ? h0[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
+            tmem_st32(tS + lane_base + c0, r);
         }
+        tmem_wait_st();
+        float st_r = 0.f, st_G = 0.f;
         if (tid < K) {
-            const float p = pend[tid];
-            if (!slow) { fsb[tid] = ex2f((p + r_) * L2E); fy[tid] = fsb[tid]; pend[tid] = G_ - r_; }
-            else { fsb[tid] = ex2f(p * L2E); fy[tid] = ex2f((p + G_) * L2E); pend[tid] = 0.f; }
+            st_r = stats[((size_t)bh * NC) * 2 * K + tid];
+            st_G = stats[((size_t)bh * NC) * 2 * K + K + tid];
         }
-        if (tid == 0 && i > 0) tma_store_wait_read();   // O staging of chunk i-1 consumed (it sits after SB)
-        __syncthreads();
-        state_pass2<K>(tS, lane_base, half, vrow, fsb, fy, sSB);   // SB = bf16(H_i e^{r}); Y <- decayed
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-            mbar_wait(&bar_qk, i & 1);
-            mbar_wait(&bar_vp[buf], (i >> 1) & 1);
-            tc_fence_after();
-            const uint32_t aV = smem_u32(sV + buf * 16384), aP = smem_u32(sP + buf * 8192);
-#pragma unroll
-            for (int kk = 0; kk < K / 16; ++kk) {
-                const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-                mma_bf16(tO, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aQ + ob, 16, 1024), idO, kk > 0);
+        int st_slow = flags[(size_t)bh * NC];
+        named_bar_sync(1, Cfg::NST);           // pend initialised
+        for (int i = 0; i < NC; ++i) {
+            const float r_ = st_r, G_ = st_G;
+            const bool slow = st_slow != 0;
+            if (i + 1 < NC) {   // next chunk's statistics
+                if (tid < K) {
+                    st_r = stats[((size_t)bh * NC + i + 1) * 2 * K + tid];
+                    st_G = stats[((size_t)bh * NC + i + 1) * 2 * K + K + tid];
+                }
+                st_slow = flags[(size_t)bh * NC + i + 1];
             }
-#pragma unroll
-            for (int kk = 0; kk < CH / 16; ++kk)
-                mma_bf16(tO, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aP + kk * 32, 16, 1024), idPV, 1);
-#pragma unroll
-            for (int kk = 0; kk < CH / 16; ++kk)
-                mma_bf16(tS, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aK + kk * 2048, 8192, 1024), idS, 1);
-            mma_commit(&bar_m);
-            if (i + 1 < NC) {   // V, P of chunk i+1 into the other buffers (their last reader, chunk i-1, is done)
-                const int nb = buf ^ 1;
-                mbar_expect_tx(&bar_vp[nb], 16384 + 8192);
-                tma_load_2d(sV + nb * 16384, &tmV, &bar_vp[nb], v0, trow + CH);
-                tma_load_2d(sV + nb * 16384 + 8192, &tmV, &bar_vp[nb], v0 + 64, trow + CH);
-                tma_load_2d(sP + nb * 8192, &tmP, &bar_vp[nb], 0, trow + CH);
+            if (tid < K) {
+                const float p = pend[tid];
+                if (!slow) { fsb[tid] = ex2f((p + r_) * L2E); fy[tid] = fsb[tid]; pend[tid] = G_ - r_; }
+                else { fsb[tid] = ex2f(p * L2E); fy[tid] = ex2f((p + G_) * L2E); pend[tid] = 0.f; }
             }
-        }
-        mbar_wait(&bar_m, i & 1);
-        tc_fence_after();
-        if (tid == 0 && i + 1 < NC) {   // Q~hi, K~hi of chunk i+1 (the MMAs that read them are complete)
-            mbar_expect_tx(&bar_qk, 2 * Cfg::OP);
-            for (int c = 0; c < K / 64; ++c) {
-                tma_load_2d(sQ + c * 8192, &tmQ, &bar_qk, 64 * c, trow + CH);
-                tma_load_2d(sK + c * 8192, &tmK, &bar_qk, 64 * c, trow + CH);
+            if (i > 0) {                       // Y final for chunk i-1 (the state MMA of chunk i-1 completed)
+                mbar_wait(&bar_s, (i - 1) & 1);
+                tc_fence_after();
+                if (tid == 0) {                // K~ of chunk i+1 into the buffer the state MMA of chunk i-1 read
+                    TR(0, i);
+                    if (i + 1 < NC) load_k(i + 1);
+                }
             }
-        }
-        {   // O^T (TMEM) -> bf16 staging [box][t][64 v] -> TMA store
-            uint32_t r[32];
-            tmem_ld32(tO + lane_base + 32 * half, r);
-            tmem_wait_ld();
-            uint8_t* dst = stg + (vrow >> 6) * 8192 + (vrow & 63) * 2;
+            named_bar_sync(1, Cfg::NST);       // fsb / fy visible
+            const uint32_t sba = tSB + lane_base + cbeg / 2;
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-                *reinterpret_cast<__nv_bfloat16*>(dst + (32 * half + j) * 128) = __float2bfloat16_rn(__uint_as_float(r[j]));
-            fence_async_smem();
+            for (int s = 0; s < K / 64; ++s) { // 32-column slices of this thread's K/2 channels
+                const int cb = cbeg + 32 * s;
+                uint32_t pk[16];
+                uint32_t r[32];
+                tmem_ld32(tS + lane_base + cb, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                    const float4 fs = *reinterpret_cast<const float4*>(fsb + cb + j);
+                    const float4 fyv = *reinterpret_cast<const float4*>(fy + cb + j);
+                    const float2 y0 = make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+                    const float2 y1 = make_float2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                    pk[j / 2] = pack2(mul2(y0, make_float2(fs.x, fs.y)));
+                    pk[j / 2 + 1] = pack2(mul2(y1, make_float2(fs.z, fs.w)));
+                    const float2 z0 = mul2(y0, make_float2(fyv.x, fyv.y)), z1 = mul2(y1, make_float2(fyv.z, fyv.w));
+                    r[j] = __float_as_uint(z0.x); r[j + 1] = __float_as_uint(z0.y);
+                    r[j + 2] = __float_as_uint(z1.x); r[j + 3] = __float_as_uint(z1.y);
+                }
+                tmem_st32(tS + lane_base + cb, r);
+                if (s == 0 && i > 0) {         // the O MMAs of chunk i-1 (the readers of SB, V, P) have completed
+                    if (tid == 0) TR(6, i);
+                    mbar_wait(&bar_oa, (i - 1) & 1);
+                    mbar_wait(&bar_ob, (i - 1) & 1);
+                    tc_fence_after();
+                    if (tid == 0) {            // V/P of chunk i+1 into the buffers chunk i-1 used
+                        TR(7, i);
+                        if (i + 1 < NC) load_vp(i + 1);
+                    }
+                }
+                tmem_st16(sba + 16 * s, pk);
+            }
+            tmem_wait_st();
             tc_fence_before();
-            __syncthreads();
-            if (tid == 0) {
-                tma_store_2d(&tmO, stg, v0, trow);
-                tma_store_2d(&tmO, stg + 8192, v0 + 64, trow);
-                tma_store_commit();
+            named_bar_sync(1, Cfg::NST);       // SB written, Y decayed; fsb may be overwritten
+            if (tid == 0) { TR(1, i); mbar_arrive(&bar_sb); }
+        }
+        mbar_wait(&bar_s, (NC - 1) & 1);
+        tc_fence_after();
+        if (final_state) {
+            for (int c0 = cbeg; c0 < cbeg + K / 2; c0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(tS + lane_base + c0, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    final_state[((size_t)bh * K + c0 + j) * V + v0 + vrow] =
+                        __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E);
             }
         }
-    }
-    if (final_state) {
-        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tS + lane_base + c0, r);
-            tmem_wait_ld();
+    } else if (warp == 8) {
+        // ------------------------------------------------------------------ state MMA issuer
+        const uint32_t idS = idesc_bf16(128, K, 1, 1);       // Y[v][ch] += V^T K~hi
+        for (int i = 0; i < NC; ++i) {
+            const int b = i & 1;
+            const uint32_t aV = smem_u32(sV + b * 16384), aK = smem_u32(sK + b * Cfg::OP);
+            mbar_wait(&bar_sb, i & 1);
+            mbar_wait(&bar_k[b], (i >> 1) & 1);
+            mbar_wait(&bar_vp[b], (i >> 1) & 1);
+            tc_fence_after();
+            if (lane == 0) TR(2, i);
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-                final_state[((size_t)bh * K + c0 + j) * V + v0 + vrow] = __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E);
+            for (int kk = 0; kk < CH / 16; ++kk)
+                mma_bf16_w(tS, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aK + kk * 2048, 8192, 1024), idS, 1);
+            mma_commit_w(&bar_s);
+            __syncwarp();
         }
+    } else if (warp < 11) {
+        // ------------------------------------------------------------------ O MMA issuers (a: + P V^T)
+        const bool is_a = warp == 9;
+        const uint32_t idO = idesc_bf16(128, 64, 0, 0);      // O^T[v][t] = SB . Q~hi^T  (SB from TMEM)
+        const uint32_t idPV = idesc_bf16(128, 64, 1, 0);     // O^T += V^T P^T
+        const uint32_t tD = is_a ? tOa : tOb;
+        const int k0 = is_a ? 0 : Cfg::NSB_A, k1 = is_a ? Cfg::NSB_A : Cfg::NSB;
+        for (int i = 0; i < NC; ++i) {
+            const int b = i & 1;
+            const uint32_t aQ = smem_u32(sQ + b * Cfg::OP);
+            mbar_wait(&bar_sb, i & 1);
+            mbar_wait(&bar_q[b], (i >> 1) & 1);
+            if (is_a) mbar_wait(&bar_vp[b], (i >> 1) & 1);
+            if (i >= 1) mbar_wait(&bar_ofree, (i - 1) & 1);
+            tc_fence_after();
+            if (is_a && lane == 0) TR(3, i);
+            for (int kk = k0; kk < k1; ++kk)
+                mma_bf16_ta_w(tD, tSB + 8 * kk, sdesc_sw128(aQ + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idO,
+                              kk > k0);
+            if (is_a) {
+                const uint32_t aV = smem_u32(sV + b * 16384), aP = smem_u32(sP + b * 8192);
+#pragma unroll
+                for (int kk = 0; kk < CH / 16; ++kk)
+                    mma_bf16_w(tD, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aP + kk * 32, 16, 1024), idPV,
+                               Cfg::NSB_A > 0 || kk > 0);
+            }
+            mma_commit_w(is_a ? &bar_oa : &bar_ob);
+            __syncwarp();
+        }
+    } else {
+        // ------------------------------------------------------------------ epilogue warps
+        const int et = tid - Cfg::NST - 96;    // 0..127
+        for (int i = 0; i < NC; ++i) {
+            const int b = i & 1;
+            mbar_wait(&bar_oa, i & 1);
+            mbar_wait(&bar_ob, i & 1);
+            tc_fence_after();
+            if (et == 0) {
+                TR(4, i);
+                if (i + 2 < NC) load_q(i + 2);  // the O MMAs of chunk i (the readers of Q~ buffer b) are complete
+                tma_store_wait_read1();         // staging buffer b (chunk i-2) has been read
+            }
+            uint8_t* dst = stg + b * 16384 + (vrow >> 6) * 8192 + (vrow & 63) * 2;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint32_t ra[32], rb[32];
+                tmem_ld32(tOa + 32 * h + lane_base, ra);
+                tmem_ld32(tOb + 32 * h + lane_base, rb);
+                tmem_wait_ld();
+                if (h == 1) {
+                    tc_fence_before();
+                    named_bar_sync(2, 128);    // O_a / O_b drained; staging b free
+                    if (et == 0) mbar_arrive(&bar_ofree);
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    *reinterpret_cast<__nv_bfloat16*>(dst + (32 * h + j) * 128) =
+                        __float2bfloat16_rn(__uint_as_float(ra[j]) + __uint_as_float(rb[j]));
+            }
+            fence_async_smem();
+            named_bar_sync(2, 128);
+            if (et == 0) {
+                const int trow = rowb + i * CH;
+                tma_store_2d(&tmO, stg + b * 16384, v0, trow);
+                tma_store_2d(&tmO, stg + b * 16384 + 8192, v0 + 64, trow);
+                tma_store_commit();
+                TR(5, i);
+            }
+        }
+        if (et == 0) tma_store_wait_all();
     }
-    if (tid == 0) tma_store_wait_all();
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc(tm, Cfg::TCOLS);
+#ifdef GLA_PHASE_TIMING
+    if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+        const long long t0 = trc[1][0];
+        printf("fwd_state trace (cycles from chunk 0 state-pass end): S0=bar_s(i-1) seen, s0done/obar=slice 0 "
+               "done / O MMAs of i-1 seen, S1=pass done, M0=state MMA issue, M1=O_a issue, E0=O ready, E1=stored\n");
+        for (int i = 1; i < 16 && i < NC; ++i)
+            printf("  chunk %2d: S0 %7lld s0done %7lld obar %7lld S1 %7lld M0 %7lld M1 %7lld E0 %7lld E1 %7lld\n", i,
+                   trc[0][i] - t0, trc[6][i] - t0, trc[7][i] - t0, trc[1][i] - t0, trc[2][i] - t0, trc[3][i] - t0,
+                   trc[4][i] - t0, trc[5][i] - t0);
+    }
+#endif
+    if (warp == 0) tmem_dealloc(tmem_base, Cfg::TCOLS);
 }
 
 // ---------------------------------------------------------------------------------------------------------------
@@ -430,7 +550,7 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     }
     {
         GLA_PROF("tc::fwd_state", st);
-        k_fwd_state<K><<<dim3(p.V / VT, (unsigned)BH), NTH, StateCfg<K>::SMEM, st>>>(
+        k_fwd_state<K><<<dim3(p.V / VT, (unsigned)BH), StateCfg<K>::NTHR, StateCfg<K>::SMEM, st>>>(
             mQ, mK, mP, mV, mO, stats, flags, p.h0, p.final_state, p.T, p.V);
     }
     return cudaGetLastError();

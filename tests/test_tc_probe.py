@@ -13,7 +13,7 @@ LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 
 @pytest.fixture(scope="module")
 def probe():
     L = ctypes.CDLL(LIB)
-    L.probe_gemm.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int] * 6
+    L.probe_gemm.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int] * 7
     return L
 
 
@@ -25,7 +25,22 @@ def test_probe_gemm(probe, M, N, K, a_mn, b_mn, tma):
     B = torch.randn(K, N, device="cuda").bfloat16()
     At = A.t().contiguous()
     D = torch.full((M, N), float("nan"), device="cuda")
-    rc = probe.probe_gemm(A.data_ptr(), At.data_ptr(), B.data_ptr(), D.data_ptr(), M, N, K, a_mn, b_mn, tma)
+    rc = probe.probe_gemm(A.data_ptr(), At.data_ptr(), B.data_ptr(), D.data_ptr(), M, N, K, a_mn, b_mn, tma, 0)
+    assert rc == 0, rc
+    ref = A.float() @ B.float()
+    err = (D - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-5, err
+
+
+@pytest.mark.parametrize("N,K", [(64, 256), (64, 128), (128, 64), (256, 64)])
+@pytest.mark.parametrize("b_mn", [0, 1])
+def test_probe_gemm_a_in_tmem(probe, N, K, b_mn):
+    """A operand read from TMEM (M = 128 lanes, bf16 pairs per column): the forward's O = SB Q~^T MMA."""
+    torch.manual_seed(1)
+    A = torch.randn(128, K, device="cuda").bfloat16()
+    B = torch.randn(K, N, device="cuda").bfloat16()
+    D = torch.full((128, N), float("nan"), device="cuda")
+    rc = probe.probe_gemm(A.data_ptr(), A.data_ptr(), B.data_ptr(), D.data_ptr(), 128, N, K, 0, b_mn, 0, 1)
     assert rc == 0, rc
     ref = A.float() @ B.float()
     err = (D - ref).abs().max().item() / ref.abs().max().item()
