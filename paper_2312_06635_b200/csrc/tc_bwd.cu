@@ -17,6 +17,7 @@
 // If any chunk's half-chunk log decay exceeds the factorisation guard, k_bwd_dq raises a device flag; the
 // TC kernels that follow then do nothing and the exact fp32 CUDA-core kernels (simt.cu) produce every
 // gradient instead (no host synchronisation).
+#include <cstdio>
 #include <cstdlib>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -873,14 +874,29 @@ struct BWalkCfg {
 };
 
 // Forward walk over chunks (recomputes H in TMEM): dq partial of this V tile (+ the intra term on V tile 0).
+// Warp roles (480 threads):
+//   warps 0-7   state pass SB = bf16(H_i e^{r}) (smem, MN-major A operand of dq^T), Y <- H_i e^{r} (TMEM);
+//               the exact-state anchors for the d log alpha carry; S_T . dS_T at the end.
+//   warp 8      state MMA Y += V^T K~ (N = K); warps 9, 10: dq^T channel halves = SB^T dO^T (+ K~^T dP^T) into
+//               one of two TMEM buffers (double-buffered so the epilogue is off the serial chain).
+//   warps 11-14 epilogue: dq partial -> global (bf16); the next chunk's input loads.
 template <int K>
-__global__ void __launch_bounds__(NTH, 1)
+struct DqCfg {
+    static constexpr int NST = 256, NTHR = NST + 3 * 32 + 128;
+    static constexpr uint32_t DQB = 64 * (K / 128);          // columns of one dq^T buffer (K/128 halves)
+    static constexpr uint32_t COL_DQ = K;
+    static constexpr uint32_t TCOLS = K + 2 * DQB > 256 ? 512 : 256;
+};
+
+template <int K>
+__global__ void __launch_bounds__(DqCfg<K>::NTHR, 1)
 k_bwd_dq2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmDP,
           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
           const float* __restrict__ stats, const float* __restrict__ h0, const float* __restrict__ dfinal,
           __nv_bfloat16* __restrict__ dqp, float* __restrict__ stdot, __nv_bfloat16* __restrict__ anch,
           const int* __restrict__ flag, int T, int V) {
     using Cfg = BWalkCfg<K>;
+    using DC = DqCfg<K>;
     if (*flag) return;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_align1k(smem_raw);
@@ -893,7 +909,7 @@ k_bwd_dq2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUten
     float* fy = fsb + K;
     float* pend = fy + K;
     float* red = pend + K;
-    __shared__ uint64_t bar_in, bar_m;
+    __shared__ uint64_t bar_in, bar_sb, bar_m[3], bar_efree[2];
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int vt = blockIdx.x, bh = blockIdx.y, v0 = vt * VT, NC = T / CH;
@@ -910,100 +926,171 @@ k_bwd_dq2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUten
         tma_load_2d(sD + 8192, &tmD, &bar_in, v0 + 64, row);
         if (intra) tma_load_2d(sdP, &tmDP, &bar_in, 0, row);
     };
-    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    if (warp == 0) tmem_alloc(&tmem_base, DC::TCOLS);
     if (tid == 0) {
         mbar_init(&bar_in, 1);
-        mbar_init(&bar_m, 1);
+        mbar_init(&bar_sb, 1);
+        for (int j = 0; j < 3; ++j) mbar_init(&bar_m[j], 1);
+        mbar_init(&bar_efree[0], 1);
+        mbar_init(&bar_efree[1], 1);
         fence_mbar_init();
         load_inputs(0);
     }
-    for (int m = tid; m < K; m += NTH) pend[m] = 0.f;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tS = tmem_base, tdq = tmem_base + K;
-    const int lq = warp & 3, half = warp >> 2;
+    const uint32_t tS = tmem_base, tdq = tmem_base + DC::COL_DQ;
+    const int lq = warp & 3;
     const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
     const int vrow = 32 * lq + lane;
-    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
-        uint32_t r[32];
+    auto wait_mmas = [&](uint32_t ph) {
+        for (int j = 0; j < 3; ++j) mbar_wait(&bar_m[j], ph);
+    };
+
+    if (warp < 8) {
+        // ------------------------------------------------------------------ state warps
+        const int half = warp >> 2;
+        for (int m = tid; m < K; m += DC::NST) pend[m] = 0.f;
+        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+            uint32_t r[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(h0 ? h0[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
-        tmem_st32(tS + lane_base + c0, r);
-    }
-    tmem_wait_st();
-    const uint32_t idDQ = idesc_bf16(128, 64, 1, 0), idS = idesc_bf16(128, K, 1, 1);
-    const uint32_t aK = smem_u32(sK), aSB = smem_u32(sSB), aV = smem_u32(sV), aD = smem_u32(sD), adP = smem_u32(sdP);
-    for (int i = 0; i < NC; ++i) {
-        if (tid < K) {   // SB = bf16(H_i e^{r}); Y <- H_i e^{r}; next pending = Gamma - r
-            const float r_ = stats[((size_t)bh * NC + i) * 2 * K + tid], G_ = stats[((size_t)bh * NC + i) * 2 * K + K + tid];
-            fsb[tid] = ex2f((pend[tid] + r_) * L2E);
-            fy[tid] = fsb[tid];
-            pend[tid] = G_ - r_;
+            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(h0 ? h0[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
+            tmem_st32(tS + lane_base + c0, r);
         }
-        __syncthreads();
-        __nv_bfloat16* arow = (i > 0 && i % ANCH == 0)
-            ? anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K : nullptr;
-        state_pass2<K>(tS, lane_base, half, vrow, fsb, fy, sSB, arow);
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-            mbar_wait(&bar_in, i & 1);
-            tc_fence_after();
+        tmem_wait_st();
+        float st_r = 0.f, st_G = 0.f;          // per-chunk statistics, one chunk ahead
+        if (tid < K) {
+            st_r = stats[((size_t)bh * NC) * 2 * K + tid];
+            st_G = stats[((size_t)bh * NC) * 2 * K + K + tid];
+        }
+        named_bar_sync(1, DC::NST);
+        for (int i = 0; i < NC; ++i) {
+            if (tid < K) {   // SB = bf16(H_i e^{r}); Y <- H_i e^{r}; next pending = Gamma - r
+                const float r_ = st_r, G_ = st_G;
+                if (i + 1 < NC) {
+                    st_r = stats[((size_t)bh * NC + i + 1) * 2 * K + tid];
+                    st_G = stats[((size_t)bh * NC + i + 1) * 2 * K + K + tid];
+                }
+                fsb[tid] = ex2f((pend[tid] + r_) * L2E);
+                fy[tid] = fsb[tid];
+                pend[tid] = G_ - r_;
+            }
+            if (i > 0) {                       // every MMA of chunk i-1 has completed (Y final, SB free)
+                wait_mmas((i - 1) & 1);
+                tc_fence_after();
+            }
+            named_bar_sync(1, DC::NST);
+            __nv_bfloat16* arow = (i > 0 && i % ANCH == 0)
+                ? anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K : nullptr;
+            state_pass2<K>(tS, lane_base, half, vrow, fsb, fy, sSB, arow);
+            fence_async_smem();
+            tc_fence_before();
+            named_bar_sync(1, DC::NST);
+            if (tid == 0) mbar_arrive(&bar_sb);
+        }
+        wait_mmas((NC - 1) & 1);
+        tc_fence_after();
+        if (dfinal) {   // S_T . dS_T partial over this V tile
+            for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(tS + lane_base + c0, r);
+                tmem_wait_ld();
 #pragma unroll
-            for (int hh = 0; hh < K / 128; ++hh) {
+                for (int j = 0; j < 32; ++j) {
+                    float x = __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E) * dfinal[((size_t)bh * K + c0 + j) * V + v0 + vrow];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                    if (lane == 0) red[lq * K + c0 + j] = x;
+                }
+            }
+            named_bar_sync(1, DC::NST);
+            for (int m = tid; m < K; m += DC::NST)
+                stdot[((size_t)vt * gridDim.y + bh) * K + m] = red[m] + red[K + m] + red[2 * K + m] + red[3 * K + m];
+        }
+    } else if (warp < 11) {
+        // ------------------------------------------------------------------ MMA issuers
+        const int role = warp - 8;
+        const uint32_t idDQ = idesc_bf16(128, 64, 1, 0), idS = idesc_bf16(128, K, 1, 1);
+        const uint32_t aK = smem_u32(sK), aSB = smem_u32(sSB), aV = smem_u32(sV), aD = smem_u32(sD), adP = smem_u32(sdP);
+        for (int i = 0; i < NC; ++i) {
+            const int b = i & 1;
+            mbar_wait(&bar_sb, i & 1);
+            mbar_wait(&bar_in, i & 1);
+            if (role > 0 && i >= 2) mbar_wait(&bar_efree[b], ((i >> 1) - 1) & 1);
+            tc_fence_after();
+            if (role == 0) {
+#pragma unroll
+                for (int kk = 0; kk < CH / 16; ++kk)
+                    mma_bf16_w(tS, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aK + kk * 2048, 8192, 1024), idS, 1);
+            } else if (role - 1 < K / 128) {
+                const int hh = role - 1;
+                const uint32_t td = tdq + DC::DQB * b + 64 * hh;
 #pragma unroll
                 for (int kk = 0; kk < VT / 16; ++kk) {   // dq^T[ch][t] = SB^T dO^T (this V tile)
                     const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-                    mma_bf16(tdq + 64 * hh, sdesc_sw128(aSB + 2 * hh * 16384 + kk * 2048, 16384, 1024),
-                             sdesc_sw128(aD + ob, 16, 1024), idDQ, kk > 0);
+                    mma_bf16_w(td, sdesc_sw128(aSB + 2 * hh * 16384 + kk * 2048, 16384, 1024),
+                               sdesc_sw128(aD + ob, 16, 1024), idDQ, kk > 0);
                 }
                 if (intra)
 #pragma unroll
                     for (int kk = 0; kk < CH / 16; ++kk)   // + K~^T dP^T (the full intra term, V tile 0 only)
-                        mma_bf16(tdq + 64 * hh, sdesc_sw128(aK + 2 * hh * 8192 + kk * 2048, 8192, 1024),
-                                 sdesc_sw128(adP + kk * 32, 16, 1024), idDQ, 1);
+                        mma_bf16_w(td, sdesc_sw128(aK + 2 * hh * 8192 + kk * 2048, 8192, 1024),
+                                   sdesc_sw128(adP + kk * 32, 16, 1024), idDQ, 1);
             }
-#pragma unroll
-            for (int kk = 0; kk < CH / 16; ++kk)
-                mma_bf16(tS, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aK + kk * 2048, 8192, 1024), idS, 1);
-            mma_commit(&bar_m);
+            mma_commit_w(&bar_m[role]);
+            __syncwarp();
         }
-        mbar_wait(&bar_m, i & 1);
-        tc_fence_after();
-        if (tid == 0 && i + 1 < NC) load_inputs(i + 1);   // every reader of the input tiles is done
-        partial_epilogue<K>(tdq, lane_base, lq, lane, warp, dqp + (size_t)vt * gridDim.y * T * K,
-                            (size_t)rowb + (size_t)i * CH);
-        tc_fence_before();
-        __syncthreads();
-    }
-    if (dfinal) {   // S_T . dS_T partial over this V tile
-        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tS + lane_base + c0, r);
-            tmem_wait_ld();
+    } else {
+        // ------------------------------------------------------------------ epilogue warps
+        const int et = tid - DC::NST - 96;
+        __nv_bfloat16* out = dqp + (size_t)vt * gridDim.y * T * K;
+        for (int i = 0; i < NC; ++i) {
+            const int b = i & 1;
+            wait_mmas(i & 1);
+            tc_fence_after();
+            if (et == 0 && i + 1 < NC) load_inputs(i + 1);   // every reader of the input tiles is done
+            const size_t row0 = (size_t)rowb + (size_t)i * CH;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                float x = __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E) * dfinal[((size_t)bh * K + c0 + j) * V + v0 + vrow];
+            for (int hh = 0; hh < K / 128; ++hh)
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-                if (lane == 0) red[lq * K + c0 + j] = x;
-            }
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t r[32];
+                    tmem_ld32(tdq + DC::DQB * b + 64 * hh + 32 * h + lane_base, r);
+                    tmem_wait_ld();
+                    const int ch = 128 * hh + vrow;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        out[(row0 + 32 * h + j) * K + ch] = __float2bfloat16_rn(__uint_as_float(r[j]));
+                }
+            tc_fence_before();
+            named_bar_sync(2, 128);
+            if (et == 0) mbar_arrive(&bar_efree[b]);
         }
-        __syncthreads();
-        for (int m = tid; m < K; m += NTH)
-            stdot[((size_t)vt * gridDim.y + bh) * K + m] = red[m] + red[K + m] + red[2 * K + m] + red[3 * K + m];
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem_base, 512);
+    if (warp == 0) tmem_dealloc(tmem_base, DC::TCOLS);
 }
 
 // Reverse walk with dH in TMEM: dv (final) and the dk partial of this V tile (+ intra term on V tile 0), dh0.
+// Warp roles (512 threads):
+//   warps 0-7   state pass dSB = bf16(dH_{i+1} e^{Gamma-r}) (smem, MN-major A operand of the dk MMAs),
+//               Z <- the same (TMEM); input loads; d log alpha anchors; dh0.
+//   warps 8-11  MMA issuers, one per independent accumulator stream (one thread issues at most one tcgen05.mma
+//               per ~110 cycles, profiles/r1_microbench.md):
+//                 8: dv^T_a = dSB[:, :K/2] K~[:, :K/2]^T + dO^T P          9: Z += dO^T Q~ ; dv^T_b = rest
+//                10: dk^T (channels 0-127) = dSB^T V^T (+ Q~^T dP)        11: dk^T (channels 128-255)
+//   warps 12-15 epilogue: dv = dv_a + dv_b -> bf16 -> TMA store; dk partial -> global.
 template <int K>
-__global__ void __launch_bounds__(NTH, 1)
+struct DkvCfg {
+    static constexpr int NST = 256, NTHR = 512;
+    static constexpr uint32_t COL_DK = K, COL_DVA = K + 64 * (K / 128), COL_DVB = COL_DVA + 64;
+    static constexpr uint32_t TCOLS = 512;
+    static_assert(COL_DVB + 64 <= TCOLS, "TMEM columns");
+};
+
+template <int K>
+__global__ void __launch_bounds__(DkvCfg<K>::NTHR, 1)
 k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmDP,
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
@@ -1012,6 +1099,7 @@ k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
            const __nv_bfloat16* __restrict__ anch, float* __restrict__ cpart, const int* __restrict__ flag, int T,
            int V) {
     using Cfg = BWalkCfg<K>;
+    using DC = DkvCfg<K>;
     if (*flag) return;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_align1k(smem_raw);
@@ -1027,13 +1115,19 @@ k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     float* fy = fsb + K;
     float* pend = fy + K;
     float* red = pend + K;
-    __shared__ uint64_t bar_in, bar_m;
+    __shared__ uint64_t bar_in, bar_sb, bar_m[4], bar_efree;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int vt = blockIdx.x, bh = blockIdx.y, v0 = vt * VT, NC = T / CH;
     const int rowb = bh * T;
     const bool intra = vt == 0;
     const uint32_t in_bytes = 2 * Cfg::OP + 32768 + 8192 + (intra ? 8192 : 0);
+#ifdef GLA_PHASE_TIMING
+    __shared__ long long trc[8][16];
+#define TRB(ev, i) do { const int _j = NC - 1 - (i); if (_j < 16) trc[ev][_j] = clock64(); } while (0)
+#else
+#define TRB(ev, i) do {} while (0)
+#endif
     auto load_inputs = [&](int i) {
         const int row = rowb + i * CH;
         mbar_expect_tx(&bar_in, in_bytes);
@@ -1048,151 +1142,246 @@ k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         tma_load_2d(sP, &tmP, &bar_in, 0, row);
         if (intra) tma_load_2d(sdP, &tmDP, &bar_in, 0, row);
     };
-    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    if (warp == 0) tmem_alloc(&tmem_base, DC::TCOLS);
     if (tid == 0) {
         mbar_init(&bar_in, 1);
-        mbar_init(&bar_m, 1);
+        mbar_init(&bar_sb, 1);
+        for (int j = 0; j < 4; ++j) mbar_init(&bar_m[j], 1);
+        mbar_init(&bar_efree, 1);
         fence_mbar_init();
         load_inputs(NC - 1);
     }
-    for (int m = tid; m < K; m += NTH) pend[m] = 0.f;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tZ = tmem_base, tdk = tmem_base + K, tdv = tmem_base + K + 128;
-    const int lq = warp & 3, half = warp >> 2;
+    const uint32_t tZ = tmem_base, tdk = tmem_base + DC::COL_DK;
+    const uint32_t tdva = tmem_base + DC::COL_DVA, tdvb = tmem_base + DC::COL_DVB;
+    const int lq = warp & 3;
     const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
     const int vrow = 32 * lq + lane;
-    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
-        uint32_t r[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            r[j] = __float_as_uint(dfinal ? dfinal[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
-        tmem_st32(tZ + lane_base + c0, r);
-    }
-    tmem_wait_st();
-    const uint32_t idZ = idesc_bf16(128, K, 1, 1);      // Z[v][ch] += dO^T Q~
-    const uint32_t idV1 = idesc_bf16(128, 64, 0, 0);    // dv^T = dSB K~^T
-    const uint32_t idV2 = idesc_bf16(128, 64, 1, 1);    // dv^T += dO^T P
-    const uint32_t idK1 = idesc_bf16(128, 64, 1, 0);    // dk^T = dSB^T V^T
-    const uint32_t idK2 = idesc_bf16(128, 64, 1, 1);    // dk^T += Q~^T dP
-    const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aSB = smem_u32(sSB), aV = smem_u32(sV), aD = smem_u32(sD),
-                   aP = smem_u32(sP), adP = smem_u32(sdP);
-    for (int i = NC - 1; i >= 0; --i) {
-        const uint32_t ph = (NC - 1 - i) & 1;
-        const int trow = rowb + i * CH;
-        if (tid < K) {   // dSB = bf16(dH_{i+1} e^{Gamma - r}); Z <- same; next pending = r
-            const float r_ = stats[((size_t)bh * NC + i) * 2 * K + tid], G_ = stats[((size_t)bh * NC + i) * 2 * K + K + tid];
-            fsb[tid] = ex2f((pend[tid] + G_ - r_) * L2E);
-            fy[tid] = fsb[tid];
-            pend[tid] = r_;
-        }
-        if (tid == 0 && i < NC - 1) tma_store_wait_read();   // dv staging of the previous chunk consumed
-        __syncthreads();
-        state_pass2<K>(tZ, lane_base, half, vrow, fsb, fy, sSB);
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-            mbar_wait(&bar_in, ph);
-            tc_fence_after();
-#pragma unroll
-            for (int kk = 0; kk < K / 16; ++kk) {   // dv^T = dSB K~^T (inter)
-                const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-                mma_bf16(tdv, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aK + ob, 16, 1024), idV1, kk > 0);
-            }
-#pragma unroll
-            for (int kk = 0; kk < CH / 16; ++kk)      // dv^T += dO^T P (intra)
-                mma_bf16(tdv, sdesc_sw128(aD + kk * 2048, 8192, 1024), sdesc_sw128(aP + kk * 2048, 8192, 1024), idV2, 1);
-#pragma unroll
-            for (int hh = 0; hh < K / 128; ++hh) {
-#pragma unroll
-                for (int kk = 0; kk < VT / 16; ++kk) {   // dk^T = dSB^T V^T (inter, this V tile)
-                    const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-                    mma_bf16(tdk + 64 * hh, sdesc_sw128(aSB + 2 * hh * 16384 + kk * 2048, 16384, 1024),
-                             sdesc_sw128(aV + ob, 16, 1024), idK1, kk > 0);
-                }
-                if (intra)
-#pragma unroll
-                    for (int kk = 0; kk < CH / 16; ++kk)   // + Q~^T dP (the full intra term, V tile 0 only)
-                        mma_bf16(tdk + 64 * hh, sdesc_sw128(aQ + 2 * hh * 8192 + kk * 2048, 8192, 1024),
-                                 sdesc_sw128(adP + kk * 2048, 8192, 1024), idK2, 1);
-            }
-#pragma unroll
-            for (int kk = 0; kk < CH / 16; ++kk)      // Z += dO^T Q~ (reverse state pass)
-                mma_bf16(tZ, sdesc_sw128(aD + kk * 2048, 8192, 1024), sdesc_sw128(aQ + kk * 2048, 8192, 1024), idZ, 1);
-            mma_commit(&bar_m);
-        }
-        mbar_wait(&bar_m, ph);
-        tc_fence_after();
-        if (tid == 0 && i > 0) load_inputs(i - 1);
-        {
+    auto wait_mmas = [&](uint32_t ph) {
+        for (int j = 0; j < 4; ++j) mbar_wait(&bar_m[j], ph);
+    };
+
+    if (warp < 8) {
+        // ------------------------------------------------------------------ state warps
+        const int half = warp >> 2;
+        for (int m = tid; m < K; m += DC::NST) pend[m] = 0.f;
+        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
             uint32_t r[32];
-            tmem_ld32(tdv + lane_base + 32 * half, r);
-            tmem_wait_ld();
-            uint8_t* dst = stg + (vrow >> 6) * 8192 + (vrow & 63) * 2;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-                *reinterpret_cast<__nv_bfloat16*>(dst + (32 * half + j) * 128) = __float2bfloat16_rn(__uint_as_float(r[j]));
+                r[j] = __float_as_uint(dfinal ? dfinal[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
+            tmem_st32(tZ + lane_base + c0, r);
         }
-        partial_epilogue<K>(tdk, lane_base, lq, lane, warp, dkp + (size_t)vt * gridDim.y * T * K, (size_t)trow);
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            tma_store_2d(&tmDV, stg, v0, trow);
-            tma_store_2d(&tmDV, stg + 8192, v0 + 64, trow);
-            tma_store_commit();
+        tmem_wait_st();
+        float st_r = 0.f, st_G = 0.f;          // per-chunk statistics, one chunk ahead
+        if (tid < K) {
+            st_r = stats[((size_t)bh * NC + NC - 1) * 2 * K + tid];
+            st_G = stats[((size_t)bh * NC + NC - 1) * 2 * K + K + tid];
         }
-        if (i > 0 && i % ANCH == 0) {   // exact carry at boundary i over this V tile (see k_bwd_dkv)
-            const __nv_bfloat16* arow = anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K;
+        named_bar_sync(1, DC::NST);
+        for (int i = NC - 1; i >= 0; --i) {
+            if (tid < K) {   // dSB = bf16(dH_{i+1} e^{Gamma - r}); Z <- same; next pending = r
+                const float r_ = st_r, G_ = st_G;
+                if (i > 0) {
+                    st_r = stats[((size_t)bh * NC + i - 1) * 2 * K + tid];
+                    st_G = stats[((size_t)bh * NC + i - 1) * 2 * K + K + tid];
+                }
+                fsb[tid] = ex2f((pend[tid] + G_ - r_) * L2E);
+                fy[tid] = fsb[tid];
+                pend[tid] = r_;
+            }
+            if (i < NC - 1) {                  // every MMA of chunk i+1 has completed
+                const int bd = i + 1;          // exact d log alpha carry at boundary bd over this V tile
+                const bool anc = bd % ANCH == 0;
+                const __nv_bfloat16* arow = anch + (((size_t)(bd / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K;
+                uint4 hv[2][4];
+                if (anc)                       // first two anchor slices in flight while the MMAs finish
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            hv[h2][u] = __ldg(reinterpret_cast<const uint4*>(arow + half * (K / 2) + 32 * h2 + 8 * u));
+                wait_mmas((NC - 2 - i) & 1);
+                tc_fence_after();
+                if (tid == 0) TRB(0, i);
+                if (anc) {
+#pragma unroll
+                    for (int sl = 0; sl < K / 64; ++sl) {
+                        const int c0 = half * (K / 2) + 32 * sl;
+                        uint32_t r[32];
+                        tmem_ld32(tZ + lane_base + c0, r);
+                        uint4 hcur[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) hcur[u] = hv[sl & 1][u];
+                        if (sl + 2 < K / 64)           // slice sl+2 into the freed registers
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                hv[sl & 1][u] = __ldg(reinterpret_cast<const uint4*>(arow + c0 + 64 + 8 * u));
+                        uint4* hvp = hcur;
+                        tmem_wait_ld();
+                        float x[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const uint32_t w = word(hvp[j >> 3], (j & 7) >> 1);
+                            x[j] = ((j & 1) ? bf16hi(w) : bf16lo(w)) * __uint_as_float(r[j]);
+                        }
+#pragma unroll
+                        for (int o = 16; o >= 1; o >>= 1) {
+                            const bool up = (lane & o) != 0;
+#pragma unroll
+                            for (int j = 0; j < o; ++j) {
+                                const float send = up ? x[j] : x[j + o];
+                                const float keep = up ? x[j + o] : x[j];
+                                x[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                            }
+                        }
+                        red[lq * K + c0 + lane] = x[0];
+                    }
+                    named_bar_sync(1, DC::NST);
+                    for (int m = tid; m < K; m += DC::NST)
+                        cpart[(((size_t)(bd / ANCH - 1) * gridDim.x + vt) * gridDim.y + bh) * K + m] =
+                            red[m] + red[K + m] + red[2 * K + m] + red[3 * K + m];
+                }
+            }
+            named_bar_sync(1, DC::NST);        // fsb / fy visible; red consumed
+            if (tid == 0) TRB(1, i);
+            state_pass2<K>(tZ, lane_base, half, vrow, fsb, fy, sSB);
+            fence_async_smem();
+            tc_fence_before();
+            named_bar_sync(1, DC::NST);
+            if (tid == 0) { TRB(2, i); mbar_arrive(&bar_sb); }
+        }
+        wait_mmas((NC - 1) & 1);
+        tc_fence_after();
+        if (dh0) {
             for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
                 uint32_t r[32];
                 tmem_ld32(tZ + lane_base + c0, r);
-                uint4 hv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) hv[u] = __ldg(reinterpret_cast<const uint4*>(arow + c0 + 8 * u));
                 tmem_wait_ld();
-                float x[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const uint32_t w = word(hv[j >> 3], (j & 7) >> 1);
-                    x[j] = ((j & 1) ? bf16hi(w) : bf16lo(w)) * __uint_as_float(r[j]);
-                }
-#pragma unroll
-                for (int o = 16; o >= 1; o >>= 1) {
-                    const bool up = (lane & o) != 0;
-#pragma unroll
-                    for (int j = 0; j < o; ++j) {
-                        const float send = up ? x[j] : x[j + o];
-                        const float keep = up ? x[j + o] : x[j];
-                        x[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-                    }
-                }
-                red[lq * K + c0 + lane] = x[0];
+                for (int j = 0; j < 32; ++j)
+                    dh0[((size_t)bh * K + c0 + j) * V + v0 + vrow] = __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E);
             }
-            __syncthreads();
-            for (int m = tid; m < K; m += NTH)
-                cpart[(((size_t)(i / ANCH - 1) * gridDim.x + vt) * gridDim.y + bh) * K + m] =
-                    red[m] + red[K + m] + red[2 * K + m] + red[3 * K + m];
-            __syncthreads();
         }
-    }
-    if (dh0) {
-        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tZ + lane_base + c0, r);
-            tmem_wait_ld();
+    } else if (warp < 12) {
+        // ------------------------------------------------------------------ MMA issuers
+        const int role = warp - 8;
+        const uint32_t idZ = idesc_bf16(128, K, 1, 1);      // Z[v][ch] += dO^T Q~
+        const uint32_t idV1 = idesc_bf16(128, 64, 0, 0);    // dv^T = dSB K~^T
+        const uint32_t idV2 = idesc_bf16(128, 64, 1, 1);    // dv^T += dO^T P
+        const uint32_t idK1 = idesc_bf16(128, 64, 1, 0);    // dk^T = dSB^T V^T
+        const uint32_t idK2 = idesc_bf16(128, 64, 1, 1);    // dk^T += Q~^T dP
+        const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aSB = smem_u32(sSB), aV = smem_u32(sV), aD = smem_u32(sD),
+                       aP = smem_u32(sP), adP = smem_u32(sdP);
+        for (int i = NC - 1; i >= 0; --i) {
+            const uint32_t ph = (NC - 1 - i) & 1;
+            mbar_wait(&bar_sb, ph);
+            mbar_wait(&bar_in, ph);
+            if (i < NC - 1) mbar_wait(&bar_efree, (NC - 2 - i) & 1);
+            tc_fence_after();
+            if (lane == 0 && role == 0) TRB(3, i);
+            if (role == 0) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-                dh0[((size_t)bh * K + c0 + j) * V + v0 + vrow] = __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E);
+                for (int kk = 0; kk < K / 32; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+                    mma_bf16_w(tdva, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aK + ob, 16, 1024), idV1, kk > 0);
+                }
+#pragma unroll
+                for (int kk = 0; kk < CH / 16; ++kk)
+                    mma_bf16_w(tdva, sdesc_sw128(aD + kk * 2048, 8192, 1024), sdesc_sw128(aP + kk * 2048, 8192, 1024), idV2, 1);
+            } else if (role == 1) {
+#pragma unroll
+                for (int kk = 0; kk < CH / 16; ++kk)
+                    mma_bf16_w(tZ, sdesc_sw128(aD + kk * 2048, 8192, 1024), sdesc_sw128(aQ + kk * 2048, 8192, 1024), idZ, 1);
+#pragma unroll
+                for (int kk = K / 32; kk < K / 16; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+                    mma_bf16_w(tdvb, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aK + ob, 16, 1024), idV1, kk > K / 32);
+                }
+            } else if (role - 2 < K / 128) {
+                const int hh = role - 2;
+#pragma unroll
+                for (int kk = 0; kk < VT / 16; ++kk) {
+                    const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+                    mma_bf16_w(tdk + 64 * hh, sdesc_sw128(aSB + 2 * hh * 16384 + kk * 2048, 16384, 1024),
+                               sdesc_sw128(aV + ob, 16, 1024), idK1, kk > 0);
+                }
+                if (intra)
+#pragma unroll
+                    for (int kk = 0; kk < CH / 16; ++kk)
+                        mma_bf16_w(tdk + 64 * hh, sdesc_sw128(aQ + 2 * hh * 8192 + kk * 2048, 8192, 1024),
+                                   sdesc_sw128(adP + kk * 2048, 8192, 1024), idK2, 1);
+            }
+            mma_commit_w(&bar_m[role]);
+            if (lane == 0 && role == 0) TRB(4, i);
+            __syncwarp();
         }
+    } else {
+        // ------------------------------------------------------------------ epilogue warps
+        const int et = tid - DC::NST - 128;
+        for (int i = NC - 1; i >= 0; --i) {
+            const uint32_t ph = (NC - 1 - i) & 1;
+            const int trow = rowb + i * CH;
+            wait_mmas(ph);
+            tc_fence_after();
+            if (et == 0) {
+                TRB(5, i);
+                if (i > 0) load_inputs(i - 1); // every reader of the input tiles (the MMAs of chunk i) is done
+                tma_store_wait_read();         // dv staging of the previous chunk consumed
+            }
+            named_bar_sync(2, 128);
+            uint8_t* dst = stg + (vrow >> 6) * 8192 + (vrow & 63) * 2;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint32_t ra[32], rb[32];
+                tmem_ld32(tdva + 32 * h + lane_base, ra);
+                tmem_ld32(tdvb + 32 * h + lane_base, rb);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    *reinterpret_cast<__nv_bfloat16*>(dst + (32 * h + j) * 128) =
+                        __float2bfloat16_rn(__uint_as_float(ra[j]) + __uint_as_float(rb[j]));
+            }
+            __nv_bfloat16* out = dkp + (size_t)vt * gridDim.y * T * K;
+#pragma unroll
+            for (int hh = 0; hh < K / 128; ++hh)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t r[32];
+                    tmem_ld32(tdk + 64 * hh + 32 * h + lane_base, r);
+                    tmem_wait_ld();
+                    const int ch = 128 * hh + vrow;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        out[((size_t)trow + 32 * h + j) * K + ch] = __float2bfloat16_rn(__uint_as_float(r[j]));
+                }
+            tc_fence_before();
+            fence_async_smem();
+            named_bar_sync(2, 128);
+            if (et == 0) {
+                TRB(6, i);
+                mbar_arrive(&bar_efree);
+                tma_store_2d(&tmDV, stg, v0, trow);
+                tma_store_2d(&tmDV, stg + 8192, v0 + 64, trow);
+                tma_store_commit();
+            }
+        }
+        if (et == 0) tma_store_wait_all();
     }
-    if (tid == 0) tma_store_wait_all();
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem_base, 512);
+#ifdef GLA_PHASE_TIMING
+    if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+        const long long t0 = trc[2][0];
+        printf("bwd_dkv trace: S0=mmas(i+1) seen S1=pass start S2=pass done M0=issue start M1=issued E0=mmas seen E1=epi done\n");
+        for (int j = 1; j < 16 && j < NC; ++j)
+            printf("  step %2d: S0 %7lld S1 %7lld S2 %7lld M0 %7lld M1 %7lld E0 %7lld E1 %7lld\n", j, trc[0][j] - t0,
+                   trc[1][j] - t0, trc[2][j] - t0, trc[3][j] - t0, trc[4][j] - t0, trc[5][j] - t0, trc[6][j] - t0);
+    }
+#endif
+    if (warp == 0) tmem_dealloc(tmem_base, DC::TCOLS);
 }
 
 // ---------------------------------------------------------------------------------------------------------------
@@ -1330,12 +1519,12 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     const dim3 grid(NVT, BH);
     {
         GLA_PROF("tc::bwd_dq", st);
-        k_bwd_dq2<K><<<grid, NTH, BWalkCfg<K>::SMEM, st>>>(mK, mDP, mV, mD, stats, p.h0, p.dfinal, dqp,
+        k_bwd_dq2<K><<<grid, DqCfg<K>::NTHR, BWalkCfg<K>::SMEM, st>>>(mK, mDP, mV, mD, stats, p.h0, p.dfinal, dqp,
                                                             p.dfinal ? stdot : nullptr, anch, flag, p.T, p.V);
     }
     {
         GLA_PROF("tc::bwd_dkv", st);
-        k_bwd_dkv2<K><<<grid, NTH, BWalkCfg<K>::SMEM, st>>>(mQ, mK, mP, mDP, mV, mD, mDV, stats, p.dfinal, dkp, p.dh0,
+        k_bwd_dkv2<K><<<grid, DkvCfg<K>::NTHR, BWalkCfg<K>::SMEM, st>>>(mQ, mK, mP, mDP, mV, mD, mDV, stats, p.dfinal, dkp, p.dh0,
                                                              anch, cpart, flag, p.T, p.V);
     }
     {

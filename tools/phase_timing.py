@@ -1,4 +1,5 @@
-"""Runs the forward once with the -DGLA_PHASE_TIMING build (libgla_timing.so) to print per-phase cycles."""
+"""Runs the forward and backward once with the -DGLA_PHASE_TIMING build (libgla_timing.so): the walk kernels
+print per-chunk event traces (clock64 cycles) of CTA (0,0)."""
 import os
 import sys
 
@@ -13,6 +14,9 @@ import synth  # noqa: E402
 CFG = {"1p3b": (16, 4, 2048, 256, 512), "340m": (8, 4, 2048, 128, 256)}
 B, H, T, K, V = CFG[sys.argv[1] if len(sys.argv) > 1 else "1p3b"]
 p = synth.problem(B, H, T, K, V, seed=1)
-q, k, v, g = (p[n].cuda() for n in ("q", "k", "v", "g"))
+q, k, v, g, do = (p[n].cuda() for n in ("q", "k", "v", "g", "do"))
 G.chunk_fwd(q, k, v, g, 64, 16)
 torch.cuda.synchronize()
+if "--bwd" in sys.argv:
+    G.chunk_bwd(q, k, v, g, do, 64, 16)
+    torch.cuda.synchronize()
