@@ -37,7 +37,7 @@ constexpr int VT = 128;
 constexpr int NTH = 256;
 constexpr float L2E = 1.4426950408889634f;
 constexpr float GUARD = 60.f;
-constexpr int ANCH = 4;   // d log alpha carry re-anchored from exact states every ANCH chunks
+constexpr int ANCH = 8;   // d log alpha carry re-anchored from exact states every ANCH chunks
 }  // namespace
 
 template <int K>
