@@ -24,6 +24,16 @@ cudaError_t bwd_tc(const BwdProblem& p, cudaStream_t st);
 size_t bwd_tc_ws(int B, int H, int T, int K, int V, int C);
 bool bwd_tc_supported(int K, int V);
 
+int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
 bool supported(int B, int H, int T, int K, int V, int C, int c, int qkv_dtype, int gate_dtype) {
     (void)B; (void)H; (void)T; (void)gate_dtype;
     return qkv_dtype == 0 && (K == 64 || K == 128 || K == 256) && V % 128 == 0 && C == 64 && c > 0 && 64 % c == 0;

@@ -14,6 +14,8 @@ cudaError_t bwd(const BwdProblem& p, cudaStream_t st);
 size_t fwd_ws(int B, int H, int T, int K, int V, int C);
 size_t bwd_ws(int B, int H, int T, int K, int V, int C);
 // 2-D bf16 TMA map over a [rows][cols] row-major tensor, box {64 cols, 64 rows}, optional 128B swizzle.
+// Number of SMs of the current device (cached; persistent kernels size their grids with it).
+int num_sms();
 cudaError_t make_map_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, bool swizzle);
 }  // namespace tc
 }  // namespace gla

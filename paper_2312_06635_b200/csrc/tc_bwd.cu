@@ -691,13 +691,16 @@ struct BPrepCfg {
     static_assert(SMEM <= 232448, "dynamic shared memory");
 };
 
+// Persistent like k_fwd_prep: CTA c processes work items (b,h, chunk) c, c + gridDim.x, ...; the next item's
+// q / k / log alpha go into the dead operand registers after the build, and its first dO / V round is loaded
+// by TMA while this item's epilogue runs.
 template <int K, typename TG>
 __global__ void __launch_bounds__(NTH, 1)
 k_bwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmDP,
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
            const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g,
-           float* __restrict__ stats, int* __restrict__ flag, int T, int V) {
+           float* __restrict__ stats, int* __restrict__ flag, int T, int V, int NC, int nitems) {
     using Cfg = BPrepCfg<K>;
     using Tl = typename Cfg::Tl;
     extern __shared__ uint8_t smem_raw[];
@@ -712,150 +715,161 @@ k_bwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     __shared__ uint64_t bar_in, bar_m, bar_done;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int chunk = blockIdx.x, bh = blockIdx.y, NC = gridDim.x;
     const int oc = tid % Tl::NOCT, rg = tid / Tl::NOCT;
     const int ch0 = 8 * oc, row0 = rg * Tl::RPG;
-    const size_t crow = (size_t)bh * T + (size_t)chunk * CH;
     const int VR = V < 256 ? V : 256, NR = V / VR, NBX = VR / 64;   // V rounds of VR columns (NBX boxes)
+    auto crow_of = [&](int it) { return (size_t)(it / NC) * T + (size_t)(it % NC) * CH; };
+    auto load_round = [&](int it, int rd) {
+        const int row = (int)crow_of(it);
+        mbar_expect_tx(&bar_in, 2 * NBX * 8192);
+        for (int b = 0; b < NBX; ++b) {
+            tma_load_2d(sD + b * 8192, &tmD, &bar_in, rd * VR + 64 * b, row);
+            tma_load_2d(sV + b * 8192, &tmV, &bar_in, rd * VR + 64 * b, row);
+        }
+    };
 
     if (warp == 0) tmem_alloc(&tmem_base, 256);
+    int item = blockIdx.x;
     if (tid == 0) {
         mbar_init(&bar_in, 1);
         mbar_init(&bar_m, 1);
         mbar_init(&bar_done, 1);
         fence_mbar_init();
-        mbar_expect_tx(&bar_in, 2 * NBX * 8192);
-        for (int b = 0; b < NBX; ++b) {
-            tma_load_2d(sD + b * 8192, &tmD, &bar_in, 64 * b, (int)crow);
-            tma_load_2d(sV + b * 8192, &tmV, &bar_in, 64 * b, (int)crow);
-        }
+        if (item < nitems) load_round(item, 0);
     }
     ChunkRegs<K> R;
-    load_chunk<K, TG, true, true>(R, q, k, g, crow, row0, ch0);
+    if (item < nitems) load_chunk<K, TG, true, true>(R, q, k, g, crow_of(item), row0, ch0);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tP = tmem_base, tdP = tmem_base + 128;
-
-    float2 off[4], rr[4], Gm[4];
-    chunk_cumsum<K>(R, exch, rg, ch0, off, rr, Gm);
-    bool bad = false;
-    if (rg == 0)
+    uint32_t in_cnt = 0, m_cnt = 0, done_ph = 0;
+    for (; item < nitems; item += gridDim.x, done_ph ^= 1) {
+        const int chunk = item % NC, bh = item / NC;
+        const size_t crow = crow_of(item);
+        if (tid == 0) tma_store_wait_read();    // the previous item's stores have read their smem
+        float2 off[4], rr[4], Gm[4];
+        chunk_cumsum<K>(R, exch, rg, ch0, off, rr, Gm);
+        bool bad = false;
+        if (rg == 0)
 #pragma unroll
-        for (int p = 0; p < 4; ++p)
-            bad |= (-rr[p].x > GUARD) | (-rr[p].y > GUARD) | (rr[p].x - Gm[p].x > GUARD) | (rr[p].y - Gm[p].y > GUARD);
-    if (__syncthreads_or(bad) && tid == 0) atomicOr(flag, 1);   // whole call -> exact CUDA-core kernels
-    if (rg == 0) {
-        float* st = stats + ((size_t)bh * NC + chunk) * 2 * K + ch0;
-        reinterpret_cast<float4*>(st)[0] = make_float4(rr[0].x, rr[0].y, rr[1].x, rr[1].y);
-        reinterpret_cast<float4*>(st)[1] = make_float4(rr[2].x, rr[2].y, rr[3].x, rr[3].y);
-        reinterpret_cast<float4*>(st + K)[0] = make_float4(Gm[0].x, Gm[0].y, Gm[1].x, Gm[1].y);
-        reinterpret_cast<float4*>(st + K)[1] = make_float4(Gm[2].x, Gm[2].y, Gm[3].x, Gm[3].y);
-    }
-    float2 refq[4], refk[4];
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-        refq[p] = make_float2(-L2E * rr[p].x, -L2E * rr[p].y);
-        refk[p] = make_float2(L2E * rr[p].x, L2E * rr[p].y);
-    }
-    const int blk = ch0 >> 6, col = ch0 & 63;
-    uint8_t* qb = sQ + blk * 16384;
-    uint8_t* kb = sK + blk * 16384;
-#pragma unroll
-    for (int r = 0; r < Tl::RPG; ++r) {
-        const int t = row0 + r;
-        float2 b[4];
-#pragma unroll
-        for (int p = 0; p < 4; ++p) b[p] = add2(R.g[r][p], off[p]);
-        scaled_row(R.q[r], b, refq, 1.f, qb + sw128_off(t, col), qb + sw128_off(64 + t, col));
-        scaled_row(R.k[r], b, refk, -1.f, kb + sw128_off(t, col), kb + sw128_off(64 + t, col));
-    }
-    fence_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-        tc_fence_after();
-        const uint32_t idPs = idesc_bf16(128, 128, 0, 0), idDP = idesc_bf16(64, 64, 0, 0);
-        const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aD = smem_u32(sD), aV = smem_u32(sV);
-#pragma unroll
-        for (int kk = 0; kk < K / 16; ++kk) {   // P: [Q~hi; Q~lo] [K~hi; K~lo]^T
-            const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-            mma_bf16(tP, sdesc_sw128(aQ + o, 16, 1024), sdesc_sw128(aK + o, 16, 1024), idPs, kk > 0);
+            for (int p = 0; p < 4; ++p)
+                bad |= (-rr[p].x > GUARD) | (-rr[p].y > GUARD) | (rr[p].x - Gm[p].x > GUARD) | (rr[p].y - Gm[p].y > GUARD);
+        if (__syncthreads_or(bad) && tid == 0) atomicOr(flag, 1);   // whole call -> exact CUDA-core kernels
+        if (rg == 0) {
+            float* st = stats + ((size_t)bh * NC + chunk) * 2 * K + ch0;
+            reinterpret_cast<float4*>(st)[0] = make_float4(rr[0].x, rr[0].y, rr[1].x, rr[1].y);
+            reinterpret_cast<float4*>(st)[1] = make_float4(rr[2].x, rr[2].y, rr[3].x, rr[3].y);
+            reinterpret_cast<float4*>(st + K)[0] = make_float4(Gm[0].x, Gm[0].y, Gm[1].x, Gm[1].y);
+            reinterpret_cast<float4*>(st + K)[1] = make_float4(Gm[2].x, Gm[2].y, Gm[3].x, Gm[3].y);
         }
-        for (int c = 0; c < K / 64; ++c) {     // Q~hi, K~hi -> HBM for the V-tiled walks
-            tma_store_2d(&tmQ, sQ + c * 16384, 64 * c, (int)crow);
-            tma_store_2d(&tmK, sK + c * 16384, 64 * c, (int)crow);
+        float2 refq[4], refk[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            refq[p] = make_float2(-L2E * rr[p].x, -L2E * rr[p].y);
+            refk[p] = make_float2(L2E * rr[p].x, L2E * rr[p].y);
         }
-        tma_store_commit();
-        for (int rd = 0; rd < NR; ++rd) {      // dP = dO V^T over the full V, VR columns per round
-            mbar_wait(&bar_in, rd & 1);
+        const int blk = ch0 >> 6, col = ch0 & 63;
+        uint8_t* qb = sQ + blk * 16384;
+        uint8_t* kb = sK + blk * 16384;
+#pragma unroll
+        for (int r = 0; r < Tl::RPG; ++r) {
+            const int t = row0 + r;
+            float2 b[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) b[p] = add2(R.g[r][p], off[p]);
+            scaled_row(R.q[r], b, refq, 1.f, qb + sw128_off(t, col), qb + sw128_off(64 + t, col));
+            scaled_row(R.k[r], b, refk, -1.f, kb + sw128_off(t, col), kb + sw128_off(64 + t, col));
+        }
+        {   // next item's q / k / log alpha into the dead operand registers
+            const int nx = item + gridDim.x;
+            if (nx < nitems) load_chunk<K, TG, true, true>(R, q, k, g, crow_of(nx), row0, ch0);
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
             tc_fence_after();
-            for (int kk = 0; kk < VR / 16; ++kk) {
-                const uint32_t o = (kk >> 2) * 8192 + (kk & 3) * 32;
-                mma_bf16(tdP, sdesc_sw128(aD + o, 16, 1024), sdesc_sw128(aV + o, 16, 1024), idDP, (rd | kk) > 0);
+            const uint32_t idPs = idesc_bf16(128, 128, 0, 0), idDP = idesc_bf16(64, 64, 0, 0);
+            const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aD = smem_u32(sD), aV = smem_u32(sV);
+#pragma unroll
+            for (int kk = 0; kk < K / 16; ++kk) {   // P: [Q~hi; Q~lo] [K~hi; K~lo]^T
+                const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                mma_bf16(tP, sdesc_sw128(aQ + o, 16, 1024), sdesc_sw128(aK + o, 16, 1024), idPs, kk > 0);
             }
-            if (rd + 1 < NR) {
-                mma_commit(&bar_m);
-                mbar_wait(&bar_m, rd & 1);   // the MMAs have consumed this round's tiles
-                mbar_expect_tx(&bar_in, 2 * NBX * 8192);
-                for (int b = 0; b < NBX; ++b) {
-                    tma_load_2d(sD + b * 8192, &tmD, &bar_in, (rd + 1) * VR + 64 * b, (int)crow);
-                    tma_load_2d(sV + b * 8192, &tmV, &bar_in, (rd + 1) * VR + 64 * b, (int)crow);
+            for (int c = 0; c < K / 64; ++c) {     // Q~hi, K~hi -> HBM for the V-tiled walks
+                tma_store_2d(&tmQ, sQ + c * 16384, 64 * c, (int)crow);
+                tma_store_2d(&tmK, sK + c * 16384, 64 * c, (int)crow);
+            }
+            tma_store_commit();
+            for (int rd = 0; rd < NR; ++rd) {      // dP = dO V^T over the full V, VR columns per round
+                mbar_wait(&bar_in, (in_cnt++) & 1);
+                tc_fence_after();
+                for (int kk = 0; kk < VR / 16; ++kk) {
+                    const uint32_t o = (kk >> 2) * 8192 + (kk & 3) * 32;
+                    mma_bf16(tdP, sdesc_sw128(aD + o, 16, 1024), sdesc_sw128(aV + o, 16, 1024), idDP, (rd | kk) > 0);
+                }
+                if (rd + 1 < NR) {
+                    mma_commit(&bar_m);
+                    mbar_wait(&bar_m, (m_cnt++) & 1);   // the MMAs have consumed this round's tiles
+                    load_round(item, rd + 1);
                 }
             }
+            mma_commit(&bar_done);
         }
-        mma_commit(&bar_done);
-    }
-    mbar_wait(&bar_done, 0);   // one-shot barrier: every MMA of this CTA has completed
-    tc_fence_after();
-    const int lq = warp & 3, half = warp >> 2;
-    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
-    const int vrow = 32 * lq + lane;
-    // dP (M=64 layout) -> causal bf16 [t][s]; the lo-row warps of P run the P exchange meanwhile
-    if (half == 1) m64_epilogue(tdP, lane_base, lq, lane, sdP);
-    if (lq >= 2 && half == 0) {
-        for (int hc = 0; hc < 2; ++hc) {
+        mbar_wait(&bar_done, done_ph);   // every MMA of this item has completed
+        tc_fence_after();
+        if (tid == 0 && item + (int)gridDim.x < nitems) load_round(item + gridDim.x, 0);   // overlaps the epilogue
+        const int lq = warp & 3, half = warp >> 2;
+        const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
+        const int vrow = 32 * lq + lane;
+        // dP (M=64 layout) -> causal bf16 [t][s]; the lo-row warps of P run the P exchange meanwhile
+        if (half == 1) m64_epilogue(tdP, lane_base, lq, lane, sdP);
+        if (lq >= 2 && half == 0) {
+            for (int hc = 0; hc < 2; ++hc) {
+                uint32_t a[32], b[32];
+                tmem_ld32(tP + lane_base + 32 * hc, a);
+                tmem_ld32(tP + lane_base + 64 + 32 * hc, b);
+                tmem_wait_ld();
+                const int t = vrow - 64;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    exch[t * 64 + ((32 * hc + j + t) & 63)] = __uint_as_float(a[j]) + __uint_as_float(b[j]);
+            }
+        }
+        __syncthreads();
+        if (lq < 2) {
             uint32_t a[32], b[32];
-            tmem_ld32(tP + lane_base + 32 * hc, a);
-            tmem_ld32(tP + lane_base + 64 + 32 * hc, b);
+            tmem_ld32(tP + lane_base + 32 * half, a);
+            tmem_ld32(tP + lane_base + 64 + 32 * half, b);
             tmem_wait_ld();
-            const int t = vrow - 64;
+            const int t = vrow;
+            uint32_t pk[16];
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-                exch[t * 64 + ((32 * hc + j + t) & 63)] = __uint_as_float(a[j]) + __uint_as_float(b[j]);
+            for (int j = 0; j < 32; j += 2) {
+                const int s_ = 32 * half + j;
+                float p0 = __uint_as_float(a[j]) + __uint_as_float(b[j]) + exch[t * 64 + ((s_ + t) & 63)];
+                float p1 = __uint_as_float(a[j + 1]) + __uint_as_float(b[j + 1]) + exch[t * 64 + ((s_ + 1 + t) & 63)];
+                pk[j / 2] = pack_bf16(s_ <= t ? p0 : 0.f, s_ + 1 <= t ? p1 : 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                *reinterpret_cast<uint4*>(sP + sw128_off(t, 32 * half + 8 * u)) =
+                    make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();                         // P, dP staged; TMEM drained; exch free
+        if (tid == 0) {
+            tma_store_2d(&tmP, sP, 0, (int)crow);
+            tma_store_2d(&tmDP, sdP, 0, (int)crow);
+            tma_store_commit();
         }
     }
-    __syncthreads();
-    if (lq < 2) {
-        uint32_t a[32], b[32];
-        tmem_ld32(tP + lane_base + 32 * half, a);
-        tmem_ld32(tP + lane_base + 64 + 32 * half, b);
-        tmem_wait_ld();
-        const int t = vrow;
-        uint32_t pk[16];
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-            const int s = 32 * half + j;
-            float p0 = __uint_as_float(a[j]) + __uint_as_float(b[j]) + exch[t * 64 + ((s + t) & 63)];
-            float p1 = __uint_as_float(a[j + 1]) + __uint_as_float(b[j + 1]) + exch[t * 64 + ((s + 1 + t) & 63)];
-            pk[j / 2] = pack_bf16(s <= t ? p0 : 0.f, s + 1 <= t ? p1 : 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            *reinterpret_cast<uint4*>(sP + sw128_off(t, 32 * half + 8 * u)) =
-                make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-    }
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-        tma_store_2d(&tmP, sP, 0, (int)crow);
-        tma_store_2d(&tmDP, sdP, 0, (int)crow);
-        tma_store_commit();
-        tma_store_wait_all();
-    }
+    if (tid == 0) tma_store_wait_all();
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc(tP, 256);
+    if (warp == 0) tmem_dealloc(tmem_base, 256);
 }
 
 template <int K>
@@ -1512,9 +1526,10 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         return e;
     {
         GLA_PROF("tc::bwd_prep", st);
-        k_bwd_prep<K, TG><<<dim3(NC, BH), NTH, BPrepCfg<K>::SMEM, st>>>(
+        const int nitems = NC * BH;
+        k_bwd_prep<K, TG><<<(unsigned)(nitems < num_sms() ? nitems : num_sms()), NTH, BPrepCfg<K>::SMEM, st>>>(
             mQ, mK, mP, mDP, mV, mD, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k, (const TG*)p.g, stats, flag,
-            p.T, p.V);
+            p.T, p.V, NC, nitems);
     }
     const dim3 grid(NVT, BH);
     {

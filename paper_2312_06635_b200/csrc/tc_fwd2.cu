@@ -47,12 +47,16 @@ struct PrepCfg {
     static_assert(Tl::RG * K * 4 <= 16384, "gtot fits the exchange buffer");
 };
 
+// Persistent: CTA c processes work items (b,h, chunk) c, c + gridDim.x, ...  The next item's q / k / log alpha
+// are loaded into the (then dead) operand registers right after the current item's operand build, so their
+// HBM latency overlaps this item's P MMA, epilogue and stores (one CTA per SM: the kernel is register- and
+// shared-memory-heavy, so the overlap has to come from within the CTA).
 template <int K, typename TG>
 __global__ void __launch_bounds__(NTH, 1)
 k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmP, const __nv_bfloat16* __restrict__ q,
            const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g, float* __restrict__ stats,
-           int* __restrict__ flags, float* __restrict__ bws, int T) {
+           int* __restrict__ flags, float* __restrict__ bws, int T, int NC, int nitems) {
     using Cfg = PrepCfg<K>;
     using Tl = typename Cfg::Tl;
     extern __shared__ uint8_t smem_raw[];
@@ -65,146 +69,157 @@ k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     __shared__ uint64_t bar;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int chunk = blockIdx.x, bh = blockIdx.y, NC = gridDim.x;
     const int oc = tid % Tl::NOCT, rg = tid / Tl::NOCT;
     const int ch0 = 8 * oc, row0 = rg * Tl::RPG;
-    const size_t crow = (size_t)bh * T + (size_t)chunk * CH;
 
     if (warp == 0) tmem_alloc(&tmem_base, 128);
     if (tid == 0) {
         mbar_init(&bar, 1);
         fence_mbar_init();
+        prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmP);
     }
     ChunkRegs<K> R;
-    load_chunk<K, TG, true, true>(R, q, k, g, crow, row0, ch0);
+    int item = blockIdx.x;
+    if (item < nitems)
+        load_chunk<K, TG, true, true>(R, q, k, g, (size_t)(item / NC) * T + (size_t)(item % NC) * CH, row0, ch0);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tP = tmem_base;
-
-    float2 off[4], rr[4], Gm[4];
-    chunk_cumsum<K>(R, gtot, rg, ch0, off, rr, Gm);
-    bool bad = false;
-    if (rg == 0)
+    uint32_t phase = 0;
+    for (; item < nitems; item += gridDim.x, phase ^= 1) {
+        const int chunk = item % NC, bh = item / NC;
+        const size_t crow = (size_t)bh * T + (size_t)chunk * CH;
+        if (tid == 0) tma_store_wait_read();    // the previous item's Q~ / K~ / P stores have read their smem
+        float2 off[4], rr[4], Gm[4];
+        chunk_cumsum<K>(R, gtot, rg, ch0, off, rr, Gm);   // (its barrier also orders the wait above)
+        bool bad = false;
+        if (rg == 0)
 #pragma unroll
-        for (int p = 0; p < 4; ++p)
-            bad |= (-rr[p].x > GUARD) | (-rr[p].y > GUARD) | (rr[p].x - Gm[p].x > GUARD) | (rr[p].y - Gm[p].y > GUARD);
-    const bool slow = __syncthreads_or(bad) != 0;
-    if (rg == 0) {   // per-chunk statistics for the state kernel: r (row 31) and Gamma (row 63)
-        float* st = stats + ((size_t)bh * NC + chunk) * 2 * K + ch0;
-        reinterpret_cast<float4*>(st)[0] = make_float4(rr[0].x, rr[0].y, rr[1].x, rr[1].y);
-        reinterpret_cast<float4*>(st)[1] = make_float4(rr[2].x, rr[2].y, rr[3].x, rr[3].y);
-        reinterpret_cast<float4*>(st + K)[0] = make_float4(Gm[0].x, Gm[0].y, Gm[1].x, Gm[1].y);
-        reinterpret_cast<float4*>(st + K)[1] = make_float4(Gm[2].x, Gm[2].y, Gm[3].x, Gm[3].y);
-        if (tid == 0) flags[(size_t)bh * NC + chunk] = slow ? 1 : 0;
-    }
-    float2 refq[4], refk[4];
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-        const float2 rq = slow ? make_float2(0.f, 0.f) : rr[p], rk = slow ? Gm[p] : rr[p];
-        refq[p] = make_float2(-L2E * rq.x, -L2E * rq.y);
-        refk[p] = make_float2(L2E * rk.x, L2E * rk.y);
-    }
-    const int blk = ch0 >> 6, col = ch0 & 63;
-    uint8_t* qb = sQ + blk * 16384;
-    uint8_t* kb = sK + blk * 16384;
-#pragma unroll
-    for (int r = 0; r < Tl::RPG; ++r) {
-        const int t = row0 + r;
-        float2 b[4];
-#pragma unroll
-        for (int p = 0; p < 4; ++p) b[p] = add2(R.g[r][p], off[p]);
-        scaled_row(R.q[r], b, refq, 1.f, qb + sw128_off(t, col), qb + sw128_off(64 + t, col));
-        scaled_row(R.k[r], b, refk, -1.f, kb + sw128_off(t, col), kb + sw128_off(64 + t, col));
-        if (slow) {
-            float4* wb = reinterpret_cast<float4*>(bws + (crow + t) * K + ch0);
-            wb[0] = make_float4(b[0].x, b[0].y, b[1].x, b[1].y);
-            wb[1] = make_float4(b[2].x, b[2].y, b[3].x, b[3].y);
+            for (int p = 0; p < 4; ++p)
+                bad |= (-rr[p].x > GUARD) | (-rr[p].y > GUARD) | (rr[p].x - Gm[p].x > GUARD) | (rr[p].y - Gm[p].y > GUARD);
+        const bool slow = __syncthreads_or(bad) != 0;
+        if (rg == 0) {   // per-chunk statistics for the state kernel: r (row 31) and Gamma (row 63)
+            float* st = stats + ((size_t)bh * NC + chunk) * 2 * K + ch0;
+            reinterpret_cast<float4*>(st)[0] = make_float4(rr[0].x, rr[0].y, rr[1].x, rr[1].y);
+            reinterpret_cast<float4*>(st)[1] = make_float4(rr[2].x, rr[2].y, rr[3].x, rr[3].y);
+            reinterpret_cast<float4*>(st + K)[0] = make_float4(Gm[0].x, Gm[0].y, Gm[1].x, Gm[1].y);
+            reinterpret_cast<float4*>(st + K)[1] = make_float4(Gm[2].x, Gm[2].y, Gm[3].x, Gm[3].y);
+            if (tid == 0) flags[(size_t)bh * NC + chunk] = slow ? 1 : 0;
         }
-    }
-    fence_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
+        float2 refq[4], refk[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const float2 rq = slow ? make_float2(0.f, 0.f) : rr[p], rk = slow ? Gm[p] : rr[p];
+            refq[p] = make_float2(-L2E * rq.x, -L2E * rq.y);
+            refk[p] = make_float2(L2E * rk.x, L2E * rk.y);
+        }
+        const int blk = ch0 >> 6, col = ch0 & 63;
+        uint8_t* qb = sQ + blk * 16384;
+        uint8_t* kb = sK + blk * 16384;
+#pragma unroll
+        for (int r = 0; r < Tl::RPG; ++r) {
+            const int t = row0 + r;
+            float2 b[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) b[p] = add2(R.g[r][p], off[p]);
+            scaled_row(R.q[r], b, refq, 1.f, qb + sw128_off(t, col), qb + sw128_off(64 + t, col));
+            scaled_row(R.k[r], b, refk, -1.f, kb + sw128_off(t, col), kb + sw128_off(64 + t, col));
+            if (slow) {
+                float4* wb = reinterpret_cast<float4*>(bws + (crow + t) * K + ch0);
+                wb[0] = make_float4(b[0].x, b[0].y, b[1].x, b[1].y);
+                wb[1] = make_float4(b[2].x, b[2].y, b[3].x, b[3].y);
+            }
+        }
+        {   // the operand registers are dead: start loading the next item (overlaps MMA, epilogue, stores)
+            const int nx = item + gridDim.x;
+            if (nx < nitems)
+                load_chunk<K, TG, true, true>(R, q, k, g, (size_t)(nx / NC) * T + (size_t)(nx % NC) * CH, row0, ch0);
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            if (!slow) {
+                const uint32_t idP = idesc_bf16(128, 128, 0, 0);
+                const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK);
+#pragma unroll
+                for (int kk = 0; kk < K / 16; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    mma_bf16(tP, sdesc_sw128(aQ + o, 16, 1024), sdesc_sw128(aK + o, 16, 1024), idP, kk > 0);
+                }
+            }
+            mma_commit(&bar);
+            // Q~hi and K~hi (rows 0-63 of each 64-channel block) -> HBM, swizzle undone by the TMA engine
+            for (int c = 0; c < K / 64; ++c) {
+                tma_store_2d(&tmQ, sQ + c * 16384, 64 * c, (int)crow);
+                tma_store_2d(&tmK, sK + c * 16384, 64 * c, (int)crow);
+            }
+            tma_store_commit();
+        }
+        const int lq = warp & 3, half = warp >> 2;
+        const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
+        const int vrow = 32 * lq + lane;
+        mbar_wait(&bar, phase);   // the P MMA (if any) has completed
         tc_fence_after();
         if (!slow) {
-            const uint32_t idP = idesc_bf16(128, 128, 0, 0);
-            const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK);
+            if (lq >= 2) {   // lo rows: lh + ll
+                uint32_t a[32], b[32];
+                tmem_ld32(tP + lane_base + 32 * half, a);
+                tmem_ld32(tP + lane_base + 64 + 32 * half, b);
+                tmem_wait_ld();
+                const int t = vrow - 64;
 #pragma unroll
-            for (int kk = 0; kk < K / 16; ++kk) {
-                const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                mma_bf16(tP, sdesc_sw128(aQ + o, 16, 1024), sdesc_sw128(aK + o, 16, 1024), idP, kk > 0);
+                for (int j = 0; j < 32; ++j)
+                    exch[t * 64 + ((32 * half + j + t) & 63)] = __uint_as_float(a[j]) + __uint_as_float(b[j]);
+            }
+            __syncthreads();
+            if (lq < 2) {    // hi rows: hh + hl + exchange, causal mask, bf16
+                uint32_t a[32], b[32];
+                tmem_ld32(tP + lane_base + 32 * half, a);
+                tmem_ld32(tP + lane_base + 64 + 32 * half, b);
+                tmem_wait_ld();
+                const int t = vrow;
+                uint32_t pk[16];
+#pragma unroll
+                for (int j = 0; j < 32; j += 2) {
+                    const int s = 32 * half + j;
+                    float p0 = __uint_as_float(a[j]) + __uint_as_float(b[j]) + exch[t * 64 + ((s + t) & 63)];
+                    float p1 = __uint_as_float(a[j + 1]) + __uint_as_float(b[j + 1]) + exch[t * 64 + ((s + 1 + t) & 63)];
+                    pk[j / 2] = pack_bf16(s <= t ? p0 : 0.f, s + 1 <= t ? p1 : 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    *reinterpret_cast<uint4*>(sP + sw128_off(t, 32 * half + 8 * u)) =
+                        make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+            }
+        } else {
+            // exact path: P[t][s] = sum_m q_tm k_sm e^{b_tm - b_sm}, s <= t, every exponent <= 0
+            __syncthreads();
+            for (int e = tid; e < CH * CH; e += NTH) {
+                const int t = e >> 6, s_ = e & 63;
+                float acc = 0.f;
+                if (s_ <= t) {
+                    const __nv_bfloat16* qt = q + (crow + t) * K;
+                    const __nv_bfloat16* ks = k + (crow + s_) * K;
+                    const float* bt = bws + (crow + t) * K;
+                    const float* bs = bws + (crow + s_) * K;
+                    for (int m = 0; m < K; ++m)
+                        acc += __bfloat162float(qt[m]) * __bfloat162float(ks[m]) * ex2f((bt[m] - bs[m]) * L2E);
+                }
+                *reinterpret_cast<__nv_bfloat16*>(sP + sw128_off(t, s_)) = __float2bfloat16_rn(acc);
             }
         }
-        mma_commit(&bar);
-        // Q~hi and K~hi (rows 0-63 of each 64-channel block) -> HBM, swizzle undone by the TMA engine
-        prefetch_tmap(&tmQ);
-        for (int c = 0; c < K / 64; ++c) {
-            tma_store_2d(&tmQ, sQ + c * 16384, 64 * c, (int)crow);
-            tma_store_2d(&tmK, sK + c * 16384, 64 * c, (int)crow);
-        }
-        tma_store_commit();
-    }
-    const int lq = warp & 3, half = warp >> 2;
-    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
-    const int vrow = 32 * lq + lane;
-    if (!slow) {
-        mbar_wait(&bar, 0);
-        tc_fence_after();
-        if (lq >= 2) {   // lo rows: lh + ll
-            uint32_t a[32], b[32];
-            tmem_ld32(tP + lane_base + 32 * half, a);
-            tmem_ld32(tP + lane_base + 64 + 32 * half, b);
-            tmem_wait_ld();
-            const int t = vrow - 64;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                exch[t * 64 + ((32 * half + j + t) & 63)] = __uint_as_float(a[j]) + __uint_as_float(b[j]);
-        }
-        __syncthreads();
-        if (lq < 2) {    // hi rows: hh + hl + exchange, causal mask, bf16
-            uint32_t a[32], b[32];
-            tmem_ld32(tP + lane_base + 32 * half, a);
-            tmem_ld32(tP + lane_base + 64 + 32 * half, b);
-            tmem_wait_ld();
-            const int t = vrow;
-            uint32_t pk[16];
-#pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-                const int s = 32 * half + j;
-                float p0 = __uint_as_float(a[j]) + __uint_as_float(b[j]) + exch[t * 64 + ((s + t) & 63)];
-                float p1 = __uint_as_float(a[j + 1]) + __uint_as_float(b[j + 1]) + exch[t * 64 + ((s + 1 + t) & 63)];
-                pk[j / 2] = pack_bf16(s <= t ? p0 : 0.f, s + 1 <= t ? p1 : 0.f);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                *reinterpret_cast<uint4*>(sP + sw128_off(t, 32 * half + 8 * u)) =
-                    make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-        }
-    } else {
-        // exact path: P[t][s] = sum_m q_tm k_sm e^{b_tm - b_sm}, s <= t, every exponent <= 0
-        __syncthreads();
-        for (int e = tid; e < CH * CH; e += NTH) {
-            const int t = e >> 6, s = e & 63;
-            float a = 0.f;
-            if (s <= t) {
-                const __nv_bfloat16* qt = q + (crow + t) * K;
-                const __nv_bfloat16* ks = k + (crow + s) * K;
-                const float* bt = bws + (crow + t) * K;
-                const float* bs = bws + (crow + s) * K;
-                for (int m = 0; m < K; ++m)
-                    a += __bfloat162float(qt[m]) * __bfloat162float(ks[m]) * ex2f((bt[m] - bs[m]) * L2E);
-            }
-            *reinterpret_cast<__nv_bfloat16*>(sP + sw128_off(t, s)) = __float2bfloat16_rn(a);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();                         // P staged; TMEM P drained; exch free
+        if (tid == 0) {
+            tma_store_2d(&tmP, sP, 0, (int)crow);
+            tma_store_commit();
         }
     }
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-        tma_store_2d(&tmP, sP, 0, (int)crow);
-        tma_store_commit();
-        tma_store_wait_all();
-    }
+    if (tid == 0) tma_store_wait_all();
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tP, 128);
@@ -545,8 +560,10 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
         return e;
     {
         GLA_PROF("tc::fwd_prep", st);
-        k_fwd_prep<K, TG><<<dim3((unsigned)NC, (unsigned)BH), NTH, PrepCfg<K>::SMEM, st>>>(
-            mQ, mK, mP, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k, (const TG*)p.g, stats, flags, bws, p.T);
+        const int nitems = (int)(NC * BH);
+        k_fwd_prep<K, TG><<<(unsigned)(nitems < num_sms() ? nitems : num_sms()), NTH, PrepCfg<K>::SMEM, st>>>(
+            mQ, mK, mP, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k, (const TG*)p.g, stats, flags, bws, p.T,
+            (int)NC, nitems);
     }
     {
         GLA_PROF("tc::fwd_state", st);
