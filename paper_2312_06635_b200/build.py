@@ -16,6 +16,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "--
          "-Xptxas", "-v"]
 FLAGS_C = [f for f in FLAGS if f != "-shared"]
 OBJ = os.path.join(HERE, "build")
+RDC = {"simt.cu"}   # device-side (tail) launches of the exact fallback need relocatable device code
 
 
 def sources():
@@ -47,7 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in sources():
         obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
         if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), hdr_t):
-            cmd = [NVCC, *ARCH, *FLAGS_C, "-I", os.path.join(HERE, "..", "include"), "-c", "-o", obj, src]
+            rdc = ["-rdc=true"] if os.path.basename(src) in RDC else []
+            cmd = [NVCC, *ARCH, *FLAGS_C, *rdc, "-I", os.path.join(HERE, "..", "include"), "-c", "-o", obj, src]
             jobs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
     info = {}
     for src, pr in jobs:
@@ -59,7 +61,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         with open(os.path.join(OBJ, os.path.basename(src)[:-3] + ".ptxas"), "w") as f:
             f.write(err)
     objs = [os.path.join(OBJ, os.path.basename(s)[:-3] + ".o") for s in sources()]
-    res = subprocess.run([NVCC, *ARCH, "-shared", "-o", LIB, *objs], capture_output=True, text=True)
+    res = subprocess.run([NVCC, *ARCH, "-shared", "-rdc=true", "-o", LIB, *objs, "-lcudadevrt"], capture_output=True,
+                         text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed linking libgla.so")
@@ -81,8 +84,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 def build_timing() -> str:
     """libgla_timing.so: the same sources with -DGLA_PHASE_TIMING (kernels print per-chunk phase traces)."""
     out = os.path.join(HERE, "libgla_timing.so")
-    cmd = [NVCC, *ARCH, *FLAGS, "-DGLA_PHASE_TIMING", "-I", os.path.join(HERE, "..", "include"), "-o", out,
-           *sources()]
+    cmd = [NVCC, *ARCH, *FLAGS, "-rdc=true", "-DGLA_PHASE_TIMING", "-I", os.path.join(HERE, "..", "include"), "-o",
+           out, *sources(), "-lcudadevrt"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
