@@ -17,5 +17,8 @@ size_t bwd_ws(int B, int H, int T, int K, int V, int C);
 // Number of SMs of the current device (cached; persistent kernels size their grids with it).
 int num_sms();
 cudaError_t make_map_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, bool swizzle);
+// General 2-D map: bf16 (elem_bytes 2) or fp32 (4) [rows][cols] row-major, box {box_cols, box_rows}.
+cudaError_t make_map_2d_ex(CUtensorMap* map, const void* base, int elem_bytes, uint64_t rows, uint64_t cols,
+                           uint32_t box_cols, uint32_t box_rows, bool swizzle);
 }  // namespace tc
 }  // namespace gla

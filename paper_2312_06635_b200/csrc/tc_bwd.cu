@@ -555,12 +555,14 @@ k_bwd_dkv(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUten
 }
 
 // ---------------------------------------------------------------------------------------------------------------
-// k_bwd_reduce: grid (K/64, BH), 256 threads = 64 rows x 4 groups of 16 channels (16-byte vector loads).
+// k_bwd_reduce: grid (K/RCW, BH), 64 x RCW/16 threads = 64 rows x groups of 16 channels (16-byte vector loads);
+// (RCW = 32 -- 512 smaller CTAs at 1.3B shapes -- measured slower: 287 vs 262 us.)
+constexpr int RCW = 64;
 // Reverse over chunks: dq = E_q (.) sum_j dq_j, dk = E_k (.) sum_j dk_j (fixed j order), and
 // d log alpha_t = carry + sum_{s >= t in chunk} (q dq - k dk)_s, the carry summing every later chunk plus
 // rowsum(S_T (.) dS_T).  The next chunk's inputs are prefetched into registers while this one is scanned.
 template <int K, int NVT, typename TG>
-__global__ void __launch_bounds__(256) k_bwd_reduce(const __nv_bfloat16* __restrict__ q,
+__global__ void __launch_bounds__(64 * (RCW / 16)) k_bwd_reduce(const __nv_bfloat16* __restrict__ q,
                                                     const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g,
                                                     const __nv_bfloat16* __restrict__ dqp,
                                                     const __nv_bfloat16* __restrict__ dkp,
@@ -569,15 +571,16 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(const __nv_bfloat16* __restr
                                                     const float* __restrict__ cpart, const int* __restrict__ flag,
                                                     int T, int BH) {
     if (*flag) return;
-    __shared__ float sb[64][65];      // g -> b (chunk-local cumsum), then x -> suffix sums
-    __shared__ float carry_s[64];
-    const int tid = threadIdx.x, t = tid >> 2, cg = tid & 3;
-    const int m0 = blockIdx.x * 64, bh = blockIdx.y;
+    constexpr int NG = RCW / 16;      // 16-channel groups per row
+    __shared__ float sb[64][RCW + 1]; // g -> b (chunk-local cumsum), then x -> suffix sums
+    __shared__ float carry_s[RCW];
+    const int tid = threadIdx.x, t = tid / NG, cg = tid % NG;
+    const int m0 = blockIdx.x * RCW, bh = blockIdx.y;
     const int mc = m0 + 16 * cg;      // this thread's 16 channels [mc, mc+16)
     const int NC = T / CH;
     const size_t head_row = (size_t)bh * T;
     const size_t plane = (size_t)BH * T * K;
-    if (tid < 64) {
+    if (tid < RCW) {
         float c0 = 0.f;
         if (stdot)
             for (int j = 0; j < NVT; ++j) c0 += stdot[((size_t)j * BH + bh) * K + m0 + tid];
@@ -608,7 +611,7 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(const __nv_bfloat16* __restr
     };
     load(NC - 1);
     for (int i = NC - 1; i >= 0; --i) {
-        if (tid < 64 && i + 1 < NC && (i + 1) % ANCH == 0) {   // exact carry rowsum(H_{i+1} (.) dH_{i+1})
+        if (tid < RCW && i + 1 < NC && (i + 1) % ANCH == 0) {   // exact carry rowsum(H_{i+1} (.) dH_{i+1})
             float c0 = 0.f;
             const size_t a = (i + 1) / ANCH - 1;
             for (int j = 0; j < NVT; ++j) c0 += cpart[((a * NVT + j) * BH + bh) * K + m0 + tid];
@@ -618,7 +621,7 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(const __nv_bfloat16* __restr
 #pragma unroll
         for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = gv[u];
         __syncthreads();
-        if (tid < 64) {
+        if (tid < RCW) {
             float run = 0.f;
             for (int r = 0; r < CH; ++r) { run += sb[r][tid]; sb[r][tid] = run; }
         }
@@ -654,6 +657,174 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(const __nv_bfloat16* __restr
         }
         if (i > 0) load(i - 1);
         __syncthreads();                   // everyone has read b
+#pragma unroll
+        for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = x[u];
+        __syncthreads();
+        if (tid < RCW) {                   // reverse cumsum with the carry of all later chunks
+            float run = carry_s[tid];
+            for (int r = CH - 1; r >= 0; --r) { run += sb[r][tid]; sb[r][tid] = run; }
+            carry_s[tid] = run;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 16; u += 4)
+            *reinterpret_cast<float4*>(dg + ix + u) =
+                make_float4(sb[t][16 * cg + u], sb[t][16 * cg + u + 1], sb[t][16 * cg + u + 2], sb[t][16 * cg + u + 3]);
+        __syncthreads();
+    }
+}
+
+// k_bwd_reduce_tma: the same computation as k_bwd_reduce, with every input tile of a chunk -- the NVT dq and dk
+// partials, q, k, log alpha ([64 rows x 64 channels] each) -- staged in shared memory by TMA (SWIZZLE_128B) two
+// chunks ahead, so the HBM latency of the partials overlaps the scans of the chunks in between (the register-
+// prefetched version waited on its loads: ncu long-scoreboard stalls at the first use of every partial).
+template <int NVT, typename TG>
+struct RedCfg {
+    static constexpr uint32_t TILE = 8192;                               // [64 rows][64 bf16] or [64][32 fp32]
+    static constexpr uint32_t GT = 64 * 64 * sizeof(TG);                 // log alpha tile bytes
+    static constexpr uint32_t STAGE = (2 * NVT + 2) * TILE + GT;
+    static constexpr int NS = 2 * STAGE + 64 * 65 * 4 + 1024 <= 232448 ? 2 : 1;
+    static constexpr uint32_t SMEM = NS * STAGE + 1024;
+};
+
+template <int K, int NVT, typename TG>
+__global__ void __launch_bounds__(256, 1)
+k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                 const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmDQP,
+                 const __grid_constant__ CUtensorMap tmDKP, const float* __restrict__ stdot,
+                 __nv_bfloat16* __restrict__ dq, __nv_bfloat16* __restrict__ dk, float* __restrict__ dg,
+                 const float* __restrict__ cpart, const int* __restrict__ flag, int T, int BH) {
+    using RC = RedCfg<NVT, TG>;
+    if (*flag) return;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = smem_align1k(smem_raw);
+    __shared__ float sb[64][65];      // g -> b (chunk-local cumsum), then x -> suffix sums
+    __shared__ float carry_s[64];
+    __shared__ uint64_t bar[2];
+    const int tid = threadIdx.x, t = tid >> 2, cg = tid & 3;
+    const int m0 = blockIdx.x * 64, bh = blockIdx.y;
+    const int mc = m0 + 16 * cg;      // this thread's 16 channels [mc, mc+16)
+    const int NC = T / CH;
+    const size_t head_row = (size_t)bh * T;
+    auto issue = [&](int i) {         // all input tiles of chunk i into stage i % NS
+        uint8_t* st = sm + (i % RC::NS) * RC::STAGE;
+        uint64_t* b = &bar[i % RC::NS];
+        const int row = (int)(head_row + (size_t)i * CH);
+        mbar_expect_tx(b, RC::STAGE);
+        for (int j = 0; j < NVT; ++j) {
+            tma_load_2d(st + j * RC::TILE, &tmDQP, b, m0, row + j * BH * T);
+            tma_load_2d(st + (NVT + j) * RC::TILE, &tmDKP, b, m0, row + j * BH * T);
+        }
+        tma_load_2d(st + 2 * NVT * RC::TILE, &tmQ, b, m0, row);
+        tma_load_2d(st + (2 * NVT + 1) * RC::TILE, &tmK, b, m0, row);
+        if (sizeof(TG) == 4) {
+            tma_load_2d(st + (2 * NVT + 2) * RC::TILE, &tmG, b, m0, row);
+            tma_load_2d(st + (2 * NVT + 2) * RC::TILE + 8192, &tmG, b, m0 + 32, row);
+        } else {
+            tma_load_2d(st + (2 * NVT + 2) * RC::TILE, &tmG, b, m0, row);
+        }
+    };
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmG); prefetch_tmap(&tmDQP); prefetch_tmap(&tmDKP);
+        for (int s2 = 0; s2 < RC::NS && NC - 1 - s2 >= 0; ++s2) issue(NC - 1 - s2);
+    }
+    if (tid < 64) {
+        float c0 = 0.f;
+        if (stdot)
+            for (int j = 0; j < NVT; ++j) c0 += stdot[((size_t)j * BH + bh) * K + m0 + tid];
+        carry_s[tid] = c0;
+    }
+    __syncthreads();
+    uint32_t uses[2] = {0u, 0u};
+    // byte offset of 8 consecutive bf16 channels [c, c+8) of row t in a SW128 [64][64] bf16 tile
+    auto bf_off = [&](int c) { return (uint32_t)(t * 128 + ((((c >> 3) ^ (t & 7))) << 4)); };
+    for (int i = NC - 1; i >= 0; --i) {
+        const int sidx = i % RC::NS;
+        const uint8_t* st = sm + sidx * RC::STAGE;
+        if (tid < 64 && i + 1 < NC && (i + 1) % ANCH == 0) {   // exact carry rowsum(H_{i+1} (.) dH_{i+1})
+            float c0 = 0.f;
+            const size_t a = (i + 1) / ANCH - 1;
+            for (int j = 0; j < NVT; ++j) c0 += cpart[((a * NVT + j) * BH + bh) * K + m0 + tid];
+            carry_s[tid] = c0;
+        }
+        mbar_wait(&bar[sidx], (uses[sidx]++) & 1);
+        // (a1) chunk-local cumsum: stage g, one thread per channel scans the 64 rows
+        {
+            const uint8_t* gt = st + (2 * NVT + 2) * RC::TILE;
+            float gv[16];
+            if (sizeof(TG) == 4) {
+                const uint8_t* box = gt + (cg >> 1) * 8192;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float4 x = *reinterpret_cast<const float4*>(box + t * 128 + (((((cg & 1) * 4 + c)) ^ (t & 7)) << 4));
+                    gv[4 * c] = x.x; gv[4 * c + 1] = x.y; gv[4 * c + 2] = x.z; gv[4 * c + 3] = x.w;
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const uint4 x = *reinterpret_cast<const uint4*>(gt + bf_off(16 * cg + 8 * c));
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const uint32_t u = word(x, w);
+                        gv[8 * c + 2 * w] = bf16lo(u);
+                        gv[8 * c + 2 * w + 1] = bf16hi(u);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = gv[u];
+        }
+        __syncthreads();
+        if (tid < 64) {
+            float run = 0.f;
+            for (int r = 0; r < CH; ++r) { run += sb[r][tid]; sb[r][tid] = run; }
+        }
+        __syncthreads();
+        float x[16], dqv[16], dkv[16];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const uint32_t o = bf_off(16 * cg + 8 * c);
+            float sq[8], sk[8];
+#pragma unroll
+            for (int w = 0; w < 8; ++w) { sq[w] = 0.f; sk[w] = 0.f; }
+#pragma unroll
+            for (int j = 0; j < NVT; ++j) {
+                const uint4 a = *reinterpret_cast<const uint4*>(st + j * RC::TILE + o);
+                const uint4 b = *reinterpret_cast<const uint4*>(st + (NVT + j) * RC::TILE + o);
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    sq[2 * w] += bf16lo(word(a, w)); sq[2 * w + 1] += bf16hi(word(a, w));
+                    sk[2 * w] += bf16lo(word(b, w)); sk[2 * w + 1] += bf16hi(word(b, w));
+                }
+            }
+            const uint4 qv = *reinterpret_cast<const uint4*>(st + 2 * NVT * RC::TILE + o);
+            const uint4 kv = *reinterpret_cast<const uint4*>(st + (2 * NVT + 1) * RC::TILE + o);
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const int u = 8 * c + w;
+                const float b = sb[t][16 * cg + u], r = sb[CH / 2 - 1][16 * cg + u];
+                dqv[u] = sq[w] * ex2f((b - r) * L2E);
+                dkv[u] = sk[w] * ex2f((r - b) * L2E);
+                const float qf = (w & 1) ? bf16hi(word(qv, w >> 1)) : bf16lo(word(qv, w >> 1));
+                const float kf = (w & 1) ? bf16hi(word(kv, w >> 1)) : bf16lo(word(kv, w >> 1));
+                x[u] = qf * dqv[u] - kf * dkv[u];
+            }
+        }
+        const size_t ix = (head_row + (size_t)i * CH + t) * K + mc;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const uint4 oq = make_uint4(pack_bf16(dqv[8 * u], dqv[8 * u + 1]), pack_bf16(dqv[8 * u + 2], dqv[8 * u + 3]),
+                                        pack_bf16(dqv[8 * u + 4], dqv[8 * u + 5]), pack_bf16(dqv[8 * u + 6], dqv[8 * u + 7]));
+            const uint4 ok = make_uint4(pack_bf16(dkv[8 * u], dkv[8 * u + 1]), pack_bf16(dkv[8 * u + 2], dkv[8 * u + 3]),
+                                        pack_bf16(dkv[8 * u + 4], dkv[8 * u + 5]), pack_bf16(dkv[8 * u + 6], dkv[8 * u + 7]));
+            *reinterpret_cast<uint4*>(dq + ix + 8 * u) = oq;
+            *reinterpret_cast<uint4*>(dk + ix + 8 * u) = ok;
+        }
+        __syncthreads();                   // everyone has read b and the stage buffers
+        if (tid == 0 && i - RC::NS >= 0) issue(i - RC::NS);   // refill this stage two chunks ahead
 #pragma unroll
         for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = x[u];
         __syncthreads();
@@ -1468,12 +1639,12 @@ static cudaError_t launch_bwd(const BwdProblem& p, cudaStream_t st) {
         const __nv_bfloat16 *q_ = (const __nv_bfloat16*)p.q, *k_ = (const __nv_bfloat16*)p.k;
         const float* sd = p.dfinal ? stdot : nullptr;
         __nv_bfloat16 *dq_ = (__nv_bfloat16*)p.dq, *dk_ = (__nv_bfloat16*)p.dk;
-        const dim3 rg(K / 64, BH);
+        const dim3 rg(K / RCW, BH);
         switch (NVT) {
-            case 1: k_bwd_reduce<K, 1, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
-            case 2: k_bwd_reduce<K, 2, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
-            case 4: k_bwd_reduce<K, 4, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
-            case 8: k_bwd_reduce<K, 8, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
+            case 1: k_bwd_reduce<K, 1, TG><<<rg, 64 * (RCW / 16), 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
+            case 2: k_bwd_reduce<K, 2, TG><<<rg, 64 * (RCW / 16), 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
+            case 4: k_bwd_reduce<K, 4, TG><<<rg, 64 * (RCW / 16), 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
+            case 8: k_bwd_reduce<K, 8, TG><<<rg, 64 * (RCW / 16), 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
             default: return cudaErrorNotSupported;
         }
     }
@@ -1544,17 +1715,30 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     }
     {
         GLA_PROF("tc::bwd_reduce", st);
-        const __nv_bfloat16 *q_ = (const __nv_bfloat16*)p.q, *k_ = (const __nv_bfloat16*)p.k;
+        CUtensorMap mQr, mKr, mGr, mDQP, mDKP;
+        const uint64_t prow = (uint64_t)NVT * BH * p.T;
+        if ((e = make_map_2d_ex(&mQr, p.q, 2, rows, K, 64, 64, true)) != cudaSuccess) return e;
+        if ((e = make_map_2d_ex(&mKr, p.k, 2, rows, K, 64, 64, true)) != cudaSuccess) return e;
+        if ((e = make_map_2d_ex(&mGr, p.g, (int)sizeof(TG), rows, K, sizeof(TG) == 4 ? 32 : 64, 64, true)) != cudaSuccess)
+            return e;
+        if ((e = make_map_2d_ex(&mDQP, dqp, 2, prow, K, 64, 64, true)) != cudaSuccess) return e;
+        if ((e = make_map_2d_ex(&mDKP, dkp, 2, prow, K, 64, 64, true)) != cudaSuccess) return e;
         const float* sd = p.dfinal ? stdot : nullptr;
         __nv_bfloat16 *dq_ = (__nv_bfloat16*)p.dq, *dk_ = (__nv_bfloat16*)p.dk;
         const dim3 rg(K / 64, BH);
+#define GLA_RED(N)                                                                                                  \
+    case N:                                                                                                         \
+        if ((e = cudaFuncSetAttribute(k_bwd_reduce_tma<K, N, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                      (int)RedCfg<N, TG>::SMEM)) != cudaSuccess)                                    \
+            return e;                                                                                               \
+        k_bwd_reduce_tma<K, N, TG><<<rg, 256, RedCfg<N, TG>::SMEM, st>>>(mQr, mKr, mGr, mDQP, mDKP, sd, dq_, dk_,   \
+                                                                          p.dg, cpart, flag, p.T, BH);              \
+        break;
         switch (NVT) {
-            case 1: k_bwd_reduce<K, 1, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
-            case 2: k_bwd_reduce<K, 2, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
-            case 4: k_bwd_reduce<K, 4, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
-            case 8: k_bwd_reduce<K, 8, TG><<<rg, 256, 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
+            GLA_RED(1) GLA_RED(2) GLA_RED(4) GLA_RED(8)
             default: return cudaErrorNotSupported;
         }
+#undef GLA_RED
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     BwdProblem sp = p;
