@@ -253,7 +253,8 @@ def main():
 
     def step():
         G.chunk_fwd(q, k, v, g, C, c, None, False, args.path, out=o, workspace=wf)
-        G.chunk_bwd(q, k, v, g, do, C, c, None, None, False, args.path, grads=grads, workspace=wb)
+        G.chunk_bwd(q, k, v, g, do, C, c, None, None, False, args.path, grads=grads, workspace=wb,
+                    fwd_workspace=wf)
 
     for _ in range(args.warmup):
         step()
@@ -306,7 +307,7 @@ def main():
                 dst.copy_(src, non_blocking=True)
             G.chunk_fwd(dd[0], dd[1], dd[2], dd[3], C, c, None, False, args.path, out=o, workspace=wf)
             G.chunk_bwd(dd[0], dd[1], dd[2], dd[3], dd[4], C, c, None, None, False, args.path,
-                        grads=(dq_, dk_, dv_, dg_, None), workspace=wb)
+                        grads=(dq_, dk_, dv_, dg_, None), workspace=wb, fwd_workspace=wf)
             ho.copy_(o, non_blocking=True)
             for dst, src in zip(hgr, (dq_, dk_, dv_, dg_)):
                 dst.copy_(src, non_blocking=True)

@@ -101,6 +101,20 @@ int gla_chunk_bwd(const gla_desc *d, const void *q, const void *k, const void *v
                   void *workspace, size_t workspace_bytes, void *stream);
 
 /*
+ * gla_chunk_bwd_saved -- gla_chunk_bwd reusing the per-chunk operands a preceding gla_chunk_fwd left in its
+ * workspace (the "saved activations" of a training step): on the tensor-core path the backward then skips
+ * recomputing the chunk-local cumsums, Q~, K~ and P = (Q~ K~^T) (.) M and only forms dP.
+ * fwd_workspace: the workspace of a gla_chunk_fwd call with the same descriptor and the same q, k, log_alpha,
+ *                not modified since (no ownership transfer; the caller keeps both buffers alive), or NULL
+ *                (then identical to gla_chunk_bwd).  Ignored on the SIMT path.
+ * Results are bitwise identical to gla_chunk_bwd's.  Other arguments, errors: as gla_chunk_bwd.
+ */
+int gla_chunk_bwd_saved(const gla_desc *d, const void *q, const void *k, const void *v, const void *log_alpha,
+                        const float *initial_state, const void *d_out, const float *d_final_state,
+                        void *dq, void *dk, void *dv, float *d_log_alpha, float *d_initial_state,
+                        void *workspace, size_t workspace_bytes, const void *fwd_workspace, void *stream);
+
+/*
  * gla_recurrent_step -- one decoding step of the recurrent form, for every (b,h):
  *   state <- diag(exp(log_alpha_t)) state + k_t^T v_t ;  out_t = q_t state
  * in:  q_t, k_t [B,H,K] and v_t [B,H,V] (dtype); log_alpha_t [B,H,K] (gate_dtype)

@@ -53,6 +53,7 @@ def lib():
         L.gla_bwd_workspace_size.restype = sz
         L.gla_chunk_fwd.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
         L.gla_chunk_bwd.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        L.gla_chunk_bwd_saved.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp]
         L.gla_recurrent_step.argtypes = [ip, ip, ip, ip, ip, ip, vp, vp, vp, vp, vp, vp, vp]
         L.gla_state_summary.argtypes = [dp, vp, vp, vp, vp, vp, vp, sz, vp]
         L.gla_dstate_summary.argtypes = [dp, vp, vp, vp, vp, vp, sz, vp]
@@ -74,7 +75,7 @@ def lib():
     return _lib
 
 
-EXPORTS = ("gla_fwd_workspace_size", "gla_bwd_workspace_size", "gla_chunk_fwd", "gla_chunk_bwd",
+EXPORTS = ("gla_fwd_workspace_size", "gla_bwd_workspace_size", "gla_chunk_fwd", "gla_chunk_bwd", "gla_chunk_bwd_saved",
            "gla_recurrent_step", "gla_state_summary", "gla_dstate_summary", "gla_state_combine",
            "gla_status_string", "gla_last_cuda_error", "gla_resolve_path", "gla_version", "gla_profile_enable",
            "gla_profile_reset", "gla_profile_count", "gla_profile_get")
@@ -151,8 +152,9 @@ def chunk_fwd(q, k, v, log_alpha, chunk: int = 64, subchunk: int = 16, initial_s
 
 def chunk_bwd(q, k, v, log_alpha, d_out, chunk: int = 64, subchunk: int = 16, initial_state=None,
               d_final_state=None, need_d_initial_state: bool = False, path: str = "auto", grads=None,
-              workspace=None):
-    """(dq, dk, dv, d_log_alpha fp32, d_initial_state fp32 or None).  gla_chunk_bwd."""
+              workspace=None, fwd_workspace=None):
+    """(dq, dk, dv, d_log_alpha fp32, d_initial_state fp32 or None).  gla_chunk_bwd, or gla_chunk_bwd_saved when
+    ``fwd_workspace`` (the workspace a chunk_fwd call on the same q, k, log_alpha filled) is given."""
     for t, n in ((q, "q"), (k, "k"), (v, "v"), (log_alpha, "log_alpha"), (d_out, "d_out")):
         _check(t, n)
     B, H, T, K = q.shape
@@ -166,6 +168,12 @@ def chunk_bwd(q, k, v, log_alpha, d_out, chunk: int = 64, subchunk: int = 16, in
         dq, dk, dv, dg, dh0 = grads
     if workspace is None:
         workspace = bwd_workspace(q, v, log_alpha, chunk, subchunk, path)
+    if fwd_workspace is not None:
+        _check(fwd_workspace, "fwd_workspace")
+        _call(lib().gla_chunk_bwd_saved, "gla_chunk_bwd_saved", ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v),
+              _ptr(log_alpha), _ptr(initial_state), _ptr(d_out), _ptr(d_final_state), _ptr(dq), _ptr(dk), _ptr(dv),
+              _ptr(dg), _ptr(dh0), _ptr(workspace), workspace.numel(), _ptr(fwd_workspace), _stream(q.device))
+        return dq, dk, dv, dg, dh0
     _call(lib().gla_chunk_bwd, "gla_chunk_bwd", ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(log_alpha),
           _ptr(initial_state), _ptr(d_out), _ptr(d_final_state), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dg),
           _ptr(dh0), _ptr(workspace), workspace.numel(), _stream(q.device))

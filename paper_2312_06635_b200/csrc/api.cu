@@ -135,10 +135,10 @@ int gla_chunk_fwd(const gla_desc* d, const void* q, const void* k, const void* v
     return cuda_status(path == GLA_PATH_TC ? gla::tc::fwd(p, st) : gla::simt::fwd(p, st));
 }
 
-int gla_chunk_bwd(const gla_desc* d, const void* q, const void* k, const void* v, const void* log_alpha,
+int gla_chunk_bwd_saved(const gla_desc* d, const void* q, const void* k, const void* v, const void* log_alpha,
                   const float* initial_state, const void* d_out, const float* d_final_state, void* dq, void* dk,
                   void* dv, float* d_log_alpha, float* d_initial_state, void* workspace, size_t workspace_bytes,
-                  void* stream) {
+                  const void* fwd_workspace, void* stream) {
     int s = check_desc(d);
     if (s) return s;
     const int path = resolve(d);
@@ -150,14 +150,23 @@ int gla_chunk_bwd(const gla_desc* d, const void* q, const void* k, const void* v
         return s ? s : copy_or_zero(d_initial_state, d_final_state, (size_t)d->B * d->H * d->K * d->V, st);
     }
     s = check_ptrs({q, k, v, log_alpha, d_out, dq, dk, dv, d_log_alpha},
-                   {initial_state, d_final_state, d_initial_state, workspace});
+                   {initial_state, d_final_state, d_initial_state, workspace, fwd_workspace});
     if (s) return s;
     if (workspace_bytes < gla_bwd_workspace_size(d) || (!workspace && gla_bwd_workspace_size(d)))
         return GLA_ERR_WORKSPACE;
     gla::BwdProblem p = make_bwd(d, 0);
     p.q = q; p.k = k; p.v = v; p.g = log_alpha; p.dO = d_out; p.h0 = initial_state; p.dfinal = d_final_state;
     p.dq = dq; p.dk = dk; p.dv = dv; p.dg = d_log_alpha; p.dh0 = d_initial_state; p.ws = workspace;
+    p.fwd_ws = fwd_workspace;
     return cuda_status(path == GLA_PATH_TC ? gla::tc::bwd(p, st) : gla::simt::bwd(p, st));
+}
+
+int gla_chunk_bwd(const gla_desc* d, const void* q, const void* k, const void* v, const void* log_alpha,
+                  const float* initial_state, const void* d_out, const float* d_final_state, void* dq, void* dk,
+                  void* dv, float* d_log_alpha, float* d_initial_state, void* workspace, size_t workspace_bytes,
+                  void* stream) {
+    return gla_chunk_bwd_saved(d, q, k, v, log_alpha, initial_state, d_out, d_final_state, dq, dk, dv, d_log_alpha,
+                               d_initial_state, workspace, workspace_bytes, nullptr, stream);
 }
 
 int gla_recurrent_step(int B, int H, int K, int V, int dtype, int gate_dtype, const void* q_t, const void* k_t,

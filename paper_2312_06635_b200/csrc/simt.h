@@ -25,6 +25,7 @@ struct BwdProblem {
     float *dg, *dh0;
     void* ws;
     const int* run_if;     // device flag: kernels return immediately when *run_if == 0 (nullptr = always run)
+    const void* fwd_ws = nullptr;   // workspace of a preceding TC gla_chunk_fwd on the same q, k, log alpha
 };
 
 namespace simt {

@@ -39,6 +39,8 @@ bool supported(int B, int H, int T, int K, int V, int C, int c, int qkv_dtype, i
     return qkv_dtype == 0 && (K == 64 || K == 128 || K == 256) && V % 128 == 0 && C == 64 && c > 0 && 64 % c == 0;
 }
 
+bool fwd_is_split() { return !use_fused(); }
+
 cudaError_t fwd(const Problem& p, cudaStream_t st) {
     if (p.mode != 0) return simt::fwd(p, st);
     return use_fused() ? fwd_tc(p, st) : fwd2_tc(p, st);

@@ -1043,6 +1043,98 @@ k_bwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     if (warp == 0) tmem_dealloc(tmem_base, 256);
 }
 
+// k_bwd_dp: dP = (dO V^T) (.) M per chunk over the full V, for the backward that reuses a forward's saved
+// Q~, K~, P (gla_chunk_bwd_saved).  Persistent; warp 0 streams 64-column dO / V boxes through a 4-stage TMA
+// ring, warp 1 issues the M=64 N=64 MMAs, warps 2-5 drain the accumulator (causal mask, bf16, TMA store).
+// It also ORs the forward's per-chunk exact-path flags into the backward's flag (R9).
+constexpr int DP_NSTG = 4;
+__global__ void __launch_bounds__(192, 1)
+k_bwd_dp(const __grid_constant__ CUtensorMap tmDP, const __grid_constant__ CUtensorMap tmV,
+         const __grid_constant__ CUtensorMap tmD, const int* __restrict__ fflags, int* __restrict__ flag, int T,
+         int V, int NC, int nitems) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = smem_align1k(smem_raw);
+    uint8_t* sdP = sm + DP_NSTG * 16384;
+    __shared__ uint64_t full[DP_NSTG], empty[DP_NSTG], acc_full, acc_empty;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int NKB = V / 64;
+    if (warp == 0) tmem_alloc(&tmem_base, 64);
+    if (tid == 0) {
+        for (int s2 = 0; s2 < DP_NSTG; ++s2) { mbar_init(&full[s2], 1); mbar_init(&empty[s2], 1); }
+        mbar_init(&acc_full, 1);
+        mbar_init(&acc_empty, 1);
+        fence_mbar_init();
+        prefetch_tmap(&tmDP); prefetch_tmap(&tmV); prefetch_tmap(&tmD);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tdP = tmem_base;
+    if (warp == 0) {
+        if (lane == 0) {
+            int any = 0;
+            uint32_t cnt = 0;
+            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+                const int row = (int)((size_t)(item / NC) * T + (size_t)(item % NC) * CH);
+                any |= fflags[item];
+                for (int kb = 0; kb < NKB; ++kb, ++cnt) {
+                    const uint32_t s2 = cnt % DP_NSTG, use = cnt / DP_NSTG;
+                    if (use > 0) mbar_wait(&empty[s2], (use - 1) & 1);
+                    mbar_expect_tx(&full[s2], 16384);
+                    tma_load_2d(sm + s2 * 16384, &tmD, &full[s2], 64 * kb, row);
+                    tma_load_2d(sm + s2 * 16384 + 8192, &tmV, &full[s2], 64 * kb, row);
+                }
+            }
+            if (any) atomicOr(flag, 1);
+        }
+    } else if (warp == 1) {
+        const uint32_t idDP = idesc_bf16(64, 64, 0, 0);
+        uint32_t cnt = 0, it = 0;
+        for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
+            if (it > 0) mbar_wait(&acc_empty, (it - 1) & 1);
+            tc_fence_after();
+            for (int kb = 0; kb < NKB; ++kb, ++cnt) {
+                const uint32_t s2 = cnt % DP_NSTG, use = cnt / DP_NSTG;
+                mbar_wait(&full[s2], use & 1);
+                tc_fence_after();
+                const uint32_t aD = smem_u32(sm + s2 * 16384), aV = aD + 8192;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    mma_bf16_w(tdP, sdesc_sw128(aD + kk * 32, 16, 1024), sdesc_sw128(aV + kk * 32, 16, 1024), idDP,
+                               (kb | kk) > 0);
+                mma_commit_w(&empty[s2]);
+            }
+            mma_commit_w(&acc_full);
+            __syncwarp();
+        }
+    } else {
+        const int lq = warp & 3, et = tid - 64;
+        const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
+        uint32_t it = 0;
+        for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
+            const int row = (int)((size_t)(item / NC) * T + (size_t)(item % NC) * CH);
+            mbar_wait(&acc_full, it & 1);
+            tc_fence_after();
+            if (et == 0) tma_store_wait_read();    // the previous item's dP store has read the staging tile
+            named_bar_sync(1, 128);
+            m64_epilogue(tdP, lane_base, lq, lane, sdP);
+            tc_fence_before();
+            fence_async_smem();
+            named_bar_sync(1, 128);
+            if (et == 0) {
+                mbar_arrive(&acc_empty);
+                tma_store_2d(&tmDP, sdP, 0, row);
+                tma_store_commit();
+            }
+        }
+        if (et == 0) tma_store_wait_all();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem_base, 64);
+}
+
 template <int K>
 struct BWalkCfg {
     static constexpr int KB = K / 64;
@@ -1667,6 +1759,13 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     __nv_bfloat16* Pm = (__nv_bfloat16*)w; w += al1k(rows * 64 * 2);
     __nv_bfloat16* dPm = (__nv_bfloat16*)w; w += al1k(rows * 64 * 2);
     float* stats = (float*)w; w += al1k((size_t)BH * NC * 2 * K * 4);
+    const bool saved = p.fwd_ws != nullptr && fwd_is_split();
+    const int* fflags = nullptr;
+    if (saved) {   // the forward's Q~hi, K~hi, P and (r, Gamma): only dP is left to form
+        const FwdSaved f = fwd2_saved(p.fwd_ws, p.B, p.H, p.T, K);
+        Qt = (__nv_bfloat16*)f.Qt; Kt = (__nv_bfloat16*)f.Kt; Pm = (__nv_bfloat16*)f.Pm;
+        stats = (float*)f.stats; fflags = f.flags;
+    }
     uint8_t* ws = w;
     int* flag = (int*)ws;
     __nv_bfloat16* dqp = (__nv_bfloat16*)(ws + 256);
@@ -1695,7 +1794,15 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         return e;
     if ((e = cudaFuncSetAttribute(k_bwd_dkv2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWalkCfg<K>::SMEM)))
         return e;
-    {
+    if (saved) {
+        GLA_PROF("tc::bwd_dp", st);
+        const int nitems = NC * BH;
+        const int smem = DP_NSTG * 16384 + 8192 + 1024;
+        if ((e = cudaFuncSetAttribute(k_bwd_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess)
+            return e;
+        const int grid_dp = nitems < 2 * num_sms() ? nitems : 2 * num_sms();
+        k_bwd_dp<<<(unsigned)grid_dp, 192, smem, st>>>(mDP, mV, mD, fflags, flag, p.T, p.V, NC, nitems);
+    } else {
         GLA_PROF("tc::bwd_prep", st);
         const int nitems = NC * BH;
         k_bwd_prep<K, TG><<<(unsigned)(nitems < num_sms() ? nitems : num_sms()), NTH, BPrepCfg<K>::SMEM, st>>>(

@@ -535,6 +535,18 @@ size_t fwd2_ws(int B, int H, int T, int K, int V) {
            al(BH * T * K * 4);
 }
 
+FwdSaved fwd2_saved(const void* ws, int B, int H, int T, int K) {
+    const size_t BH = (size_t)B * H, NC = T / CH, rows = BH * T;
+    const uint8_t* w = (const uint8_t*)ws;
+    FwdSaved f;
+    f.Qt = w; w += al(rows * K * 2);
+    f.Kt = w; w += al(rows * K * 2);
+    f.Pm = w; w += al(rows * 64 * 2);
+    f.stats = (const float*)w; w += al(BH * NC * 2 * K * 4);
+    f.flags = (const int*)w;
+    return f;
+}
+
 template <int K, typename TG>
 static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     const size_t BH = (size_t)p.B * p.H, NC = p.T / CH, rows = BH * p.T;

@@ -89,3 +89,23 @@ def test_tc_bwd_long_sequence_dlog_alpha(T):
     for name, x, y in zip(("dq", "dk", "dv", "dlog_alpha"), got[:4], ref[:4]):
         e = nerr_slices(x.float().cpu().numpy(), y)
         assert e < (TOL if name == "dlog_alpha" else 1e-2), (name, e)
+
+
+@pytest.mark.parametrize("gate", ["std", "strong", "extreme"])
+def test_tc_bwd_saved_forward_operands(gate):
+    """gla_chunk_bwd_saved (reuses the forward's Q~, K~, P, (r, Gamma) and exact-path flags, forms only dP)
+    is bitwise identical to the recomputing backward, including when a chunk takes the exact fallback."""
+    p = problem(2, 2, 320, 256, 512, seed=31, gate=gate, h0=True, dfinal=True)
+    pc = cuda(p)
+    wf = G.fwd_workspace(pc["q"], pc["v"], pc["g"], 64, 16, "tc")
+    G.chunk_fwd(pc["q"], pc["k"], pc["v"], pc["g"], 64, 16, pc["h0"], True, "tc", workspace=wf)
+    a = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, pc["h0"], pc["dfinal"], True, "tc")
+    b = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, pc["h0"], pc["dfinal"], True, "tc",
+                    fwd_workspace=wf)
+    torch.cuda.synchronize()
+    for x, y, n in zip(a, b, ("dq", "dk", "dv", "dlog_alpha", "dh0")):
+        assert torch.equal(x, y), n
+    if gate == "std":   # (the recomputing backward is checked against the oracle for every gate elsewhere)
+        ref = oracle_bwd(p)
+        for name, x, y in zip(("dq", "dk", "dv", "dlog_alpha", "dh0"), b, ref):
+            assert nerr_slices(x.float().cpu().numpy(), y) < TOL, name

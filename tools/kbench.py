@@ -18,12 +18,12 @@ o = torch.empty(B, H, T, V, dtype=q.dtype, device="cuda")
 gr = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), torch.empty(q.shape, device="cuda"), None)
 for _ in range(3):
     G.chunk_fwd(q, k, v, g, out=o, workspace=wf)
-    G.chunk_bwd(q, k, v, g, do, grads=gr, workspace=wb)
+    G.chunk_bwd(q, k, v, g, do, grads=gr, workspace=wb, fwd_workspace=wf)
 torch.cuda.synchronize()
 G.profile(True)
 for _ in range(10):
     G.chunk_fwd(q, k, v, g, out=o, workspace=wf)
-    G.chunk_bwd(q, k, v, g, do, grads=gr, workspace=wb)
+    G.chunk_bwd(q, k, v, g, do, grads=gr, workspace=wb, fwd_workspace=wf)
 torch.cuda.synchronize()
 res = G.profile_read()
 tot = 0.0
