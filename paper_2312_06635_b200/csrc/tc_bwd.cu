@@ -705,6 +705,9 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     const int m0 = blockIdx.x * 64, bh = blockIdx.y;
     const int mc = m0 + 16 * cg;      // this thread's 16 channels [mc, mc+16)
     const int NC = T / CH;
+    // Segment blockIdx.z: chunks [i_lo, i_hi].  The exact carries at every ANCH-th chunk boundary (cpart) make the
+    // segments independent, so they run as separate CTAs (more, shorter CTAs: better wave balance).
+    const int i_lo = blockIdx.z * ANCH, i_hi = min(NC, i_lo + ANCH) - 1;
     const size_t head_row = (size_t)bh * T;
     auto issue = [&](int i) {         // all input tiles of chunk i into stage i % NS
         uint8_t* st = sm + (i % RC::NS) * RC::STAGE;
@@ -729,19 +732,24 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         mbar_init(&bar[1], 1);
         fence_mbar_init();
         prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmG); prefetch_tmap(&tmDQP); prefetch_tmap(&tmDKP);
-        for (int s2 = 0; s2 < RC::NS && NC - 1 - s2 >= 0; ++s2) issue(NC - 1 - s2);
+        for (int s2 = 0; s2 < RC::NS && i_hi - s2 >= i_lo; ++s2) issue(i_hi - s2);
     }
-    if (tid < 64) {
+    if (tid < 64) {   // carry entering the segment from above: the final-state term, or the exact anchor
         float c0 = 0.f;
-        if (stdot)
-            for (int j = 0; j < NVT; ++j) c0 += stdot[((size_t)j * BH + bh) * K + m0 + tid];
+        if (i_hi == NC - 1) {
+            if (stdot)
+                for (int j = 0; j < NVT; ++j) c0 += stdot[((size_t)j * BH + bh) * K + m0 + tid];
+        } else {
+            const size_t a2 = (i_hi + 1) / ANCH - 1;
+            for (int j = 0; j < NVT; ++j) c0 += cpart[((a2 * NVT + j) * BH + bh) * K + m0 + tid];
+        }
         carry_s[tid] = c0;
     }
     __syncthreads();
     uint32_t uses[2] = {0u, 0u};
     // byte offset of 8 consecutive bf16 channels [c, c+8) of row t in a SW128 [64][64] bf16 tile
     auto bf_off = [&](int c) { return (uint32_t)(t * 128 + ((((c >> 3) ^ (t & 7))) << 4)); };
-    for (int i = NC - 1; i >= 0; --i) {
+    for (int i = i_hi; i >= i_lo; --i) {
         const int sidx = i % RC::NS;
         const uint8_t* st = sm + sidx * RC::STAGE;
         if (tid < 64 && i + 1 < NC && (i + 1) % ANCH == 0) {   // exact carry rowsum(H_{i+1} (.) dH_{i+1})
@@ -824,7 +832,7 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             *reinterpret_cast<uint4*>(dk + ix + 8 * u) = ok;
         }
         __syncthreads();                   // everyone has read b and the stage buffers
-        if (tid == 0 && i - RC::NS >= 0) issue(i - RC::NS);   // refill this stage two chunks ahead
+        if (tid == 0 && i - RC::NS >= i_lo) issue(i - RC::NS);   // refill this stage two chunks ahead
 #pragma unroll
         for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = x[u];
         __syncthreads();
@@ -1832,7 +1840,7 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         if ((e = make_map_2d_ex(&mDKP, dkp, 2, prow, K, 64, 64, true)) != cudaSuccess) return e;
         const float* sd = p.dfinal ? stdot : nullptr;
         __nv_bfloat16 *dq_ = (__nv_bfloat16*)p.dq, *dk_ = (__nv_bfloat16*)p.dk;
-        const dim3 rg(K / 64, BH);
+        const dim3 rg(K / 64, BH, (NC + ANCH - 1) / ANCH);
 #define GLA_RED(N)                                                                                                  \
     case N:                                                                                                         \
         if ((e = cudaFuncSetAttribute(k_bwd_reduce_tma<K, N, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
