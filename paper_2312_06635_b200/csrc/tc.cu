@@ -41,6 +41,15 @@ bool supported(int B, int H, int T, int K, int V, int C, int c, int qkv_dtype, i
 
 bool fwd_is_split() { return !use_fused(); }
 
+bool saved_anchors() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("GLA_SERIAL_WALKS");
+        v = (s && s[0] == '1') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 cudaError_t fwd(const Problem& p, cudaStream_t st) {
     if (p.mode != 0) return simt::fwd(p, st);
     return use_fused() ? fwd_tc(p, st) : fwd2_tc(p, st);

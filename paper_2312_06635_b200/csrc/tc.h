@@ -14,14 +14,19 @@ cudaError_t bwd(const BwdProblem& p, cudaStream_t st);
 size_t fwd_ws(int B, int H, int T, int K, int V, int C);
 size_t bwd_ws(int B, int H, int T, int K, int V, int C);
 // 2-D bf16 TMA map over a [rows][cols] row-major tensor, box {64 cols, 64 rows}, optional 128B swizzle.
+// d log alpha carry re-anchored from exact states every ANCH chunks (R12).
+constexpr int ANCH = 8;
 // The per-chunk operands a TC forward (tc_fwd2.cu) leaves in its workspace, reused by the backward.
 struct FwdSaved {
     const void *Qt, *Kt, *Pm;     // Q~hi, K~hi [B*H*T, K] bf16; P [B*H*T, 64] bf16
     const float* stats;           // (r, Gamma) per (b,h, chunk) [B*H, T/64, 2, K] fp32
     const int* flags;             // per-chunk exact-path flags [B*H, T/64]
+    const void* anch;             // bf16(H_i e^{r_i}) at chunks i = ANCH, 2 ANCH, ...: [(T/64-1)/ANCH, B*H, V, K]
 };
 FwdSaved fwd2_saved(const void* ws, int B, int H, int T, int K);
 bool fwd_is_split();              // false when GLA_FWD_FUSED=1 selected the single fused forward
+bool saved_anchors();             // false when GLA_SERIAL_WALKS=1: the forward saves no anchor states and the
+                                  // backward walks run one after the other (A/B measurements)
 
 // Number of SMs of the current device (cached; persistent kernels size their grids with it).
 int num_sms();

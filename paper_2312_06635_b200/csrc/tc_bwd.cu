@@ -19,6 +19,7 @@
 // gradient instead (no host synchronisation).
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -37,7 +38,6 @@ constexpr int VT = 128;
 constexpr int NTH = 256;
 constexpr float L2E = 1.4426950408889634f;
 constexpr float GUARD = 60.f;
-constexpr int ANCH = 8;   // d log alpha carry re-anchored from exact states every ANCH chunks
 }  // namespace
 
 template <int K>
@@ -1265,7 +1265,7 @@ k_bwd_dq2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUten
                 tc_fence_after();
             }
             named_bar_sync(1, DC::NST);
-            __nv_bfloat16* arow = (i > 0 && i % ANCH == 0)
+            __nv_bfloat16* arow = (anch && i > 0 && i % ANCH == 0)   // (NULL: the forward saved them)
                 ? anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K : nullptr;
             state_pass2<K>(tS, lane_base, half, vrow, fsb, fy, sSB, arow);
             fence_async_smem();
@@ -1757,6 +1757,30 @@ static cudaError_t launch_bwd(const BwdProblem& p, cudaStream_t st) {
 }
 
 // Split backward: prep + TMA-fed walks + reduce (+ exact CUDA-core fallback behind the guard flag).
+// Per-device side stream (non-blocking, created once) and per-thread fork/join events for running the two
+// backward walks concurrently.  Returns nullptr if creation fails (the caller then stays on one stream).
+static cudaStream_t side_stream() {
+    static cudaStream_t streams[64] = {};
+    static std::mutex mu;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!streams[dev]) {
+        cudaStream_t s = nullptr;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        streams[dev] = s;
+    }
+    return streams[dev];
+}
+static cudaEvent_t fork_event(int which) {
+    thread_local cudaEvent_t evs[64][2] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (!evs[dev][which] && cudaEventCreateWithFlags(&evs[dev][which], cudaEventDisableTiming) != cudaSuccess)
+        return nullptr;
+    return evs[dev][which];
+}
+
 template <int K, typename TG>
 static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     const int BH = p.B * p.H, NVT = p.V / VT, NC = p.T / CH;
@@ -1769,10 +1793,12 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     float* stats = (float*)w; w += al1k((size_t)BH * NC * 2 * K * 4);
     const bool saved = p.fwd_ws != nullptr && fwd_is_split();
     const int* fflags = nullptr;
-    if (saved) {   // the forward's Q~hi, K~hi, P and (r, Gamma): only dP is left to form
+    const __nv_bfloat16* saved_anch = nullptr;
+    if (saved) {   // the forward's Q~hi, K~hi, P, (r, Gamma) and anchor states: only dP is left to form
         const FwdSaved f = fwd2_saved(p.fwd_ws, p.B, p.H, p.T, K);
         Qt = (__nv_bfloat16*)f.Qt; Kt = (__nv_bfloat16*)f.Kt; Pm = (__nv_bfloat16*)f.Pm;
         stats = (float*)f.stats; fflags = f.flags;
+        if (saved_anchors()) saved_anch = (const __nv_bfloat16*)f.anch;
     }
     uint8_t* ws = w;
     int* flag = (int*)ws;
@@ -1818,15 +1844,33 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
             p.T, p.V, NC, nitems);
     }
     const dim3 grid(NVT, BH);
+    // With the forward's anchors the two walks are independent: the dq walk runs on the library's side stream
+    // concurrently with the dkv walk (each is 256 one-per-SM CTAs, 1.73 waves alone on 148 SMs).
+    cudaStream_t sq = st;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    if (saved_anch) {
+        sq = side_stream();
+        if (!sq || !(ev_in = fork_event(0)) || !(ev_out = fork_event(1))) sq = st;
+    }
+    if (sq != st) {
+        if ((e = cudaEventRecord(ev_in, st)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(sq, ev_in, 0)) != cudaSuccess) return e;
+    }
     {
-        GLA_PROF("tc::bwd_dq", st);
-        k_bwd_dq2<K><<<grid, DqCfg<K>::NTHR, BWalkCfg<K>::SMEM, st>>>(mK, mDP, mV, mD, stats, p.h0, p.dfinal, dqp,
-                                                            p.dfinal ? stdot : nullptr, anch, flag, p.T, p.V);
+        GLA_PROF("tc::bwd_dq", sq);
+        k_bwd_dq2<K><<<grid, DqCfg<K>::NTHR, BWalkCfg<K>::SMEM, sq>>>(mK, mDP, mV, mD, stats, p.h0, p.dfinal, dqp,
+                                                                    p.dfinal ? stdot : nullptr,
+                                                                    saved_anch ? nullptr : anch, flag, p.T, p.V);
     }
     {
         GLA_PROF("tc::bwd_dkv", st);
-        k_bwd_dkv2<K><<<grid, DkvCfg<K>::NTHR, BWalkCfg<K>::SMEM, st>>>(mQ, mK, mP, mDP, mV, mD, mDV, stats, p.dfinal, dkp, p.dh0,
-                                                             anch, cpart, flag, p.T, p.V);
+        k_bwd_dkv2<K><<<grid, DkvCfg<K>::NTHR, BWalkCfg<K>::SMEM, st>>>(mQ, mK, mP, mDP, mV, mD, mDV, stats, p.dfinal,
+                                                                      dkp, p.dh0, saved_anch ? saved_anch : anch, cpart,
+                                                                      flag, p.T, p.V);
+    }
+    if (sq != st) {
+        if ((e = cudaEventRecord(ev_out, sq)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(st, ev_out, 0)) != cudaSuccess) return e;
     }
     {
         GLA_PROF("tc::bwd_reduce", st);

@@ -262,7 +262,8 @@ __global__ void __launch_bounds__(StateCfg<K>::NTHR, 1)
 k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmV,
             const __grid_constant__ CUtensorMap tmO, const float* __restrict__ stats, const int* __restrict__ flags,
-            const float* __restrict__ h0, float* __restrict__ final_state, int T, int V) {
+            const float* __restrict__ h0, float* __restrict__ final_state, __nv_bfloat16* __restrict__ anch, int T,
+            int V) {
     using Cfg = StateCfg<K>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_align1k(smem_raw);
@@ -372,6 +373,8 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
             named_bar_sync(1, Cfg::NST);       // fsb / fy visible
             const uint32_t sba = tSB + lane_base + cbeg / 2;
+            __nv_bfloat16* arow = (anch && i > 0 && i % ANCH == 0 && !slow)
+                ? anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K : nullptr;
 #pragma unroll
             for (int s = 0; s < K / 64; ++s) { // 32-column slices of this thread's K/2 channels
                 const int cb = cbeg + 32 * s;
@@ -403,6 +406,11 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     }
                 }
                 tmem_st16(sba + 16 * s, pk);
+                if (arow)                      // exact state for the backward's d log alpha anchors
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        *reinterpret_cast<uint4*>(arow + cb + 8 * u) =
+                            make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
             }
             tmem_wait_st();
             tc_fence_before();
@@ -529,10 +537,12 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 // ---------------------------------------------------------------------------------------------------------------
 static size_t al(size_t x) { return (x + 1023) & ~size_t(1023); }
 
+static size_t n_anch(int T) { const int NC = T / CH; return NC > 1 ? (size_t)(NC - 1) / ANCH : 0; }
+
 size_t fwd2_ws(int B, int H, int T, int K, int V) {
     const size_t BH = (size_t)B * H, NC = T / CH;
     return al(BH * T * K * 2) * 2 + al(BH * T * 64 * 2) + al(BH * NC * 2 * K * 4) + al(BH * NC * 4) +
-           al(BH * T * K * 4);
+           al(BH * T * K * 4) + al(n_anch(T) * BH * V * K * 2);
 }
 
 FwdSaved fwd2_saved(const void* ws, int B, int H, int T, int K) {
@@ -543,7 +553,9 @@ FwdSaved fwd2_saved(const void* ws, int B, int H, int T, int K) {
     f.Kt = w; w += al(rows * K * 2);
     f.Pm = w; w += al(rows * 64 * 2);
     f.stats = (const float*)w; w += al(BH * NC * 2 * K * 4);
-    f.flags = (const int*)w;
+    f.flags = (const int*)w; w += al(BH * NC * 4);
+    w += al(rows * K * 4);                // bws (exact-path cumsums)
+    f.anch = w;
     return f;
 }
 
@@ -556,7 +568,8 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     __nv_bfloat16* Pm = (__nv_bfloat16*)w; w += al(rows * 64 * 2);
     float* stats = (float*)w; w += al(BH * NC * 2 * K * 4);
     int* flags = (int*)w; w += al(BH * NC * 4);
-    float* bws = (float*)w;
+    float* bws = (float*)w; w += al(rows * K * 4);
+    __nv_bfloat16* anch = (__nv_bfloat16*)w;
     CUtensorMap mQ, mK, mP, mV, mO;
     cudaError_t e;
     if ((e = make_map_2d(&mQ, Qt, rows, K, true)) != cudaSuccess) return e;
@@ -580,7 +593,7 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     {
         GLA_PROF("tc::fwd_state", st);
         k_fwd_state<K><<<dim3(p.V / VT, (unsigned)BH), StateCfg<K>::NTHR, StateCfg<K>::SMEM, st>>>(
-            mQ, mK, mP, mV, mO, stats, flags, p.h0, p.final_state, p.T, p.V);
+            mQ, mK, mP, mV, mO, stats, flags, p.h0, p.final_state, saved_anchors() ? anch : nullptr, p.T, p.V);
     }
     return cudaGetLastError();
 }
