@@ -1848,7 +1848,7 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     // concurrently with the dkv walk (each is 256 one-per-SM CTAs, 1.73 waves alone on 148 SMs).
     cudaStream_t sq = st;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-    if (saved_anch) {
+    if (saved_anch && !prof::enabled()) {   // (the launch tracer times kernels one at a time)
         sq = side_stream();
         if (!sq || !(ev_in = fork_event(0)) || !(ev_out = fork_event(1))) sq = st;
     }
