@@ -275,7 +275,7 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
     float* fy = fsb + K;
     float* pend = fy + K;
-    __shared__ uint64_t bar_q[2], bar_k[2], bar_vp[2], bar_sb, bar_s, bar_oa, bar_ob, bar_ofree;
+    __shared__ uint64_t bar_q[2], bar_k[2], bar_vp[2], bar_sb, bar_s, bar_oa, bar_ob, bar_ofree, bar_anch;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int vt = blockIdx.x, bh = blockIdx.y;
@@ -312,7 +312,7 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         mbar_init(&bar_q[0], 1); mbar_init(&bar_q[1], 1); mbar_init(&bar_k[0], 1); mbar_init(&bar_k[1], 1);
         mbar_init(&bar_vp[0], 1); mbar_init(&bar_vp[1], 1);
         mbar_init(&bar_sb, 1); mbar_init(&bar_s, 1);
-        mbar_init(&bar_oa, 1); mbar_init(&bar_ob, 1); mbar_init(&bar_ofree, 1);
+        mbar_init(&bar_oa, 1); mbar_init(&bar_ob, 1); mbar_init(&bar_ofree, 1); mbar_init(&bar_anch, 1);
         fence_mbar_init();
         prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmP); prefetch_tmap(&tmV); prefetch_tmap(&tmO);
         load_q(0);
@@ -373,8 +373,6 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
             named_bar_sync(1, Cfg::NST);       // fsb / fy visible
             const uint32_t sba = tSB + lane_base + cbeg / 2;
-            __nv_bfloat16* arow = (anch && i > 0 && i % ANCH == 0 && !slow)
-                ? anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K : nullptr;
 #pragma unroll
             for (int s = 0; s < K / 64; ++s) { // 32-column slices of this thread's K/2 channels
                 const int cb = cbeg + 32 * s;
@@ -399,6 +397,8 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     if (tid == 0) TR(6, i);
                     mbar_wait(&bar_oa, (i - 1) & 1);
                     mbar_wait(&bar_ob, (i - 1) & 1);
+                    if (anch && i - 1 > 0 && (i - 1) % ANCH == 0)   // the epilogue has copied SB_{i-1} out
+                        mbar_wait(&bar_anch, ((i - 1) / ANCH - 1) & 1);
                     tc_fence_after();
                     if (tid == 0) {            // V/P of chunk i+1 into the buffers chunk i-1 used
                         TR(7, i);
@@ -406,11 +406,6 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     }
                 }
                 tmem_st16(sba + 16 * s, pk);
-                if (arow)                      // exact state for the backward's d log alpha anchors
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        *reinterpret_cast<uint4*>(arow + cb + 8 * u) =
-                            make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
             }
             tmem_wait_st();
             tc_fence_before();
@@ -488,6 +483,22 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 TR(4, i);
                 if (i + 2 < NC) load_q(i + 2);  // the O MMAs of chunk i (the readers of Q~ buffer b) are complete
                 tma_store_wait_read1();         // staging buffer b (chunk i-2) has been read
+            }
+            if (anch && i > 0 && i % ANCH == 0) {   // exact state SB_i = bf16(H_i e^{r}) for the backward's anchors
+                __nv_bfloat16* arow = anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K;
+#pragma unroll 1
+                for (int c0 = 0; c0 < K / 2; c0 += 32) {   // TMEM column c holds channels 2c, 2c+1
+                    uint32_t r[32];
+                    tmem_ld32(tSB + lane_base + c0, r);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        *reinterpret_cast<uint4*>(arow + 2 * c0 + 8 * u) =
+                            make_uint4(r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]);
+                }
+                tc_fence_before();
+                named_bar_sync(2, 128);
+                if (et == 0) mbar_arrive(&bar_anch);
             }
             uint8_t* dst = stg + b * 16384 + (vrow >> 6) * 8192 + (vrow & 63) * 2;
 #pragma unroll
