@@ -34,6 +34,22 @@ int num_sms() {
     return n;
 }
 
+int fwd_segments(int BH, int V, int NC) {
+    static int off = -1;
+    if (off < 0) {
+        const char* e = getenv("GLA_SEGMENTS");
+        off = (e && e[0] == '1') ? 1 : 0;
+    }
+    int S = 1;
+    if (off) return S;
+    // The summary walks cost ~0.8 of a full walk, so splitting pays only when the unsplit walk would use at most
+    // a quarter of the SMs (measured: S = 2 at 64 CTAs was slower; S = 4 at 32 CTAs 1.5x faster end to end).
+    const int nvt = V / 128 > 0 ? V / 128 : 1, ctas = BH * nvt;
+    if ((long)ctas * 4 > num_sms()) return 1;
+    while ((long)ctas * 2 * S <= num_sms() && NC % (2 * S) == 0 && NC / (2 * S) >= 8) S *= 2;
+    return S >= 4 ? S : 1;
+}
+
 bool supported(int B, int H, int T, int K, int V, int C, int c, int qkv_dtype, int gate_dtype) {
     (void)B; (void)H; (void)T; (void)gate_dtype;
     return qkv_dtype == 0 && (K == 64 || K == 128 || K == 256) && V % 128 == 0 && C == 64 && c > 0 && 64 % c == 0;

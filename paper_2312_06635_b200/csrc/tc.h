@@ -22,8 +22,22 @@ struct FwdSaved {
     const float* stats;           // (r, Gamma) per (b,h, chunk) [B*H, T/64, 2, K] fp32
     const int* flags;             // per-chunk exact-path flags [B*H, T/64]
     const void* anch;             // bf16(H_i e^{r_i}) at chunks i = ANCH, 2 ANCH, ...: [(T/64-1)/ANCH, B*H, V, K]
+    const float* h0v;             // segment-entry states [B*H*S, K, V] fp32 (S > 1 only)
+    int S;                        // intra-GPU segments the forward used (fwd_segments)
 };
-FwdSaved fwd2_saved(const void* ws, int B, int H, int T, int K);
+// Intra-GPU segment split of long sequences: the walks run over B*H*S virtual units of T/S
+// tokens each -- the same [B*H*T, D] rows, since unit (b,h) segment s starts at row (b*H + h)*T + s*T/S.
+// Used only when the unsplit walks fill at most a quarter of the SMs; S doubles while the split walks still fit
+// in one wave and every segment keeps >= 8 chunks (S >= 4, else 1).  GLA_SEGMENTS=1 disables it.
+int fwd_segments(int BH, int V, int NC);
+// Sequential state chains over the segments of every (b,h): forward H_{s+1} = e^{D_s} H_s + S_loc_s
+// (writes H_s for every s; H_0 = h0 or 0), backward dF_{s-1} = e^{D_s} dF_s + dh_loc_s (dF_{S-1} = dfinal or 0).
+// D_s = sum of the chunk totals Gamma over segment s, read from the prep statistics.
+cudaError_t seg_chain_fwd(const float* stats, const float* h0, const float* S_loc, float* Hv, int BH, int S, int NC,
+                          int K, int V, cudaStream_t st);
+cudaError_t seg_chain_bwd(const float* stats, const float* dfinal, const float* dh_loc, float* dFv, int BH, int S,
+                          int NC, int K, int V, cudaStream_t st);
+FwdSaved fwd2_saved(const void* ws, int B, int H, int T, int K, int V);
 bool fwd_is_split();              // false when GLA_FWD_FUSED=1 selected the single fused forward
 bool saved_anchors();             // false when GLA_SERIAL_WALKS=1: the forward saves no anchor states and the
                                   // backward walks run one after the other (A/B measurements)

@@ -1382,7 +1382,8 @@ k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
            const __grid_constant__ CUtensorMap tmDV, const float* __restrict__ stats,
            const float* __restrict__ dfinal, __nv_bfloat16* __restrict__ dkp, float* __restrict__ dh0,
            const __nv_bfloat16* __restrict__ anch, float* __restrict__ cpart, const int* __restrict__ flag, int T,
-           int V) {
+           int V, int emit) {
+    // emit == 0: adjoint-only walk (segment summaries dh_loc): only the Z update runs and only dh0 is written.
     using Cfg = BWalkCfg<K>;
     using DC = DkvCfg<K>;
     if (*flag) return;
@@ -1479,7 +1480,7 @@ k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
             }
             if (i < NC - 1) {                  // every MMA of chunk i+1 has completed
                 const int bd = i + 1;          // exact d log alpha carry at boundary bd over this V tile
-                const bool anc = bd % ANCH == 0;
+                const bool anc = anch != nullptr && bd % ANCH == 0;
                 const __nv_bfloat16* arow = anch + (((size_t)(bd / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K;
                 uint4 hv[2][4];
                 if (anc)                       // first two anchor slices in flight while the MMAs finish
@@ -1567,7 +1568,7 @@ k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
             if (i < NC - 1) mbar_wait(&bar_efree, (NC - 2 - i) & 1);
             tc_fence_after();
             if (lane == 0 && role == 0) TRB(3, i);
-            if (role == 0) {
+            if (role == 0 && emit) {
 #pragma unroll
                 for (int kk = 0; kk < K / 32; ++kk) {
                     const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
@@ -1580,12 +1581,13 @@ k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
 #pragma unroll
                 for (int kk = 0; kk < CH / 16; ++kk)
                     mma_bf16_w(tZ, sdesc_sw128(aD + kk * 2048, 8192, 1024), sdesc_sw128(aQ + kk * 2048, 8192, 1024), idZ, 1);
+                if (emit)
 #pragma unroll
                 for (int kk = K / 32; kk < K / 16; ++kk) {
                     const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
                     mma_bf16_w(tdvb, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aK + ob, 16, 1024), idV1, kk > K / 32);
                 }
-            } else if (role - 2 < K / 128) {
+            } else if (role - 2 < K / 128 && emit) {
                 const int hh = role - 2;
 #pragma unroll
                 for (int kk = 0; kk < VT / 16; ++kk) {
@@ -1615,6 +1617,12 @@ k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
                 TRB(5, i);
                 if (i > 0) load_inputs(i - 1); // every reader of the input tiles (the MMAs of chunk i) is done
                 tma_store_wait_read();         // dv staging of the previous chunk consumed
+            }
+            if (!emit) {                       // adjoint-only walk: no dv / dk to drain
+                tc_fence_before();
+                named_bar_sync(2, 128);
+                if (et == 0) mbar_arrive(&bar_efree);
+                continue;
             }
             named_bar_sync(2, 128);
             uint8_t* dst = stg + (vrow >> 6) * 8192 + (vrow & 63) * 2;
@@ -1686,12 +1694,14 @@ size_t bwd_tc_ws(int B, int H, int T, int K, int V, int C) {
     const size_t BH = (size_t)B * H, NVT = V / VT;
     size_t bytes = 256 + split_ws(B, H, T, K);                  // flag + split-backward scratch
     bytes += 2 * NVT * BH * T * K * sizeof(__nv_bfloat16);       // dq, dk partials
-    bytes += NVT * BH * K * sizeof(float);                       // S_T . dS_T partials
+    const int Smax = fwd_segments((int)BH, V, T / CH);
+    bytes += NVT * BH * Smax * K * sizeof(float);                // S_T . dS_T partials (per segment)
     bytes = (bytes + 255) & ~size_t(255);
     const size_t NA = (T / C > 1) ? (size_t)(T / C - 1) / ANCH : 0;
     bytes += NA * BH * V * K * sizeof(__nv_bfloat16);           // state anchors (bf16)
     bytes += NA * NVT * BH * K * sizeof(float);                 // anchor row-sum partials
     bytes = (bytes + 255) & ~size_t(255);
+    if (Smax > 1) bytes += 2 * BH * Smax * K * V * sizeof(float);   // per-segment d_final / d_initial states
     return bytes + simt::bwd_ws(B, H, T, K, V, C);              // exact-path fallback scratch
 }
 
@@ -1794,24 +1804,32 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     const bool saved = p.fwd_ws != nullptr && fwd_is_split();
     const int* fflags = nullptr;
     const __nv_bfloat16* saved_anch = nullptr;
+    const float* h0v = nullptr;
+    int S = 1;   // intra-GPU segments (the forward's choice; only with its saved segment-entry states)
     if (saved) {   // the forward's Q~hi, K~hi, P, (r, Gamma) and anchor states: only dP is left to form
-        const FwdSaved f = fwd2_saved(p.fwd_ws, p.B, p.H, p.T, K);
+        const FwdSaved f = fwd2_saved(p.fwd_ws, p.B, p.H, p.T, K, p.V);
         Qt = (__nv_bfloat16*)f.Qt; Kt = (__nv_bfloat16*)f.Kt; Pm = (__nv_bfloat16*)f.Pm;
         stats = (float*)f.stats; fflags = f.flags;
         if (saved_anchors()) saved_anch = (const __nv_bfloat16*)f.anch;
+        if (f.S > 1) { S = f.S; h0v = f.h0v; }
     }
+    const int BHv = BH * S, Tv = p.T / S;   // virtual units (segments) of the walks and the reduce
     uint8_t* ws = w;
     int* flag = (int*)ws;
     __nv_bfloat16* dqp = (__nv_bfloat16*)(ws + 256);
     __nv_bfloat16* dkp = dqp + (size_t)NVT * BH * p.T * K;
     float* stdot = (float*)(dkp + (size_t)NVT * BH * p.T * K);
-    size_t used = 256 + 2 * (size_t)NVT * BH * p.T * K * 2 + (size_t)NVT * BH * K * 4;
+    const int Smax = fwd_segments(BH, p.V, NC);
+    size_t used = 256 + 2 * (size_t)NVT * BH * p.T * K * 2 + (size_t)NVT * BH * Smax * K * 4;
     used = (used + 255) & ~size_t(255);
     const size_t NA = (NC > 1) ? (size_t)(NC - 1) / ANCH : 0;
     __nv_bfloat16* anch = (__nv_bfloat16*)(ws + used);
     float* cpart = (float*)(ws + used + NA * BH * p.V * K * 2);
     used += NA * BH * p.V * K * 2 + NA * NVT * BH * K * 4;
     used = (used + 255) & ~size_t(255);
+    float* dFv = (float*)(ws + used);                       // per-segment d_final_state (S > 1)
+    float* dhv = dFv + (Smax > 1 ? (size_t)BH * Smax * K * p.V : 0);   // per-segment dh0 / dh_loc
+    if (Smax > 1) used += 2 * (size_t)BH * Smax * K * p.V * 4;
     cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
     CUtensorMap mQ, mK, mP, mDP, mV, mD, mDV;
@@ -1843,7 +1861,23 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
             mQ, mK, mP, mDP, mV, mD, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k, (const TG*)p.g, stats, flag,
             p.T, p.V, NC, nitems);
     }
-    const dim3 grid(NVT, BH);
+    const dim3 grid(NVT, BHv);
+    const float* dfin = p.dfinal;
+    float* dh0w = p.dh0;
+    if (S > 1) {
+        // adjoint-only walks: every segment's d_initial_state with a zero d_final_state, then the reverse chain
+        // gives every segment's true d_final_state (the segment-entry states h0v come from the forward)
+        {
+            GLA_PROF("tc::bwd_dstate_summary", st);
+            k_bwd_dkv2<K><<<grid, DkvCfg<K>::NTHR, BWalkCfg<K>::SMEM, st>>>(
+                mQ, mK, mP, mDP, mV, mD, mDV, stats, nullptr, dkp, dhv, nullptr, cpart, flag, Tv, p.V, 0);
+        }
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if ((e = seg_chain_bwd(stats, p.dfinal, dhv, dFv, BH, S, NC, K, p.V, st)) != cudaSuccess) return e;
+        dfin = dFv;
+        dh0w = p.dh0 ? dhv : nullptr;
+    }
+    const float* h0w = S > 1 ? h0v : p.h0;
     // With the forward's anchors the two walks are independent: the dq walk runs on the library's side stream
     // concurrently with the dkv walk (each is 256 one-per-SM CTAs, 1.73 waves alone on 148 SMs).
     cudaStream_t sq = st;
@@ -1858,15 +1892,15 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     }
     {
         GLA_PROF("tc::bwd_dq", sq);
-        k_bwd_dq2<K><<<grid, DqCfg<K>::NTHR, BWalkCfg<K>::SMEM, sq>>>(mK, mDP, mV, mD, stats, p.h0, p.dfinal, dqp,
-                                                                    p.dfinal ? stdot : nullptr,
-                                                                    saved_anch ? nullptr : anch, flag, p.T, p.V);
+        k_bwd_dq2<K><<<grid, DqCfg<K>::NTHR, BWalkCfg<K>::SMEM, sq>>>(mK, mDP, mV, mD, stats, h0w, dfin, dqp,
+                                                                    dfin ? stdot : nullptr,
+                                                                    saved_anch ? nullptr : anch, flag, Tv, p.V);
     }
     {
         GLA_PROF("tc::bwd_dkv", st);
-        k_bwd_dkv2<K><<<grid, DkvCfg<K>::NTHR, BWalkCfg<K>::SMEM, st>>>(mQ, mK, mP, mDP, mV, mD, mDV, stats, p.dfinal,
-                                                                      dkp, p.dh0, saved_anch ? saved_anch : anch, cpart,
-                                                                      flag, p.T, p.V);
+        k_bwd_dkv2<K><<<grid, DkvCfg<K>::NTHR, BWalkCfg<K>::SMEM, st>>>(mQ, mK, mP, mDP, mV, mD, mDV, stats, dfin,
+                                                                      dkp, dh0w, saved_anch ? saved_anch : anch, cpart,
+                                                                      flag, Tv, p.V, 1);
     }
     if (sq != st) {
         if ((e = cudaEventRecord(ev_out, sq)) != cudaSuccess) return e;
@@ -1882,16 +1916,17 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
             return e;
         if ((e = make_map_2d_ex(&mDQP, dqp, 2, prow, K, 64, 64, true)) != cudaSuccess) return e;
         if ((e = make_map_2d_ex(&mDKP, dkp, 2, prow, K, 64, 64, true)) != cudaSuccess) return e;
-        const float* sd = p.dfinal ? stdot : nullptr;
+        const float* sd = dfin ? stdot : nullptr;
         __nv_bfloat16 *dq_ = (__nv_bfloat16*)p.dq, *dk_ = (__nv_bfloat16*)p.dk;
-        const dim3 rg(K / 64, BH, (NC + ANCH - 1) / ANCH);
+        const int NCv = NC / S;
+        const dim3 rg(K / 64, BHv, (NCv + ANCH - 1) / ANCH);
 #define GLA_RED(N)                                                                                                  \
     case N:                                                                                                         \
         if ((e = cudaFuncSetAttribute(k_bwd_reduce_tma<K, N, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                                       (int)RedCfg<N, TG>::SMEM)) != cudaSuccess)                                    \
             return e;                                                                                               \
         k_bwd_reduce_tma<K, N, TG><<<rg, 256, RedCfg<N, TG>::SMEM, st>>>(mQr, mKr, mGr, mDQP, mDKP, sd, dq_, dk_,   \
-                                                                          p.dg, cpart, flag, p.T, BH);              \
+                                                                          p.dg, cpart, flag, Tv, BHv);              \
         break;
         switch (NVT) {
             GLA_RED(1) GLA_RED(2) GLA_RED(4) GLA_RED(8)
@@ -1900,6 +1935,12 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
 #undef GLA_RED
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (S > 1 && p.dh0) {   // the first segment's d_initial_state of every (b,h)
+        const size_t KV = (size_t)K * p.V;
+        if ((e = cudaMemcpy2DAsync(p.dh0, KV * 4, dhv, S * KV * 4, KV * 4, BH, cudaMemcpyDeviceToDevice, st)) !=
+            cudaSuccess)
+            return e;
+    }
     BwdProblem sp = p;
     sp.ws = ws + used;
     sp.run_if = flag;

@@ -263,7 +263,9 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmV,
             const __grid_constant__ CUtensorMap tmO, const float* __restrict__ stats, const int* __restrict__ flags,
             const float* __restrict__ h0, float* __restrict__ final_state, __nv_bfloat16* __restrict__ anch, int T,
-            int V) {
+            int V, int emit) {
+    // emit == 0: state-only walk (segment summaries): the output MMAs, epilogue and Q~ loads are skipped and
+    // only final_state is produced (the barriers keep their arrivals so the schedule is unchanged).
     using Cfg = StateCfg<K>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_align1k(smem_raw);
@@ -315,10 +317,10 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         mbar_init(&bar_oa, 1); mbar_init(&bar_ob, 1); mbar_init(&bar_ofree, 1); mbar_init(&bar_anch, 1);
         fence_mbar_init();
         prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmP); prefetch_tmap(&tmV); prefetch_tmap(&tmO);
-        load_q(0);
+        if (emit) load_q(0);
         load_k(0);
         load_vp(0);
-        if (NC > 1) { load_q(1); load_k(1); load_vp(1); }
+        if (NC > 1) { if (emit) load_q(1); load_k(1); load_vp(1); }
     }
     tc_fence_before();
     __syncthreads();
@@ -453,15 +455,16 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const int b = i & 1;
             const uint32_t aQ = smem_u32(sQ + b * Cfg::OP);
             mbar_wait(&bar_sb, i & 1);
-            mbar_wait(&bar_q[b], (i >> 1) & 1);
+            if (emit) mbar_wait(&bar_q[b], (i >> 1) & 1);
             if (is_a) mbar_wait(&bar_vp[b], (i >> 1) & 1);
             if (i >= 1) mbar_wait(&bar_ofree, (i - 1) & 1);
             tc_fence_after();
             if (is_a && lane == 0) TR(3, i);
+            if (emit)
             for (int kk = k0; kk < k1; ++kk)
                 mma_bf16_ta_w(tD, tSB + 8 * kk, sdesc_sw128(aQ + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idO,
                               kk > k0);
-            if (is_a) {
+            if (is_a && emit) {
                 const uint32_t aV = smem_u32(sV + b * 16384), aP = smem_u32(sP + b * 8192);
 #pragma unroll
                 for (int kk = 0; kk < CH / 16; ++kk)
@@ -481,7 +484,7 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             tc_fence_after();
             if (et == 0) {
                 TR(4, i);
-                if (i + 2 < NC) load_q(i + 2);  // the O MMAs of chunk i (the readers of Q~ buffer b) are complete
+                if (emit && i + 2 < NC) load_q(i + 2);   // the O MMAs of chunk i (Q~ buffer b's readers) are complete
                 tma_store_wait_read1();         // staging buffer b (chunk i-2) has been read
             }
             if (anch && i > 0 && i % ANCH == 0) {   // exact state SB_i = bf16(H_i e^{r}) for the backward's anchors
@@ -499,6 +502,12 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 tc_fence_before();
                 named_bar_sync(2, 128);
                 if (et == 0) mbar_arrive(&bar_anch);
+            }
+            if (!emit) {                       // state-only walk: nothing to drain, keep the schedule
+                tc_fence_before();
+                named_bar_sync(2, 128);
+                if (et == 0) mbar_arrive(&bar_ofree);
+                continue;
             }
             uint8_t* dst = stg + b * 16384 + (vrow >> 6) * 8192 + (vrow & 63) * 2;
 #pragma unroll
@@ -552,11 +561,12 @@ static size_t n_anch(int T) { const int NC = T / CH; return NC > 1 ? (size_t)(NC
 
 size_t fwd2_ws(int B, int H, int T, int K, int V) {
     const size_t BH = (size_t)B * H, NC = T / CH;
+    const int S = fwd_segments((int)BH, V, (int)NC);
     return al(BH * T * K * 2) * 2 + al(BH * T * 64 * 2) + al(BH * NC * 2 * K * 4) + al(BH * NC * 4) +
-           al(BH * T * K * 4) + al(n_anch(T) * BH * V * K * 2);
+           al(BH * T * K * 4) + al(n_anch(T) * BH * V * K * 2) + (S > 1 ? 2 * al(BH * S * K * V * 4) : 0);
 }
 
-FwdSaved fwd2_saved(const void* ws, int B, int H, int T, int K) {
+FwdSaved fwd2_saved(const void* ws, int B, int H, int T, int K, int V) {
     const size_t BH = (size_t)B * H, NC = T / CH, rows = BH * T;
     const uint8_t* w = (const uint8_t*)ws;
     FwdSaved f;
@@ -566,7 +576,9 @@ FwdSaved fwd2_saved(const void* ws, int B, int H, int T, int K) {
     f.stats = (const float*)w; w += al(BH * NC * 2 * K * 4);
     f.flags = (const int*)w; w += al(BH * NC * 4);
     w += al(rows * K * 4);                // bws (exact-path cumsums)
-    f.anch = w;
+    f.anch = w; w += al(n_anch(T) * BH * V * K * 2);
+    f.S = fwd_segments((int)BH, V, (int)NC);
+    f.h0v = f.S > 1 ? (const float*)w : nullptr;
     return f;
 }
 
@@ -580,7 +592,10 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     float* stats = (float*)w; w += al(BH * NC * 2 * K * 4);
     int* flags = (int*)w; w += al(BH * NC * 4);
     float* bws = (float*)w; w += al(rows * K * 4);
-    __nv_bfloat16* anch = (__nv_bfloat16*)w;
+    __nv_bfloat16* anch = (__nv_bfloat16*)w; w += al(n_anch(p.T) * BH * p.V * K * 2);
+    const int S = fwd_segments((int)BH, p.V, (int)NC);
+    float* h0v = (float*)w; w += S > 1 ? al(BH * S * K * p.V * 4) : 0;   // segment-entry states (saved for bwd)
+    float* slv = (float*)w;                                              // segment summaries / final states
     CUtensorMap mQ, mK, mP, mV, mO;
     cudaError_t e;
     if ((e = make_map_2d(&mQ, Qt, rows, K, true)) != cudaSuccess) return e;
@@ -601,10 +616,36 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
             mQ, mK, mP, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k, (const TG*)p.g, stats, flags, bws, p.T,
             (int)NC, nitems);
     }
-    {
+    __nv_bfloat16* an = saved_anchors() ? anch : nullptr;
+    if (S == 1) {
         GLA_PROF("tc::fwd_state", st);
         k_fwd_state<K><<<dim3(p.V / VT, (unsigned)BH), StateCfg<K>::NTHR, StateCfg<K>::SMEM, st>>>(
-            mQ, mK, mP, mV, mO, stats, flags, p.h0, p.final_state, saved_anchors() ? anch : nullptr, p.T, p.V);
+            mQ, mK, mP, mV, mO, stats, flags, p.h0, p.final_state, an, p.T, p.V, 1);
+        return cudaGetLastError();
+    }
+    // Long sequences: B*H*S virtual units of T/S tokens (same rows).  (1) state-only walks give each segment's
+    // end state from a zero start, (2) the chain turns them into every segment's entry state, (3) the full walks
+    // run all segments in parallel from those states (P:516-518's two-stage scan, inside one GPU).
+    const int Tv = p.T / S;
+    const dim3 gv(p.V / VT, (unsigned)(BH * S));
+    {
+        GLA_PROF("tc::fwd_state_summary", st);
+        k_fwd_state<K><<<gv, StateCfg<K>::NTHR, StateCfg<K>::SMEM, st>>>(mQ, mK, mP, mV, mO, stats, flags, nullptr,
+                                                                         slv, nullptr, Tv, p.V, 0);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = seg_chain_fwd(stats, p.h0, slv, h0v, (int)BH, S, (int)NC, K, p.V, st)) != cudaSuccess) return e;
+    {
+        GLA_PROF("tc::fwd_state", st);
+        k_fwd_state<K><<<gv, StateCfg<K>::NTHR, StateCfg<K>::SMEM, st>>>(mQ, mK, mP, mV, mO, stats, flags, h0v,
+                                                                         p.final_state ? slv : nullptr, an, Tv, p.V, 1);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (p.final_state) {   // the last segment's end state of every (b,h)
+        const size_t KV = (size_t)K * p.V;
+        if ((e = cudaMemcpy2DAsync(p.final_state, KV * 4, slv + (S - 1) * KV, S * KV * 4, KV * 4, BH,
+                                   cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+            return e;
     }
     return cudaGetLastError();
 }
@@ -619,5 +660,78 @@ cudaError_t fwd2_tc(const Problem& p, cudaStream_t st) {
     }
 }
 
+}  // namespace tc
+}  // namespace gla
+
+// ---------------------------------------------------------------------------------------------------------------
+// Segment state chains (see tc.h).  One thread per (b,h, k, 4 v): the S-step chain is sequential, every element
+// independent; D_s is re-summed per thread from the statistics (S x NC/S floats, L2-resident).
+namespace gla {
+namespace tc {
+namespace {
+constexpr int SEG_CH = 64;
+__device__ __forceinline__ float seg_decay(const float* stats, int bh, int s, int NCs, int NC, int K, int k) {
+    float d = 0.f;
+    for (int c = s * NCs; c < (s + 1) * NCs; ++c) d += stats[((size_t)bh * NC + c) * 2 * K + K + k];
+    return d;
+}
+__global__ void k_seg_chain_fwd(const float* __restrict__ stats, const float* __restrict__ h0,
+                                const float* __restrict__ S_loc, float* __restrict__ Hv, int BH, int S, int NC, int K,
+                                int V) {
+    const size_t n = (size_t)BH * K * (V / 4);
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n) return;
+    const int bh = (int)(idx / ((size_t)K * (V / 4)));
+    const size_t rem = idx % ((size_t)K * (V / 4));
+    const int k = (int)(rem / (V / 4)), v = 4 * (int)(rem % (V / 4));
+    const size_t KV = (size_t)K * V, off = (size_t)k * V + v;
+    float4 H = h0 ? *reinterpret_cast<const float4*>(h0 + bh * KV + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int NCs = NC / S;
+    for (int s = 0; s < S; ++s) {
+        *reinterpret_cast<float4*>(Hv + ((size_t)bh * S + s) * KV + off) = H;
+        if (s + 1 < S) {
+            const float a = __expf(seg_decay(stats, bh, s, NCs, NC, K, k));
+            const float4 l = *reinterpret_cast<const float4*>(S_loc + ((size_t)bh * S + s) * KV + off);
+            H = make_float4(a * H.x + l.x, a * H.y + l.y, a * H.z + l.z, a * H.w + l.w);
+        }
+    }
+}
+__global__ void k_seg_chain_bwd(const float* __restrict__ stats, const float* __restrict__ dfinal,
+                                const float* __restrict__ dh_loc, float* __restrict__ dFv, int BH, int S, int NC, int K,
+                                int V) {
+    const size_t n = (size_t)BH * K * (V / 4);
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n) return;
+    const int bh = (int)(idx / ((size_t)K * (V / 4)));
+    const size_t rem = idx % ((size_t)K * (V / 4));
+    const int k = (int)(rem / (V / 4)), v = 4 * (int)(rem % (V / 4));
+    const size_t KV = (size_t)K * V, off = (size_t)k * V + v;
+    float4 F = dfinal ? *reinterpret_cast<const float4*>(dfinal + bh * KV + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int NCs = NC / S;
+    for (int s = S - 1; s >= 0; --s) {
+        *reinterpret_cast<float4*>(dFv + ((size_t)bh * S + s) * KV + off) = F;
+        if (s > 0) {
+            const float a = __expf(seg_decay(stats, bh, s, NCs, NC, K, k));
+            const float4 l = *reinterpret_cast<const float4*>(dh_loc + ((size_t)bh * S + s) * KV + off);
+            F = make_float4(a * F.x + l.x, a * F.y + l.y, a * F.z + l.z, a * F.w + l.w);
+        }
+    }
+}
+}  // namespace
+
+cudaError_t seg_chain_fwd(const float* stats, const float* h0, const float* S_loc, float* Hv, int BH, int S, int NC,
+                          int K, int V, cudaStream_t st) {
+    const size_t n = (size_t)BH * K * (V / 4);
+    GLA_PROF("tc::seg_chain", st);
+    k_seg_chain_fwd<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stats, h0, S_loc, Hv, BH, S, NC, K, V);
+    return cudaGetLastError();
+}
+cudaError_t seg_chain_bwd(const float* stats, const float* dfinal, const float* dh_loc, float* dFv, int BH, int S,
+                          int NC, int K, int V, cudaStream_t st) {
+    const size_t n = (size_t)BH * K * (V / 4);
+    GLA_PROF("tc::seg_chain", st);
+    k_seg_chain_bwd<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stats, dfinal, dh_loc, dFv, BH, S, NC, K, V);
+    return cudaGetLastError();
+}
 }  // namespace tc
 }  // namespace gla

@@ -8,7 +8,7 @@ import torch
 import oracle
 import synth
 from paper_2312_06635_b200 import binding as G
-from tests.helpers import cuda, nerr_slices, oracle_bwd, problem
+from tests.helpers import cuda, nerr_slices, oracle_bwd, oracle_fwd, problem
 from tests.test_gpu_parity import check_bwd
 
 pytestmark = pytest.mark.gpu
@@ -109,3 +109,24 @@ def test_tc_bwd_saved_forward_operands(gate):
         ref = oracle_bwd(p)
         for name, x, y in zip(("dq", "dk", "dv", "dlog_alpha", "dh0"), b, ref):
             assert nerr_slices(x.float().cpu().numpy(), y) < TOL, name
+
+
+@pytest.mark.parametrize("B,H,T,K,V", [(1, 2, 4096, 256, 512), (1, 1, 4096, 128, 256)])
+def test_tc_segmented_long_sequence(B, H, T, K, V):
+    """Few (b,h) units at long T: the forward and the saved backward split every sequence into S segments run in
+    parallel (state-only / adjoint-only summary walks + segment chains).  Outputs, final state and
+    every gradient (h0, d_final_state given) against the fp64 oracle."""
+    p = problem(B, H, T, K, V, seed=41, h0=True, dfinal=True)
+    pc = cuda(p)
+    wf = G.fwd_workspace(pc["q"], pc["v"], pc["g"], 64, 16, "tc")
+    o, fs = G.chunk_fwd(pc["q"], pc["k"], pc["v"], pc["g"], 64, 16, pc["h0"], True, "tc", workspace=wf)
+    got = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, pc["h0"], pc["dfinal"], True, "tc",
+                      fwd_workspace=wf)
+    torch.cuda.synchronize()
+    ro, rfs = oracle_fwd(p)
+    assert nerr_slices(o.float().cpu().numpy(), ro) < TOL
+    assert nerr_slices(fs.cpu().numpy(), rfs) < TOL
+    ref = oracle_bwd(p)
+    for name, x, y in zip(("dq", "dk", "dv", "dlog_alpha", "dh0"), got, ref):
+        e = nerr_slices(x.float().cpu().numpy(), y)
+        assert e < TOL, (name, e)
