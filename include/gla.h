@@ -120,6 +120,7 @@ int gla_chunk_bwd_saved(const gla_desc *d, const void *q, const void *k, const v
  * in:  q_t, k_t [B,H,K] and v_t [B,H,V] (dtype); log_alpha_t [B,H,K] (gate_dtype)
  * in/out: state [B,H,K,V] fp32 (updated in place)
  * out: out_t [B,H,V] (dtype)
+ * errors: GLA_ERR_SHAPE also for K > 1024.
  */
 int gla_recurrent_step(int B, int H, int K, int V, int dtype, int gate_dtype,
                        const void *q_t, const void *k_t, const void *v_t, const void *log_alpha_t,

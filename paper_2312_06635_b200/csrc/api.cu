@@ -171,7 +171,7 @@ int gla_chunk_bwd(const gla_desc* d, const void* q, const void* k, const void* v
 
 int gla_recurrent_step(int B, int H, int K, int V, int dtype, int gate_dtype, const void* q_t, const void* k_t,
                        const void* v_t, const void* log_alpha_t, float* state, void* out_t, void* stream) {
-    if (B < 0 || H < 0 || K <= 0 || V <= 0) return GLA_ERR_SHAPE;
+    if (B < 0 || H < 0 || K <= 0 || V <= 0 || K > 1024) return GLA_ERR_SHAPE;   // (K <= 1024: staged in smem)
     if (!ok_dtype(dtype) || !ok_dtype(gate_dtype)) return GLA_ERR_DTYPE;
     int s = check_ptrs({q_t, k_t, v_t, log_alpha_t, state, out_t}, {});
     if (s) return s;

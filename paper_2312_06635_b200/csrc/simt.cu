@@ -517,48 +517,58 @@ __global__ void __launch_bounds__(NT) k_bwd_dv(const TQ* __restrict__ q, const T
 }
 
 // ---------------------------------------------------------------------------------------------
-// Decode step.  grid (ceil(V/128), BH), 256 threads = 32 column-quads x 8 row groups.
-template <typename TQ, typename TG>
-__global__ void __launch_bounds__(256) k_step(const TQ* __restrict__ q, const TQ* __restrict__ k,
-                                              const TQ* __restrict__ v, const TG* __restrict__ g,
-                                              float* __restrict__ state, TQ* __restrict__ out, int K, int V) {
-    __shared__ float red[8][128];
+constexpr int MAXK_STEP = 1024;
+// Decode step.  grid (ceil(V / (4 CQ)), BH), CQ x RG threads = CQ column-quads x RG row groups; every thread
+// streams its K / RG state rows (float4 read-modify-write, rows of a warp contiguous), o reduced over the row
+// groups in shared memory (fixed order).  Small batches use narrow tiles (CQ = 8, RG = 16) to spread the state
+// over more SMs; large batches the wide ones (CQ = 32, RG = 8).
+template <typename TQ, typename TG, int CQ, int RG>
+__global__ void __launch_bounds__(CQ * RG) k_step(const TQ* __restrict__ q, const TQ* __restrict__ k,
+                                                  const TQ* __restrict__ v, const TG* __restrict__ g,
+                                                  float* __restrict__ state, TQ* __restrict__ out, int K, int V) {
+    __shared__ float red[RG][4 * CQ];
+    __shared__ float sa[MAXK_STEP], sk[MAXK_STEP], sq[MAXK_STEP];   // alpha, k, q of this unit (staged once)
     const int bh = blockIdx.y, tid = threadIdx.x;
-    const int col = blockIdx.x * 128 + (tid % 32) * 4;
-    const int rg = tid / 32;
+    const int col = blockIdx.x * 4 * CQ + (tid % CQ) * 4;
+    const int rg = tid / CQ;
+    for (int m = tid; m < K; m += CQ * RG) {
+        sa[m] = expf(to_f(g[(size_t)bh * K + m]));
+        sk[m] = to_f(k[(size_t)bh * K + m]);
+        sq[m] = to_f(q[(size_t)bh * K + m]);
+    }
     float o[4] = {0.f, 0.f, 0.f, 0.f};
     float vv[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) vv[u] = (col + u < V) ? to_f(v[(size_t)bh * V + col + u]) : 0.f;
-    for (int m = rg; m < K; m += 8) {
-        const float a = expf(to_f(g[(size_t)bh * K + m]));
-        const float km = to_f(k[(size_t)bh * K + m]);
-        const float qm = to_f(q[(size_t)bh * K + m]);
+    const bool vec = col + 3 < V && (V % 4) == 0;
+    __syncthreads();
+    for (int m = rg; m < K; m += RG) {
+        const float a = sa[m], km = sk[m], qm = sq[m];
         float* row = state + ((size_t)bh * K + m) * V;
-        if (col + 3 < V && (V % 4) == 0) {
-            float4 s = *reinterpret_cast<float4*>(row + col);
-            s.x = a * s.x + km * vv[0]; s.y = a * s.y + km * vv[1];
-            s.z = a * s.z + km * vv[2]; s.w = a * s.w + km * vv[3];
-            *reinterpret_cast<float4*>(row + col) = s;
-            o[0] += qm * s.x; o[1] += qm * s.y; o[2] += qm * s.z; o[3] += qm * s.w;
+        if (vec) {
+            float4 s4 = *reinterpret_cast<float4*>(row + col);
+            s4.x = a * s4.x + km * vv[0]; s4.y = a * s4.y + km * vv[1];
+            s4.z = a * s4.z + km * vv[2]; s4.w = a * s4.w + km * vv[3];
+            *reinterpret_cast<float4*>(row + col) = s4;
+            o[0] += qm * s4.x; o[1] += qm * s4.y; o[2] += qm * s4.z; o[3] += qm * s4.w;
         } else {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if (col + u < V) {
-                    const float s = a * row[col + u] + km * vv[u];
-                    row[col + u] = s;
-                    o[u] += qm * s;
+                    const float sv = a * row[col + u] + km * vv[u];
+                    row[col + u] = sv;
+                    o[u] += qm * sv;
                 }
         }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) red[rg][(tid % 32) * 4 + u] = o[u];
+    for (int u = 0; u < 4; ++u) red[rg][(tid % CQ) * 4 + u] = o[u];
     __syncthreads();
-    if (tid < 128) {
-        float a = 0.f;
-        for (int r = 0; r < 8; ++r) a += red[r][tid];
-        const int c = blockIdx.x * 128 + tid;
-        if (c < V) out[(size_t)bh * V + c] = from_f<TQ>(a);
+    if (tid < 4 * CQ) {
+        float acc = 0.f;
+        for (int r = 0; r < RG; ++r) acc += red[r][tid];
+        const int c = blockIdx.x * 4 * CQ + tid;
+        if (c < V) out[(size_t)bh * V + c] = from_f<TQ>(acc);
     }
 }
 
@@ -703,8 +713,12 @@ static cudaError_t step_impl(int BH, int K, int V, const void* q, const void* k,
                              float* state, void* out, cudaStream_t st) {
     {
         GLA_PROF("simt::k_step", st);
-        k_step<TQ, TG><<<dim3(cdiv(V, 128), BH), 256, 0, st>>>((const TQ*)q, (const TQ*)k, (const TQ*)v,
-                                                              (const TG*)g, state, (TQ*)out, K, V);
+        if ((long)BH * cdiv(V, 128) < 2 * 148)   // few units: narrow tiles, more CTAs
+            k_step<TQ, TG, 8, 16><<<dim3(cdiv(V, 32), BH), 128, 0, st>>>((const TQ*)q, (const TQ*)k, (const TQ*)v,
+                                                                       (const TG*)g, state, (TQ*)out, K, V);
+        else
+            k_step<TQ, TG, 32, 8><<<dim3(cdiv(V, 128), BH), 256, 0, st>>>((const TQ*)q, (const TQ*)k, (const TQ*)v,
+                                                                        (const TG*)g, state, (TQ*)out, K, V);
     }
     return cudaGetLastError();
 }

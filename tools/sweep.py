@@ -61,7 +61,8 @@ for name, (B, H, T, K, V) in [("340M (configs[1])", (8, 4, 2048, 128, 256)), ("1
     del q, k, v, g, do, wf, wb, o, gr
     torch.cuda.empty_cache()
 
-print("\n## Decode: gla_recurrent_step (fp32 state read + written once per step), H = 4, K = 256, V = 512\n")
+print("\n## Decode: gla_recurrent_step (fp32 state read + written once per step), H = 4, K = 256, V = 512; "
+      "20 steps per CUDA graph replay\n")
 print("| B | us / step | M head-steps/s | state GB/s | % of HBM copy peak |")
 print("|---|---|---|---|---|")
 for B in (1, 16, 64, 256):
@@ -72,6 +73,17 @@ for B in (1, 16, 64, 256):
     gt = torch.nn.functional.logsigmoid(torch.randn(B, H, K, device="cuda")) / 16
     st = torch.zeros(B, H, K, V, device="cuda")
     out = torch.empty(B, H, V, device="cuda", dtype=torch.bfloat16)
-    ms = timeit(lambda: G.recurrent_step(qt, kt, vt, gt, st, out), n=50, warm=10)
+    # 20 steps captured in a CUDA graph and replayed: device time per step without host launch overhead
+    s_ = torch.cuda.Stream()
+    s_.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s_):
+        for _ in range(3):
+            G.recurrent_step(qt, kt, vt, gt, st, out)
+    torch.cuda.current_stream().wait_stream(s_)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for _ in range(20):
+            G.recurrent_step(qt, kt, vt, gt, st, out)
+    ms = timeit(graph.replay, n=20, warm=3) / 20
     by = B * H * K * V * 8
     print(f"| {B} | {ms * 1e3:.1f} | {B * H / ms / 1e3:.2f} | {by / ms / 1e6:.0f} | {100 * by / ms / 1e6 / HBM:.1f} |")
