@@ -79,8 +79,6 @@ def kernel_algo(name, B, H, T, K, V, C, c, g_bytes=4, e=2):
         "tc::bwd_dkv": (u * (2 * e * K + 2 * e * V + 2 * P + st + e * V + nvt * e * K),
                         u * (6 * K * V + (C + 1) * K + (C + c) * V)),
         "tc::bwd_reduce": (u * (2 * nvt * e * K + 2 * e * K + g_bytes * K + 2 * e * K + 4 * K), 0),
-        # fused single-kernel forward (GLA_FWD_FUSED=1): q, k, v, g in; o out
-        "tc::fwd": (u * (2 * e * K + e * V + g_bytes * K + e * V), u * fwd_f),
         # fp32 CUDA-core kernels
         "simt::k_fwd_state": (u * (2 * e * K + e * V + g_bytes * K + e * V + 4 * C), u * 4 * K * V + u * (C + 1) * V),
         "simt::k_intra_P": (u * (2 * e * K + g_bytes * K + 4 * C), u * (C + 1) * K),
@@ -343,7 +341,7 @@ def main():
         pass
 
     def traffic_of(name):
-        key = {"tc::fwd": "k_fwd<", "tc::fwd_prep": "k_fwd_prep<", "tc::fwd_state": "k_fwd_state<",
+        key = {"tc::fwd_prep": "k_fwd_prep<", "tc::fwd_state": "k_fwd_state<",
                "tc::bwd_prep": "k_bwd_prep<", "tc::bwd_dq": "k_bwd_dq2<", "tc::bwd_dkv": "k_bwd_dkv2<",
                "tc::bwd_reduce": "k_bwd_reduce_tma<", "tc::bwd_dp": "k_bwd_dp"}.get(name)
         for n, v in ncu.items():

@@ -1,4 +1,4 @@
-// tc.cu -- dispatch for the tensor-core path (tcgen05 kernels in tc_fwd.cu / tc_bwd.cu).
+// tc.cu -- dispatch for the tensor-core path (tcgen05 kernels in tc_fwd2.cu / tc_bwd.cu), segment choice.
 #include <cstdlib>
 
 #include "tc.h"
@@ -6,20 +6,9 @@
 namespace gla {
 namespace tc {
 
-cudaError_t fwd_tc(const Problem& p, cudaStream_t st);     // single fused kernel (tc_fwd.cu)
-size_t fwd_tc_ws(int B, int H, int T, int K, int V);
 cudaError_t fwd2_tc(const Problem& p, cudaStream_t st);    // prep + state kernels (tc_fwd2.cu), the default
 size_t fwd2_ws(int B, int H, int T, int K, int V);
 
-// GLA_FWD_FUSED=1 selects the single fused forward kernel (kept for A/B measurements).
-static bool use_fused() {
-    static int v = -1;
-    if (v < 0) {
-        const char* s = getenv("GLA_FWD_FUSED");
-        v = (s && s[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
 cudaError_t bwd_tc(const BwdProblem& p, cudaStream_t st);
 size_t bwd_tc_ws(int B, int H, int T, int K, int V, int C);
 bool bwd_tc_supported(int K, int V);
@@ -55,7 +44,7 @@ bool supported(int B, int H, int T, int K, int V, int C, int c, int qkv_dtype, i
     return qkv_dtype == 0 && (K == 64 || K == 128 || K == 256) && V % 128 == 0 && C == 64 && c > 0 && 64 % c == 0;
 }
 
-bool fwd_is_split() { return !use_fused(); }
+bool fwd_is_split() { return true; }
 
 bool saved_anchors() {
     static int v = -1;
@@ -68,7 +57,7 @@ bool saved_anchors() {
 
 cudaError_t fwd(const Problem& p, cudaStream_t st) {
     if (p.mode != 0) return simt::fwd(p, st);
-    return use_fused() ? fwd_tc(p, st) : fwd2_tc(p, st);
+    return fwd2_tc(p, st);
 }
 
 // Backward: tcgen05 kernels for K in {128, 256}; K = 64 (and dstate summaries) run the CUDA-core kernels.
@@ -78,8 +67,7 @@ cudaError_t bwd(const BwdProblem& p, cudaStream_t st) {
 }
 
 size_t fwd_ws(int B, int H, int T, int K, int V, int C) {
-    const size_t a = fwd_tc_ws(B, H, T, K, V), b = fwd2_ws(B, H, T, K, V);
-    return a > b ? a : b;
+    return fwd2_ws(B, H, T, K, V);
 }
 size_t bwd_ws(int B, int H, int T, int K, int V, int C) {
     return bwd_tc_supported(K, V) ? bwd_tc_ws(B, H, T, K, V, C) : simt::bwd_ws(B, H, T, K, V, C);

@@ -38,7 +38,7 @@ cudaError_t seg_chain_fwd(const float* stats, const float* h0, const float* S_lo
 cudaError_t seg_chain_bwd(const float* stats, const float* dfinal, const float* dh_loc, float* dFv, int BH, int S,
                           int NC, int K, int V, cudaStream_t st);
 FwdSaved fwd2_saved(const void* ws, int B, int H, int T, int K, int V);
-bool fwd_is_split();              // false when GLA_FWD_FUSED=1 selected the single fused forward
+bool fwd_is_split();              // the forward leaves its per-chunk operands in the workspace (always)
 bool saved_anchors();             // false when GLA_SERIAL_WALKS=1: the forward saves no anchor states and the
                                   // backward walks run one after the other (A/B measurements)
 

@@ -9,14 +9,16 @@
 //   dH_i = e^{r} (.) [ e^{Gamma-r} dH_{i+1} + Q~^T dO ]                      (reverse state pass)
 //   d log alpha_t = sum_{s>=t} (q dq - k dk)_s + rowsum(S_T (.) dS_T)
 // The d_k x d_v states are V-tiled (128 value columns per CTA, TMEM-resident), so the contractions over V
-// (dO H^T, V dH^T, dO V^T) are computed per V tile; dq and dk are linear in them, so each CTA emits its
-// per-tile partial (bf16) and k_bwd_reduce sums the V/128 partials in a fixed order (deterministic).
-//   k_bwd_dq  : forward walk, recomputes H in TMEM          -> dq partials, S_T . dS_T partials
-//   k_bwd_dkv : reverse walk, dH in TMEM                    -> dv (final), dk partials, dh0
-//   k_bwd_reduce: per (b,h, 32 channels), reverse over chunks -> dq, dk, d log alpha (carry across chunks)
-// If any chunk's half-chunk log decay exceeds the factorisation guard, k_bwd_dq raises a device flag; the
-// TC kernels that follow then do nothing and the exact fp32 CUDA-core kernels (simt.cu) produce every
-// gradient instead (no host synchronisation).
+// (dO H^T, V dH^T) are computed per V tile; dq and dk are linear in them, so each CTA emits its per-tile
+// partial (bf16) and the reduce kernel sums the V/128 partials in a fixed order (deterministic).
+//   k_bwd_prep / k_bwd_dp : chunk-parallel operands (Q~hi, K~hi, P, dP, statistics; or only dP when the
+//                           forward's operands are reused, gla_chunk_bwd_saved)
+//   k_bwd_dq2  : forward walk, recomputes H in TMEM          -> dq partials, S_T . dS_T partials, anchors
+//   k_bwd_dkv2 : reverse walk, dH in TMEM                    -> dv (final), dk partials, anchor carries, dh0
+//   k_bwd_reduce_tma : per (b,h, 64 channels, segment)       -> dq, dk, d log alpha (carry across chunks)
+// If any chunk's half-chunk log decay exceeds the factorisation guard the prep (or the forward) raises a device
+// flag; the TC kernels that follow then do nothing and a gate kernel tail-launches the exact fp32 CUDA-core
+// backward (simt.cu), which produces every gradient instead (no host synchronisation).
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -40,30 +42,6 @@ constexpr float L2E = 1.4426950408889634f;
 constexpr float GUARD = 60.f;
 }  // namespace
 
-template <int K>
-struct BwdCfg {
-    using Tl = Tile<K>;                                // operand-build thread mapping (tc_build.cuh)
-    static constexpr int KB = K / 64;
-    static constexpr int NH = K / 128;                 // 128-channel halves (M=128 MMAs over channels)
-    // shared memory (bytes, 1024-aligned blocks)
-    static constexpr uint32_t OP_BYTES = KB * 8192;    // [KB][64 t][128 B] bf16 operand (Q~ or K~, hi only)
-    static constexpr uint32_t SB_BYTES = KB * 16384;   // [KB][128 v][128 B]
-    static constexpr uint32_t OFF_Q = 0;
-    static constexpr uint32_t OFF_K = OFF_Q + OP_BYTES;
-    static constexpr uint32_t OFF_SB = OFF_K + OP_BYTES;
-    static constexpr uint32_t OFF_V = OFF_SB + SB_BYTES;    // [2][64 t][128 B]
-    static constexpr uint32_t OFF_DO = OFF_V + 16384;       // [2][64 t][128 B]
-    static constexpr uint32_t OFF_P = OFF_DO + 16384;       // [64 t][128 B]
-    static constexpr uint32_t OFF_DP = OFF_P + 8192;        // [64 t][128 B]
-    static constexpr uint32_t OFF_STG = OFF_DP + 8192;      // [2][64 s][128 B] dv staging
-    static constexpr uint32_t OFF_F = OFF_STG + 16384;      // fsb[K], fy[K], pend[K], red[4][K]
-    static constexpr uint32_t SMEM = OFF_F + 4 * (3 * K + 4 * K) + 1024;
-    static_assert(Tl::RG * K * 4 <= 8192, "gtot aliases the 8 KB P buffer");
-    static_assert(SMEM <= 232448, "dynamic shared memory");
-    // TMEM columns
-    static constexpr uint32_t COL_S = 0, COL_A = K, COL_B = K + 64, COL_C = K + 128;
-};
-
 // ---------------------------------------------------------------------------------------------------------------
 // Shared pieces: the TMEM state pass and the accumulator epilogues.
 // M=64 accumulator [64 t x 64 s] in TMEM -> causal-masked bf16 rows [t][s] (SW128) in smem.
@@ -86,591 +64,6 @@ __device__ __forceinline__ void m64_epilogue(uint32_t tcol, uint32_t lane_base, 
         for (int u = 0; u < 8; ++u)
             *reinterpret_cast<uint4*>(dst + sw128_off(t, 8 * u)) =
                 make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-    }
-}
-
-// [ch x t] accumulator halves (M=128 over channels) -> bf16 partial rows [t][ch] in global memory.
-template <int K>
-__device__ __forceinline__ void partial_epilogue(uint32_t tcol, uint32_t lane_base, int lq, int lane, int warp,
-                                                 __nv_bfloat16* out, size_t row0) {
-    constexpr int NH = K / 128;
-    // work items: (half hh, t-range); 8 warps -> lq quarter of channels, warp/4 -> item
-    for (int item = warp >> 2; item < NH * 2; item += 2) {
-        const int hh = item >> 1, tpart = item & 1;
-        uint32_t r[32];
-        tmem_ld32(tcol + 64 * hh + lane_base + 32 * tpart, r);
-        tmem_wait_ld();
-        const int ch = 128 * hh + 32 * lq + lane;
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            out[(row0 + 32 * tpart + j) * K + ch] = __float2bfloat16_rn(__uint_as_float(r[j]));
-    }
-}
-
-// ---------------------------------------------------------------------------------------------------------------
-// k_bwd_dq: forward walk.  grid (V/128, BH).
-template <int K, typename TG>
-__global__ void __launch_bounds__(NTH, 1)
-k_bwd_dq(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
-         const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g, const float* __restrict__ h0,
-         const float* __restrict__ dfinal, __nv_bfloat16* __restrict__ dqp, float* __restrict__ stdot,
-         __nv_bfloat16* __restrict__ anch, int* __restrict__ flag, int T, int V) {
-    using Cfg = BwdCfg<K>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = smem_align1k(smem_raw);
-    uint8_t* sK = sm + Cfg::OFF_K;
-    uint8_t* sSB = sm + Cfg::OFF_SB;
-    uint8_t* sV = sm + Cfg::OFF_V;
-    uint8_t* sD = sm + Cfg::OFF_DO;
-    uint8_t* sdP = sm + Cfg::OFF_DP;
-    float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
-    float* fy = fsb + K;
-    float* pend = fy + K;
-    float* red = pend + K;
-    float* gtot = reinterpret_cast<float*>(sm + Cfg::OFF_P);   // cumsum exchange (P is unused here)
-    __shared__ uint64_t bar_in, bar_m1, bar_m2;
-    __shared__ uint32_t tmem_base;
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int vt = blockIdx.x, bh = blockIdx.y;
-    const int v0 = vt * VT;
-    const int NC = T / CH;
-    const int oc = tid % Cfg::Tl::NOCT, rg = tid / Cfg::Tl::NOCT;
-    const int ch0 = 8 * oc, row0 = rg * Cfg::Tl::RPG;
-
-    if (warp == 0) tmem_alloc(&tmem_base, 512);
-    if (tid == 0) {
-        mbar_init(&bar_in, 1);
-        mbar_init(&bar_m1, 1);
-        mbar_init(&bar_m2, 1);
-        fence_mbar_init();
-        prefetch_tmap(&tmV);
-        prefetch_tmap(&tmD);
-    }
-    for (int m = tid; m < K; m += NTH) pend[m] = 0.f;
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tm = tmem_base;
-    const uint32_t tS = tm + Cfg::COL_S, tdP = tm + Cfg::COL_A, tdq = tm + Cfg::COL_B;
-    const int lq = warp & 3, half = warp >> 2;
-    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
-    const int vrow = 32 * lq + lane;
-
-    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
-        uint32_t r[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            r[j] = __float_as_uint(h0 ? h0[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
-        tmem_st32(tS + lane_base + c0, r);
-    }
-    tmem_wait_st();
-
-    const size_t head_row = (size_t)bh * T;
-    ChunkRegs<K> R;
-    load_chunk<K, TG, false, true>(R, nullptr, k, g, head_row, row0, ch0);
-
-    const uint32_t idDP = idesc_bf16(64, 64, 0, 0);      // dP = dO V^T (K-major both, contraction over v)
-    const uint32_t idDQ = idesc_bf16(128, 64, 1, 0);     // dq^T: A = SB (MN-major [ch][v]) / K~ (MN [ch][s])
-    const uint32_t idS = idesc_bf16(128, K, 1, 1);       // Y[v][ch] += V^T K~
-    const uint32_t aK = smem_u32(sK), aSB = smem_u32(sSB), aV = smem_u32(sV), aD = smem_u32(sD),
-                   adP = smem_u32(sdP);
-    bool any_slow = false;
-
-    for (int i = 0; i < NC; ++i) {
-        const uint32_t ph = i & 1;
-        const int trow = (int)(head_row + (size_t)i * CH);
-        if (tid == 0) {
-            mbar_expect_tx(&bar_in, 32768);
-            tma_load_2d(sV, &tmV, &bar_in, v0, trow);
-            tma_load_2d(sV + 8192, &tmV, &bar_in, v0 + 64, trow);
-            tma_load_2d(sD, &tmD, &bar_in, v0, trow);
-            tma_load_2d(sD + 8192, &tmD, &bar_in, v0 + 64, trow);
-        }
-        float2 off[4], rr[4], Gm[4];
-        chunk_cumsum<K>(R, gtot, rg, ch0, off, rr, Gm);
-        bool bad_here = false;
-        if (rg == 0)
-#pragma unroll
-            for (int p = 0; p < 4; ++p)
-                bad_here |= (-rr[p].x > GUARD) | (-rr[p].y > GUARD) | (rr[p].x - Gm[p].x > GUARD) |
-                            (rr[p].y - Gm[p].y > GUARD);
-        any_slow |= __syncthreads_or(bad_here) != 0;
-        if (rg == 0) {   // SB = bf16(H_i e^{r}); Y <- H_i e^{r}; next pending = Gamma - r
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int m = ch0 + u;
-                const float r_ = (u & 1) ? rr[u >> 1].y : rr[u >> 1].x, G_ = (u & 1) ? Gm[u >> 1].y : Gm[u >> 1].x;
-                fsb[m] = ex2f((pend[m] + r_) * L2E);
-                fy[m] = fsb[m];
-                pend[m] = G_ - r_;
-            }
-        }
-        float2 refk[4];
-#pragma unroll
-        for (int p = 0; p < 4; ++p) refk[p] = make_float2(L2E * rr[p].x, L2E * rr[p].y);
-        uint8_t* kbase = sK + (ch0 >> 6) * 8192;
-        const int col = ch0 & 63;
-#pragma unroll
-        for (int r = 0; r < Cfg::Tl::RPG; ++r) {
-            float2 b[4];
-#pragma unroll
-            for (int p = 0; p < 4; ++p) b[p] = add2(R.g[r][p], off[p]);
-            scaled_row(R.k[r], b, refk, -1.f, kbase + sw128_off(row0 + r, col), nullptr);
-        }
-        if (i + 1 < NC) load_chunk<K, TG, false, true>(R, nullptr, k, g, head_row + (size_t)(i + 1) * CH, row0, ch0);
-        __syncthreads();
-        // SB = bf16(H_i e^r); Y <- H_i e^r.  Every ANCH chunks SB is also kept in HBM: k_bwd_dkv forms
-        // rowsum(H_i (.) dH_i) from it, the exact d log alpha carry at that boundary (R12).
-        __nv_bfloat16* arow = (i > 0 && i % ANCH == 0)
-            ? anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K : nullptr;
-        state_pass2<K>(tS, lane_base, half, vrow, fsb, fy, sSB, arow);
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-            mbar_wait(&bar_in, ph);
-            tc_fence_after();
-#pragma unroll
-            for (int kk = 0; kk < VT / 16; ++kk) {   // dP_j = dO_j V_j^T over this V tile
-                const uint32_t o = (kk >> 2) * 8192 + (kk & 3) * 32;
-                mma_bf16(tdP, sdesc_sw128(aD + o, 16, 1024), sdesc_sw128(aV + o, 16, 1024), idDP, kk > 0);
-            }
-#pragma unroll
-            for (int hh = 0; hh < Cfg::NH; ++hh)
-#pragma unroll
-                for (int kk = 0; kk < VT / 16; ++kk) {   // dq^T[ch][t] = SB^T dO^T (contraction over v)
-                    const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-                    mma_bf16(tdq + 64 * hh, sdesc_sw128(aSB + 2 * hh * 16384 + kk * 2048, 16384, 1024),
-                             sdesc_sw128(aD + ob, 16, 1024), idDQ, kk > 0);
-                }
-#pragma unroll
-            for (int kk = 0; kk < CH / 16; ++kk)       // Y += V^T K~   (state passing)
-                mma_bf16(tS, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aK + kk * 2048, 8192, 1024),
-                         idS, 1);
-            mma_commit(&bar_m1);
-        }
-        mbar_wait(&bar_m1, ph);
-        tc_fence_after();
-        if (half == 0) m64_epilogue(tdP, lane_base, lq, lane, sdP);
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-#pragma unroll
-            for (int hh = 0; hh < Cfg::NH; ++hh)
-#pragma unroll
-                for (int kk = 0; kk < CH / 16; ++kk)   // dq^T += K~^T dP^T (contraction over s)
-                    mma_bf16(tdq + 64 * hh, sdesc_sw128(aK + 2 * hh * 8192 + kk * 2048, 8192, 1024),
-                             sdesc_sw128(adP + kk * 32, 16, 1024), idDQ, 1);
-            mma_commit(&bar_m2);
-        }
-        mbar_wait(&bar_m2, ph);
-        tc_fence_after();
-        partial_epilogue<K>(tdq, lane_base, lq, lane, warp, dqp + (size_t)vt * gridDim.y * T * K, head_row + (size_t)i * CH);
-        tc_fence_before();
-        __syncthreads();
-    }
-    if (tid == 0 && any_slow) atomicOr(flag, 1);
-    // S_T . dS_T partial over this V tile: red[lq][ch] = sum over 32 lanes of S_T[ch][v] dfinal[ch][v]
-    if (dfinal) {
-        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tS + lane_base + c0, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                float x = __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E) *
-                          dfinal[((size_t)bh * K + c0 + j) * V + v0 + vrow];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-                if (lane == 0) red[lq * K + c0 + j] = x;
-            }
-        }
-        __syncthreads();
-        for (int m = tid; m < K; m += NTH)
-            stdot[((size_t)vt * gridDim.y + bh) * K + m] = red[m] + red[K + m] + red[2 * K + m] + red[3 * K + m];
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) tmem_dealloc(tm, 512);
-}
-
-// ---------------------------------------------------------------------------------------------------------------
-// k_bwd_dkv: reverse walk.  grid (V/128, BH).
-template <int K, typename TG>
-__global__ void __launch_bounds__(NTH, 1)
-k_bwd_dkv(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
-          const __grid_constant__ CUtensorMap tmDV, const __nv_bfloat16* __restrict__ q,
-          const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g, const float* __restrict__ dfinal,
-          __nv_bfloat16* __restrict__ dkp, float* __restrict__ dh0, const __nv_bfloat16* __restrict__ anch,
-          float* __restrict__ cpart, const int* __restrict__ flag, int T, int V) {
-    using Cfg = BwdCfg<K>;
-    if (*flag) return;   // exact CUDA-core path takes over
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = smem_align1k(smem_raw);
-    uint8_t* sQ = sm + Cfg::OFF_Q;
-    uint8_t* sK = sm + Cfg::OFF_K;
-    uint8_t* sSB = sm + Cfg::OFF_SB;
-    uint8_t* sV = sm + Cfg::OFF_V;
-    uint8_t* sD = sm + Cfg::OFF_DO;
-    uint8_t* sP = sm + Cfg::OFF_P;
-    uint8_t* sdP = sm + Cfg::OFF_DP;
-    uint8_t* stg = sm + Cfg::OFF_STG;
-    float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
-    float* fy = fsb + K;
-    float* pend = fy + K;
-    float* red = pend + K;                         // [4][K] anchor row-sum partials
-    float* gtot = reinterpret_cast<float*>(sP);   // cumsum exchange; P is free at chunk start
-    __shared__ uint64_t bar_in, bar_m1, bar_m2;
-    __shared__ uint32_t tmem_base;
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int vt = blockIdx.x, bh = blockIdx.y;
-    const int v0 = vt * VT;
-    const int NC = T / CH;
-    const int oc = tid % Cfg::Tl::NOCT, rg = tid / Cfg::Tl::NOCT;
-    const int ch0 = 8 * oc, row0 = rg * Cfg::Tl::RPG;
-
-    if (warp == 0) tmem_alloc(&tmem_base, 512);
-    if (tid == 0) {
-        mbar_init(&bar_in, 1);
-        mbar_init(&bar_m1, 1);
-        mbar_init(&bar_m2, 1);
-        fence_mbar_init();
-        prefetch_tmap(&tmV);
-        prefetch_tmap(&tmD);
-        prefetch_tmap(&tmDV);
-    }
-    for (int m = tid; m < K; m += NTH) pend[m] = 0.f;
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tm = tmem_base;
-    const uint32_t tZ = tm + Cfg::COL_S, tP = tm + Cfg::COL_A, tdP = tm + Cfg::COL_B, tdk = tm + Cfg::COL_A,
-                   tdv = tm + Cfg::COL_C;
-    const int lq = warp & 3, half = warp >> 2;
-    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
-    const int vrow = 32 * lq + lane;
-
-    // Z = dH_T = d_final_state (or 0), pending exponent 0
-    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
-        uint32_t r[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            r[j] = __float_as_uint(dfinal ? dfinal[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
-        tmem_st32(tZ + lane_base + c0, r);
-    }
-    tmem_wait_st();
-
-    const size_t head_row = (size_t)bh * T;
-    ChunkRegs<K> R;
-    load_chunk<K, TG, true, true>(R, q, k, g, head_row + (size_t)(NC - 1) * CH, row0, ch0);
-
-    const uint32_t idP = idesc_bf16(64, 64, 0, 0);        // P = Q~ K~^T ; dP = dO V^T
-    const uint32_t idZ = idesc_bf16(128, K, 1, 1);        // Z[v][ch] += dO^T Q~
-    const uint32_t idV1 = idesc_bf16(128, 64, 0, 0);      // dv^T[v][s] = dSB K~^T  (A K-major, B K-major)
-    const uint32_t idV2 = idesc_bf16(128, 64, 1, 1);      // dv^T += dO^T P          (A MN, B MN)
-    const uint32_t idK1 = idesc_bf16(128, 64, 1, 0);      // dk^T[ch][s] = dSB^T V^T (A MN, B K-major)
-    const uint32_t idK2 = idesc_bf16(128, 64, 1, 1);      // dk^T += Q~^T dP         (A MN, B MN)
-    const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aSB = smem_u32(sSB), aV = smem_u32(sV), aD = smem_u32(sD),
-                   aP = smem_u32(sP), adP = smem_u32(sdP);
-
-    for (int i = NC - 1; i >= 0; --i) {
-        const uint32_t ph = (NC - 1 - i) & 1;
-        const int trow = (int)(head_row + (size_t)i * CH);
-        if (tid == 0) {
-            mbar_expect_tx(&bar_in, 32768);
-            tma_load_2d(sV, &tmV, &bar_in, v0, trow);
-            tma_load_2d(sV + 8192, &tmV, &bar_in, v0 + 64, trow);
-            tma_load_2d(sD, &tmD, &bar_in, v0, trow);
-            tma_load_2d(sD + 8192, &tmD, &bar_in, v0 + 64, trow);
-        }
-        float2 off[4], rr[4], Gm[4];
-        chunk_cumsum<K>(R, gtot, rg, ch0, off, rr, Gm);
-        if (rg == 0) {   // dSB = bf16(dH_{i+1} e^{Gamma - r}); Z <- same; next pending = r
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int m = ch0 + u;
-                const float r_ = (u & 1) ? rr[u >> 1].y : rr[u >> 1].x, G_ = (u & 1) ? Gm[u >> 1].y : Gm[u >> 1].x;
-                fsb[m] = ex2f((pend[m] + G_ - r_) * L2E);
-                fy[m] = fsb[m];
-                pend[m] = r_;
-            }
-        }
-        float2 refq[4], refk[4];
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            refq[p] = make_float2(-L2E * rr[p].x, -L2E * rr[p].y);
-            refk[p] = make_float2(L2E * rr[p].x, L2E * rr[p].y);
-        }
-        uint8_t* qbase = sQ + (ch0 >> 6) * 8192;
-        uint8_t* kbase = sK + (ch0 >> 6) * 8192;
-        const int col = ch0 & 63;
-#pragma unroll
-        for (int r = 0; r < Cfg::Tl::RPG; ++r) {
-            const int t = row0 + r;
-            float2 b[4];
-#pragma unroll
-            for (int p = 0; p < 4; ++p) b[p] = add2(R.g[r][p], off[p]);
-            scaled_row(R.q[r], b, refq, 1.f, qbase + sw128_off(t, col), nullptr);
-            scaled_row(R.k[r], b, refk, -1.f, kbase + sw128_off(t, col), nullptr);
-        }
-        if (i > 0) load_chunk<K, TG, true, true>(R, q, k, g, head_row + (size_t)(i - 1) * CH, row0, ch0);
-        if (tid == 0 && i < NC - 1) tma_store_wait_read();   // dv staging of the previous chunk consumed
-        __syncthreads();
-        state_pass2<K>(tZ, lane_base, half, vrow, fsb, fy, sSB);   // dSB = bf16(dH~), Z <- dH~
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-            mbar_wait(&bar_in, ph);
-            tc_fence_after();
-#pragma unroll
-            for (int kk = 0; kk < K / 16; ++kk) {   // P = Q~ K~^T
-                const uint32_t o = (kk >> 2) * 8192 + (kk & 3) * 32;
-                mma_bf16(tP, sdesc_sw128(aQ + o, 16, 1024), sdesc_sw128(aK + o, 16, 1024), idP, kk > 0);
-            }
-#pragma unroll
-            for (int kk = 0; kk < VT / 16; ++kk) {  // dP_j = dO_j V_j^T
-                const uint32_t o = (kk >> 2) * 8192 + (kk & 3) * 32;
-                mma_bf16(tdP, sdesc_sw128(aD + o, 16, 1024), sdesc_sw128(aV + o, 16, 1024), idP, kk > 0);
-            }
-#pragma unroll
-            for (int kk = 0; kk < K / 16; ++kk) {   // dv^T = dSB K~^T  (inter)
-                const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-                mma_bf16(tdv, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aK + ob, 16, 1024), idV1, kk > 0);
-            }
-#pragma unroll
-            for (int kk = 0; kk < CH / 16; ++kk)      // Z += dO^T Q~   (reverse state pass)
-                mma_bf16(tZ, sdesc_sw128(aD + kk * 2048, 8192, 1024), sdesc_sw128(aQ + kk * 2048, 8192, 1024), idZ,
-                         1);
-            mma_commit(&bar_m1);
-        }
-        mbar_wait(&bar_m1, ph);
-        tc_fence_after();
-        m64_epilogue(half == 0 ? tP : tdP, lane_base, lq, lane, half == 0 ? sP : sdP);
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-#pragma unroll
-            for (int kk = 0; kk < CH / 16; ++kk)      // dv^T += dO^T P   (intra)
-                mma_bf16(tdv, sdesc_sw128(aD + kk * 2048, 8192, 1024), sdesc_sw128(aP + kk * 2048, 8192, 1024), idV2,
-                         1);
-#pragma unroll
-            for (int hh = 0; hh < Cfg::NH; ++hh) {
-#pragma unroll
-                for (int kk = 0; kk < VT / 16; ++kk) {   // dk^T = dSB^T V^T (inter, contraction over v)
-                    const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-                    mma_bf16(tdk + 64 * hh, sdesc_sw128(aSB + 2 * hh * 16384 + kk * 2048, 16384, 1024),
-                             sdesc_sw128(aV + ob, 16, 1024), idK1, kk > 0);
-                }
-#pragma unroll
-                for (int kk = 0; kk < CH / 16; ++kk)     // dk^T += Q~^T dP  (intra, contraction over t)
-                    mma_bf16(tdk + 64 * hh, sdesc_sw128(aQ + 2 * hh * 8192 + kk * 2048, 8192, 1024),
-                             sdesc_sw128(adP + kk * 2048, 8192, 1024), idK2, 1);
-            }
-            mma_commit(&bar_m2);
-        }
-        mbar_wait(&bar_m2, ph);
-        tc_fence_after();
-        // dv^T [v][s] -> bf16 staging [box][s][64 v] -> TMA store
-        {
-            uint32_t r[32];
-            tmem_ld32(tdv + lane_base + 32 * half, r);
-            tmem_wait_ld();
-            uint8_t* dst = stg + (vrow >> 6) * 8192 + (vrow & 63) * 2;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                *reinterpret_cast<__nv_bfloat16*>(dst + (32 * half + j) * 128) =
-                    __float2bfloat16_rn(__uint_as_float(r[j]));
-        }
-        partial_epilogue<K>(tdk, lane_base, lq, lane, warp, dkp + (size_t)vt * gridDim.y * T * K,
-                            head_row + (size_t)i * CH);
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            tma_store_2d(&tmDV, stg, v0, trow);
-            tma_store_2d(&tmDV, stg + 8192, v0 + 64, trow);
-            tma_store_commit();
-        }
-        if (i > 0 && i % ANCH == 0) {
-            // exact carry at boundary i over this V tile: sum_v H_i[ch][v] dH_i[ch][v]
-            //   = sum_v SB_anchor[v][ch] * Z[v][ch]   (SB = bf16(H_i e^{r_i}), dH_i = e^{r_i} Z)
-            const __nv_bfloat16* arow = anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K;
-            for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
-                uint32_t r[32];
-                tmem_ld32(tZ + lane_base + c0, r);
-                uint4 hv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) hv[u] = __ldg(reinterpret_cast<const uint4*>(arow + c0 + 8 * u));
-                tmem_wait_ld();
-                float x[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const uint32_t w = word(hv[j >> 3], (j & 7) >> 1);
-                    x[j] = ((j & 1) ? bf16hi(w) : bf16lo(w)) * __uint_as_float(r[j]);
-                }
-                // butterfly transpose-reduce over the 32 lanes (31 shuffles): lane l ends with column l's sum
-#pragma unroll
-                for (int o = 16; o >= 1; o >>= 1) {
-                    const bool up = (lane & o) != 0;
-#pragma unroll
-                    for (int j = 0; j < o; ++j) {
-                        const float send = up ? x[j] : x[j + o];
-                        const float keep = up ? x[j + o] : x[j];
-                        x[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-                    }
-                }
-                red[lq * K + c0 + lane] = x[0];
-            }
-            __syncthreads();
-            for (int m = tid; m < K; m += NTH)
-                cpart[(((size_t)(i / ANCH - 1) * gridDim.x + vt) * gridDim.y + bh) * K + m] =
-                    red[m] + red[K + m] + red[2 * K + m] + red[3 * K + m];
-            __syncthreads();
-        }
-    }
-    if (dh0) {   // dH_0 = Z e^{pend}
-        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tZ + lane_base + c0, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                dh0[((size_t)bh * K + c0 + j) * V + v0 + vrow] = __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E);
-        }
-    }
-    if (tid == 0) tma_store_wait_all();
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) tmem_dealloc(tm, 512);
-}
-
-// ---------------------------------------------------------------------------------------------------------------
-// k_bwd_reduce: grid (K/RCW, BH), 64 x RCW/16 threads = 64 rows x groups of 16 channels (16-byte vector loads);
-// (RCW = 32 -- 512 smaller CTAs at 1.3B shapes -- measured slower: 287 vs 262 us.)
-constexpr int RCW = 64;
-// Reverse over chunks: dq = E_q (.) sum_j dq_j, dk = E_k (.) sum_j dk_j (fixed j order), and
-// d log alpha_t = carry + sum_{s >= t in chunk} (q dq - k dk)_s, the carry summing every later chunk plus
-// rowsum(S_T (.) dS_T).  The next chunk's inputs are prefetched into registers while this one is scanned.
-template <int K, int NVT, typename TG>
-__global__ void __launch_bounds__(64 * (RCW / 16)) k_bwd_reduce(const __nv_bfloat16* __restrict__ q,
-                                                    const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g,
-                                                    const __nv_bfloat16* __restrict__ dqp,
-                                                    const __nv_bfloat16* __restrict__ dkp,
-                                                    const float* __restrict__ stdot, __nv_bfloat16* __restrict__ dq,
-                                                    __nv_bfloat16* __restrict__ dk, float* __restrict__ dg,
-                                                    const float* __restrict__ cpart, const int* __restrict__ flag,
-                                                    int T, int BH) {
-    if (*flag) return;
-    constexpr int NG = RCW / 16;      // 16-channel groups per row
-    __shared__ float sb[64][RCW + 1]; // g -> b (chunk-local cumsum), then x -> suffix sums
-    __shared__ float carry_s[RCW];
-    const int tid = threadIdx.x, t = tid / NG, cg = tid % NG;
-    const int m0 = blockIdx.x * RCW, bh = blockIdx.y;
-    const int mc = m0 + 16 * cg;      // this thread's 16 channels [mc, mc+16)
-    const int NC = T / CH;
-    const size_t head_row = (size_t)bh * T;
-    const size_t plane = (size_t)BH * T * K;
-    if (tid < RCW) {
-        float c0 = 0.f;
-        if (stdot)
-            for (int j = 0; j < NVT; ++j) c0 += stdot[((size_t)j * BH + bh) * K + m0 + tid];
-        carry_s[tid] = c0;
-    }
-    uint4 pq[NVT][2], pk[NVT][2], qv[2], kv[2];
-    float gv[16];
-    auto load = [&](int i) {
-        const size_t ix = (head_row + (size_t)i * CH + t) * K + mc;
-#pragma unroll
-        for (int j = 0; j < NVT; ++j)
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                pq[j][u] = __ldg(reinterpret_cast<const uint4*>(dqp + j * plane + ix + 8 * u));
-                pk[j][u] = __ldg(reinterpret_cast<const uint4*>(dkp + j * plane + ix + 8 * u));
-            }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            qv[u] = __ldg(reinterpret_cast<const uint4*>(q + ix + 8 * u));
-            kv[u] = __ldg(reinterpret_cast<const uint4*>(k + ix + 8 * u));
-        }
-#pragma unroll
-        for (int u = 0; u < 16; u += 2) {
-            const float2 x = ld_g2<TG>(g + ix + u);
-            gv[u] = x.x;
-            gv[u + 1] = x.y;
-        }
-    };
-    load(NC - 1);
-    for (int i = NC - 1; i >= 0; --i) {
-        if (tid < RCW && i + 1 < NC && (i + 1) % ANCH == 0) {   // exact carry rowsum(H_{i+1} (.) dH_{i+1})
-            float c0 = 0.f;
-            const size_t a = (i + 1) / ANCH - 1;
-            for (int j = 0; j < NVT; ++j) c0 += cpart[((a * NVT + j) * BH + bh) * K + m0 + tid];
-            carry_s[tid] = c0;
-        }
-        // (a1) chunk-local cumsum: stage g, one thread per channel scans the 64 rows
-#pragma unroll
-        for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = gv[u];
-        __syncthreads();
-        if (tid < RCW) {
-            float run = 0.f;
-            for (int r = 0; r < CH; ++r) { run += sb[r][tid]; sb[r][tid] = run; }
-        }
-        __syncthreads();
-        float x[16], dqv[16], dkv[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            const float b = sb[t][16 * cg + u], r = sb[CH / 2 - 1][16 * cg + u];
-            float sq = 0.f, sk = 0.f;
-#pragma unroll
-            for (int j = 0; j < NVT; ++j) {
-                const __nv_bfloat16* a = reinterpret_cast<const __nv_bfloat16*>(&pq[j][u >> 3]);
-                const __nv_bfloat16* c = reinterpret_cast<const __nv_bfloat16*>(&pk[j][u >> 3]);
-                sq += __bfloat162float(a[u & 7]);
-                sk += __bfloat162float(c[u & 7]);
-            }
-            dqv[u] = sq * ex2f((b - r) * L2E);
-            dkv[u] = sk * ex2f((r - b) * L2E);
-            const float qf = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(&qv[u >> 3])[u & 7]);
-            const float kf = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(&kv[u >> 3])[u & 7]);
-            x[u] = qf * dqv[u] - kf * dkv[u];
-        }
-        const size_t ix = (head_row + (size_t)i * CH + t) * K + mc;
-        uint4 oq[2], ok[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            oq[u] = make_uint4(pack_bf16(dqv[8 * u], dqv[8 * u + 1]), pack_bf16(dqv[8 * u + 2], dqv[8 * u + 3]),
-                               pack_bf16(dqv[8 * u + 4], dqv[8 * u + 5]), pack_bf16(dqv[8 * u + 6], dqv[8 * u + 7]));
-            ok[u] = make_uint4(pack_bf16(dkv[8 * u], dkv[8 * u + 1]), pack_bf16(dkv[8 * u + 2], dkv[8 * u + 3]),
-                               pack_bf16(dkv[8 * u + 4], dkv[8 * u + 5]), pack_bf16(dkv[8 * u + 6], dkv[8 * u + 7]));
-            *reinterpret_cast<uint4*>(dq + ix + 8 * u) = oq[u];
-            *reinterpret_cast<uint4*>(dk + ix + 8 * u) = ok[u];
-        }
-        if (i > 0) load(i - 1);
-        __syncthreads();                   // everyone has read b
-#pragma unroll
-        for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = x[u];
-        __syncthreads();
-        if (tid < RCW) {                   // reverse cumsum with the carry of all later chunks
-            float run = carry_s[tid];
-            for (int r = CH - 1; r >= 0; --r) { run += sb[r][tid]; sb[r][tid] = run; }
-            carry_s[tid] = run;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < 16; u += 4)
-            *reinterpret_cast<float4*>(dg + ix + u) =
-                make_float4(sb[t][16 * cg + u], sb[t][16 * cg + u + 1], sb[t][16 * cg + u + 2], sb[t][16 * cg + u + 3]);
-        __syncthreads();
     }
 }
 
@@ -1705,66 +1098,6 @@ size_t bwd_tc_ws(int B, int H, int T, int K, int V, int C) {
     return bytes + simt::bwd_ws(B, H, T, K, V, C);              // exact-path fallback scratch
 }
 
-template <int K, typename TG>
-static cudaError_t launch_bwd(const BwdProblem& p, cudaStream_t st) {
-    using Cfg = BwdCfg<K>;
-    const int BH = p.B * p.H, NVT = p.V / VT;
-    uint8_t* ws = (uint8_t*)p.ws + split_ws(p.B, p.H, p.T, K);   // (the split path uses the front part)
-    int* flag = (int*)ws;
-    __nv_bfloat16* dqp = (__nv_bfloat16*)(ws + 256);
-    __nv_bfloat16* dkp = dqp + (size_t)NVT * BH * p.T * K;
-    float* stdot = (float*)(dkp + (size_t)NVT * BH * p.T * K);
-    size_t used = 256 + 2 * (size_t)NVT * BH * p.T * K * 2 + (size_t)NVT * BH * K * 4;
-    used = (used + 255) & ~size_t(255);
-    const size_t NA = (p.T / CH > 1) ? (size_t)(p.T / CH - 1) / ANCH : 0;
-    __nv_bfloat16* anch = (__nv_bfloat16*)(ws + used);
-    float* cpart = (float*)(ws + used + NA * BH * p.V * K * 2);
-    used += NA * BH * p.V * K * 2 + NA * NVT * BH * K * 4;
-    used = (used + 255) & ~size_t(255);
-    cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), st);
-    if (e != cudaSuccess) return e;
-    CUtensorMap mV, mD, mDV;
-    const uint64_t rows = (uint64_t)BH * p.T;
-    if ((e = make_map_2d(&mV, p.v, rows, p.V, true)) != cudaSuccess) return e;
-    if ((e = make_map_2d(&mD, p.dO, rows, p.V, true)) != cudaSuccess) return e;
-    if ((e = make_map_2d(&mDV, p.dv, rows, p.V, false)) != cudaSuccess) return e;
-    const uint32_t smem = Cfg::SMEM;
-    if ((e = cudaFuncSetAttribute(k_bwd_dq<K, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
-        return e;
-    if ((e = cudaFuncSetAttribute(k_bwd_dkv<K, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
-        return e;
-    dim3 grid(NVT, BH);
-    {
-        GLA_PROF("tc::bwd_dq", st);
-        k_bwd_dq<K, TG><<<grid, NTH, smem, st>>>(mV, mD, (const __nv_bfloat16*)p.k, (const TG*)p.g, p.h0, p.dfinal,
-                                                 dqp, p.dfinal ? stdot : nullptr, anch, flag, p.T, p.V);
-    }
-    {
-        GLA_PROF("tc::bwd_dkv", st);
-        k_bwd_dkv<K, TG><<<grid, NTH, smem, st>>>(mV, mD, mDV, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k,
-                                                  (const TG*)p.g, p.dfinal, dkp, p.dh0, anch, cpart, flag, p.T, p.V);
-    }
-    {
-        GLA_PROF("tc::bwd_reduce", st);
-        const __nv_bfloat16 *q_ = (const __nv_bfloat16*)p.q, *k_ = (const __nv_bfloat16*)p.k;
-        const float* sd = p.dfinal ? stdot : nullptr;
-        __nv_bfloat16 *dq_ = (__nv_bfloat16*)p.dq, *dk_ = (__nv_bfloat16*)p.dk;
-        const dim3 rg(K / RCW, BH);
-        switch (NVT) {
-            case 1: k_bwd_reduce<K, 1, TG><<<rg, 64 * (RCW / 16), 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
-            case 2: k_bwd_reduce<K, 2, TG><<<rg, 64 * (RCW / 16), 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
-            case 4: k_bwd_reduce<K, 4, TG><<<rg, 64 * (RCW / 16), 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
-            case 8: k_bwd_reduce<K, 8, TG><<<rg, 64 * (RCW / 16), 0, st>>>(q_, k_, (const TG*)p.g, dqp, dkp, sd, dq_, dk_, p.dg, cpart, flag, p.T, BH); break;
-            default: return cudaErrorNotSupported;
-        }
-    }
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    // exact path: runs only when the guard flag was raised (kernels return immediately otherwise)
-    BwdProblem sp = p;
-    sp.ws = ws + used;
-    sp.run_if = flag;
-    return simt::bwd(sp, st);
-}
 
 // Split backward: prep + TMA-fed walks + reduce (+ exact CUDA-core fallback behind the guard flag).
 // Per-device side stream (non-blocking, created once) and per-thread fork/join events for running the two
@@ -1947,23 +1280,13 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     return simt::bwd(sp, st);
 }
 
-static bool bwd_fused() {   // GLA_BWD_FUSED=1: the earlier per-V-tile-build backward (A/B measurements)
-    static int v = -1;
-    if (v < 0) {
-        const char* s = getenv("GLA_BWD_FUSED");
-        v = (s && s[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
 
 cudaError_t bwd_tc(const BwdProblem& p, cudaStream_t st) {
     const bool gf = p.gate_dtype == 1;
     switch (p.K) {
         case 128:
-            if (bwd_fused()) return gf ? launch_bwd<128, float>(p, st) : launch_bwd<128, __nv_bfloat16>(p, st);
             return gf ? launch_bwd2<128, float>(p, st) : launch_bwd2<128, __nv_bfloat16>(p, st);
         case 256:
-            if (bwd_fused()) return gf ? launch_bwd<256, float>(p, st) : launch_bwd<256, __nv_bfloat16>(p, st);
             return gf ? launch_bwd2<256, float>(p, st) : launch_bwd2<256, __nv_bfloat16>(p, st);
         default: return cudaErrorNotSupported;
     }

@@ -10,10 +10,11 @@
 //               state passing with the d_k x 128 state tile resident in TMEM and the output
 //               O = Q~ (H e^r) + P V.  All of its inputs arrive by TMA (Q~hi, K~hi, V, P double-buffered), so
 //               no CUDA-core time goes to loading or rebuilding operands per V tile.
-// Compared with the single fused kernel (tc_fwd.cu), the operand construction and P run once per chunk
-// instead of once per V tile (4x at d_v' = 512), at the price of writing / re-reading Q~hi, K~hi and P
-// (2.1 KB per token-head at K = 256).  Exact path for chunks failing the factorisation guard: as tc_fwd.cu
-// (prep computes P in fp32 log space with factors <= 1; the state kernel applies the decay before the update).
+// Compared with one fused kernel per (b,h) x V tile (the first design, in git history), the operand
+// construction and P run once per chunk instead of once per V tile (4x at d_v' = 512), at the price of writing /
+// re-reading Q~hi, K~hi and P (2.1 KB per token-head at K = 256).  Exact path for chunks failing the
+// factorisation guard: prep computes P in fp32 log space with factors <= 1 and Q~ = q e^{b}, K~ = k e^{Gamma-b};
+// the state kernel applies the decay before the update.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cstdio>
