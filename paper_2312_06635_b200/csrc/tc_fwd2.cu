@@ -255,7 +255,9 @@ struct StateCfg {
     static constexpr uint32_t TCOLS = COL_OB + 64 > 256 ? 512 : 256;
     static constexpr int NST = 256, NTHR = NST + 3 * 32 + 128;  // state, 3 MMA issuers, epilogue
     static constexpr int NSB = K / 16;                           // K-steps of the SB Q~^T product
-    static constexpr int NSB_B = (NSB + 4) / 2, NSB_A = NSB - NSB_B;   // O_a also takes the 4 P V^T steps
+    static constexpr int NHALF = K >= 128 ? 2 : 1;               // channel halves of the pipelined state pass
+    static constexpr int CPH = K / NHALF, CPT = CPH / 2;         // channels per half, per state thread and half
+    static constexpr int NSB_A = NHALF == 2 ? NSB / 2 : NSB, NSB_B = NSB - NSB_A;   // O_a: half 0 (+ P V^T)
 };
 
 template <int K>
@@ -278,7 +280,7 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
     float* fy = fsb + K;
     float* pend = fy + K;
-    __shared__ uint64_t bar_q[2], bar_k[2], bar_vp[2], bar_sb, bar_s, bar_oa, bar_ob, bar_ofree, bar_anch;
+    __shared__ uint64_t bar_q[2], bar_k[2], bar_vp[2], bar_sbh[2], bar_sh[2], bar_oa, bar_ob, bar_ofree, bar_anch;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int vt = blockIdx.x, bh = blockIdx.y;
@@ -314,7 +316,7 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     if (tid == 0) {
         mbar_init(&bar_q[0], 1); mbar_init(&bar_q[1], 1); mbar_init(&bar_k[0], 1); mbar_init(&bar_k[1], 1);
         mbar_init(&bar_vp[0], 1); mbar_init(&bar_vp[1], 1);
-        mbar_init(&bar_sb, 1); mbar_init(&bar_s, 1);
+        mbar_init(&bar_sbh[0], 1); mbar_init(&bar_sbh[1], 1); mbar_init(&bar_sh[0], 1); mbar_init(&bar_sh[1], 1);
         mbar_init(&bar_oa, 1); mbar_init(&bar_ob, 1); mbar_init(&bar_ofree, 1); mbar_init(&bar_anch, 1);
         fence_mbar_init();
         prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmP); prefetch_tmap(&tmV); prefetch_tmap(&tmO);
@@ -333,16 +335,19 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 
     if (warp < 8) {
         // ------------------------------------------------------------------ state warps
-        const int half = warp >> 2;
-        const int cbeg = half * (K / 2);
+        // Channel-half pipelining: the pass runs over channel half 0, signals, then half 1.  The state / output
+        // MMAs of half 0 start while half 1 is being converted, and the next chunk's half-0 pass only waits for
+        // the half-0 MMAs.  Warp w owns TMEM lane quadrant w%4 and the (w/4)-th quarter-share of every half.
+        const int sub = warp >> 2;
         for (int m = tid; m < K; m += Cfg::NST) pend[m] = 0.f;
-        for (int c0 = cbeg; c0 < cbeg + K / 2; c0 += 32) {
-            uint32_t r[32];
+        for (int hh = 0; hh < Cfg::NHALF; ++hh)
+            for (int c0 = hh * Cfg::CPH + sub * Cfg::CPT; c0 < hh * Cfg::CPH + (sub + 1) * Cfg::CPT; c0 += 32) {
+                uint32_t r[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-                r[j] = __float_as_uint(h0 ? h0[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
-            tmem_st32(tS + lane_base + c0, r);
-        }
+                for (int j = 0; j < 32; ++j)
+                    r[j] = __float_as_uint(h0 ? h0[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
+                tmem_st32(tS + lane_base + c0, r);
+            }
         tmem_wait_st();
         float st_r = 0.f, st_G = 0.f;
         if (tid < K) {
@@ -366,87 +371,100 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 if (!slow) { fsb[tid] = ex2f((p + r_) * L2E); fy[tid] = fsb[tid]; pend[tid] = G_ - r_; }
                 else { fsb[tid] = ex2f(p * L2E); fy[tid] = ex2f((p + G_) * L2E); pend[tid] = 0.f; }
             }
-            if (i > 0) {                       // Y final for chunk i-1 (the state MMA of chunk i-1 completed)
-                mbar_wait(&bar_s, (i - 1) & 1);
-                tc_fence_after();
-                if (tid == 0) {                // K~ of chunk i+1 into the buffer the state MMA of chunk i-1 read
-                    TR(0, i);
-                    if (i + 1 < NC) load_k(i + 1);
-                }
-            }
             named_bar_sync(1, Cfg::NST);       // fsb / fy visible
-            const uint32_t sba = tSB + lane_base + cbeg / 2;
-#pragma unroll
-            for (int s = 0; s < K / 64; ++s) { // 32-column slices of this thread's K/2 channels
-                const int cb = cbeg + 32 * s;
-                uint32_t pk[16];
-                uint32_t r[32];
-                tmem_ld32(tS + lane_base + cb, r);
-                tmem_wait_ld();
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                    const float4 fs = *reinterpret_cast<const float4*>(fsb + cb + j);
-                    const float4 fyv = *reinterpret_cast<const float4*>(fy + cb + j);
-                    const float2 y0 = make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
-                    const float2 y1 = make_float2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-                    pk[j / 2] = pack2(mul2(y0, make_float2(fs.x, fs.y)));
-                    pk[j / 2 + 1] = pack2(mul2(y1, make_float2(fs.z, fs.w)));
-                    const float2 z0 = mul2(y0, make_float2(fyv.x, fyv.y)), z1 = mul2(y1, make_float2(fyv.z, fyv.w));
-                    r[j] = __float_as_uint(z0.x); r[j + 1] = __float_as_uint(z0.y);
-                    r[j + 2] = __float_as_uint(z1.x); r[j + 3] = __float_as_uint(z1.y);
-                }
-                tmem_st32(tS + lane_base + cb, r);
-                if (s == 0 && i > 0) {         // the O MMAs of chunk i-1 (the readers of SB, V, P) have completed
-                    if (tid == 0) TR(6, i);
-                    mbar_wait(&bar_oa, (i - 1) & 1);
-                    mbar_wait(&bar_ob, (i - 1) & 1);
-                    if (anch && i - 1 > 0 && (i - 1) % ANCH == 0)   // the epilogue has copied SB_{i-1} out
-                        mbar_wait(&bar_anch, ((i - 1) / ANCH - 1) & 1);
+#pragma unroll 1
+            for (int hh = 0; hh < Cfg::NHALF; ++hh) {
+                if (i > 0) {                   // half hh of Y final for chunk i-1
+                    mbar_wait(&bar_sh[hh], (i - 1) & 1);
                     tc_fence_after();
-                    if (tid == 0) {            // V/P of chunk i+1 into the buffers chunk i-1 used
-                        TR(7, i);
-                        if (i + 1 < NC) load_vp(i + 1);
+                    if (tid == 0 && hh == Cfg::NHALF - 1) {   // both state-MMA halves of chunk i-1 done: K~ buffer free
+                        TR(0, i);
+                        if (i + 1 < NC) load_k(i + 1);
                     }
                 }
-                tmem_st16(sba + 16 * s, pk);
+                const int cbeg = hh * Cfg::CPH + sub * Cfg::CPT;
+                const uint32_t sba = tSB + lane_base + cbeg / 2;
+#pragma unroll
+                for (int s = 0; s < Cfg::CPT / 32; ++s) {   // 32-column slices of this thread's channels
+                    const int cb = cbeg + 32 * s;
+                    uint32_t pk[16];
+                    uint32_t r[32];
+                    tmem_ld32(tS + lane_base + cb, r);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const float4 fs = *reinterpret_cast<const float4*>(fsb + cb + j);
+                        const float4 fyv = *reinterpret_cast<const float4*>(fy + cb + j);
+                        const float2 y0 = make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+                        const float2 y1 = make_float2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                        pk[j / 2] = pack2(mul2(y0, make_float2(fs.x, fs.y)));
+                        pk[j / 2 + 1] = pack2(mul2(y1, make_float2(fs.z, fs.w)));
+                        const float2 z0 = mul2(y0, make_float2(fyv.x, fyv.y)), z1 = mul2(y1, make_float2(fyv.z, fyv.w));
+                        r[j] = __float_as_uint(z0.x); r[j + 1] = __float_as_uint(z0.y);
+                        r[j + 2] = __float_as_uint(z1.x); r[j + 3] = __float_as_uint(z1.y);
+                    }
+                    tmem_st32(tS + lane_base + cb, r);
+                    if (s == 0 && i > 0) {     // the output MMAs of chunk i-1 on this half (the readers of SB) done
+                        if (tid == 0 && hh == 0) TR(6, i);
+                        mbar_wait(hh == 0 ? &bar_oa : &bar_ob, (i - 1) & 1);
+                        if (hh == 0 && anch && i - 1 > 0 && (i - 1) % ANCH == 0)   // epilogue copied SB_{i-1} out
+                            mbar_wait(&bar_anch, ((i - 1) / ANCH - 1) & 1);
+                        tc_fence_after();
+                        if (tid == 0 && hh == Cfg::NHALF - 1) {   // V/P of chunk i+1 into the buffers i-1 used
+                            TR(7, i);
+                            // (O_a of chunk i-1, the P V reader, was waited for in half 0 by this thread; waiting
+                            // on it again here could alias its next phase)
+                            if (i + 1 < NC) load_vp(i + 1);
+                        }
+                    }
+                    tmem_st16(sba + 16 * s, pk);
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                named_bar_sync(1, Cfg::NST);   // half hh: SB written, Y decayed
+                if (tid == 0) { if (hh == Cfg::NHALF - 1) TR(1, i); mbar_arrive(&bar_sbh[hh]); }
             }
-            tmem_wait_st();
-            tc_fence_before();
-            named_bar_sync(1, Cfg::NST);       // SB written, Y decayed; fsb may be overwritten
-            if (tid == 0) { TR(1, i); mbar_arrive(&bar_sb); }
         }
-        mbar_wait(&bar_s, (NC - 1) & 1);
+        mbar_wait(&bar_sh[Cfg::NHALF - 1], (NC - 1) & 1);
+        if (Cfg::NHALF > 1) mbar_wait(&bar_sh[0], (NC - 1) & 1);
         tc_fence_after();
         if (final_state) {
-            for (int c0 = cbeg; c0 < cbeg + K / 2; c0 += 32) {
-                uint32_t r[32];
-                tmem_ld32(tS + lane_base + c0, r);
-                tmem_wait_ld();
+            for (int hh = 0; hh < Cfg::NHALF; ++hh)
+                for (int c0 = hh * Cfg::CPH + sub * Cfg::CPT; c0 < hh * Cfg::CPH + (sub + 1) * Cfg::CPT; c0 += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(tS + lane_base + c0, r);
+                    tmem_wait_ld();
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    final_state[((size_t)bh * K + c0 + j) * V + v0 + vrow] =
-                        __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E);
-            }
+                    for (int j = 0; j < 32; ++j)
+                        final_state[((size_t)bh * K + c0 + j) * V + v0 + vrow] =
+                            __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E);
+                }
         }
     } else if (warp == 8) {
-        // ------------------------------------------------------------------ state MMA issuer
-        const uint32_t idS = idesc_bf16(128, K, 1, 1);       // Y[v][ch] += V^T K~hi
+        // ------------------------------------------------------------------ state MMA issuer (per channel half)
+        const uint32_t idS = idesc_bf16(128, Cfg::CPH, 1, 1);   // Y[v][ch] += V^T K~hi over one channel half
         for (int i = 0; i < NC; ++i) {
             const int b = i & 1;
             const uint32_t aV = smem_u32(sV + b * 16384), aK = smem_u32(sK + b * Cfg::OP);
-            mbar_wait(&bar_sb, i & 1);
-            mbar_wait(&bar_k[b], (i >> 1) & 1);
-            mbar_wait(&bar_vp[b], (i >> 1) & 1);
-            tc_fence_after();
-            if (lane == 0) TR(2, i);
+            for (int hh = 0; hh < Cfg::NHALF; ++hh) {
+                mbar_wait(&bar_sbh[hh], i & 1);
+                if (hh == 0) {
+                    mbar_wait(&bar_k[b], (i >> 1) & 1);
+                    mbar_wait(&bar_vp[b], (i >> 1) & 1);
+                }
+                tc_fence_after();
+                if (lane == 0 && hh == 0) TR(2, i);
+                const uint32_t aKh = aK + hh * (Cfg::CPH / 64) * 8192;
 #pragma unroll
-            for (int kk = 0; kk < CH / 16; ++kk)
-                mma_bf16_w(tS, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aK + kk * 2048, 8192, 1024), idS, 1);
-            mma_commit_w(&bar_s);
+                for (int kk = 0; kk < CH / 16; ++kk)
+                    mma_bf16_w(tS + hh * Cfg::CPH, sdesc_sw128(aV + kk * 2048, 8192, 1024),
+                               sdesc_sw128(aKh + kk * 2048, 8192, 1024), idS, 1);
+                mma_commit_w(&bar_sh[hh]);
+            }
             __syncwarp();
         }
     } else if (warp < 11) {
-        // ------------------------------------------------------------------ O MMA issuers (a: + P V^T)
+        // ------------------------------------------------------------------ O MMA issuers (a: half 0 + P V^T)
         const bool is_a = warp == 9;
         const uint32_t idO = idesc_bf16(128, 64, 0, 0);      // O^T[v][t] = SB . Q~hi^T  (SB from TMEM)
         const uint32_t idPV = idesc_bf16(128, 64, 1, 0);     // O^T += V^T P^T
@@ -455,16 +473,16 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         for (int i = 0; i < NC; ++i) {
             const int b = i & 1;
             const uint32_t aQ = smem_u32(sQ + b * Cfg::OP);
-            mbar_wait(&bar_sb, i & 1);
+            mbar_wait(&bar_sbh[is_a || Cfg::NHALF == 1 ? 0 : 1], i & 1);
             if (emit) mbar_wait(&bar_q[b], (i >> 1) & 1);
             if (is_a) mbar_wait(&bar_vp[b], (i >> 1) & 1);
             if (i >= 1) mbar_wait(&bar_ofree, (i - 1) & 1);
             tc_fence_after();
             if (is_a && lane == 0) TR(3, i);
             if (emit)
-            for (int kk = k0; kk < k1; ++kk)
-                mma_bf16_ta_w(tD, tSB + 8 * kk, sdesc_sw128(aQ + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idO,
-                              kk > k0);
+                for (int kk = k0; kk < k1; ++kk)
+                    mma_bf16_ta_w(tD, tSB + 8 * kk, sdesc_sw128(aQ + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idO,
+                                  kk > k0);
             if (is_a && emit) {
                 const uint32_t aV = smem_u32(sV + b * 16384), aP = smem_u32(sP + b * 8192);
 #pragma unroll
@@ -515,7 +533,12 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             for (int h = 0; h < 2; ++h) {
                 uint32_t ra[32], rb[32];
                 tmem_ld32(tOa + 32 * h + lane_base, ra);
-                tmem_ld32(tOb + 32 * h + lane_base, rb);
+                if constexpr (Cfg::NSB_B > 0) {
+                    tmem_ld32(tOb + 32 * h + lane_base, rb);
+                } else {                       // (K = 64: O_b receives no MMAs)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) rb[j] = 0u;
+                }
                 tmem_wait_ld();
                 if (h == 1) {
                     tc_fence_before();
