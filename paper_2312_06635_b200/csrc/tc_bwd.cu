@@ -13,7 +13,7 @@
 // partial (bf16) and the reduce kernel sums the V/128 partials in a fixed order (deterministic).
 //   k_bwd_prep / k_bwd_dp : chunk-parallel operands (Q~hi, K~hi, P, dP, statistics; or only dP when the
 //                           forward's operands are reused, gla_chunk_bwd_saved)
-//   k_bwd_dq2  : forward walk, recomputes H in TMEM          -> dq partials, S_T . dS_T partials, anchors
+//   k_bwd_dq3  : forward walk, recomputes H in TMEM          -> dq partials, S_T . dS_T partials, anchors
 //   k_bwd_dkv2 : reverse walk, dH in TMEM                    -> dv (final), dk partials, anchor carries, dh0
 //   k_bwd_reduce_tma : per (b,h, 64 channels, segment)       -> dq, dk, d log alpha (carry across chunks)
 // If any chunk's half-chunk log decay exceeds the factorisation guard the prep (or the forward) raises a device
@@ -551,68 +551,83 @@ struct BWalkCfg {
     static_assert(SMEM <= 232448, "dynamic shared memory");
 };
 
-// Forward walk over chunks (recomputes H in TMEM): dq partial of this V tile (+ the intra term on V tile 0).
-// Warp roles (480 threads):
-//   warps 0-7   state pass SB = bf16(H_i e^{r}) (smem, MN-major A operand of dq^T), Y <- H_i e^{r} (TMEM);
-//               the exact-state anchors for the d log alpha carry; S_T . dS_T at the end.
-//   warp 8      state MMA Y += V^T K~ (N = K); warps 9, 10: dq^T channel halves = SB^T dO^T (+ K~^T dP^T) into
-//               one of two TMEM buffers (double-buffered so the epilogue is off the serial chain).
-//   warps 11-14 epilogue: dq partial -> global (bf16); the next chunk's input loads.
+// k_bwd_dq3: the dq walk pipelined over 128-channel halves with double-buffered inputs.
+//   warps 0-7   state pass, one channel half at a time (SB half -> smem, Y half decayed), each half signalled;
+//   warp 8      state MMA per half (Y[:, half] += V^T K~[:, half], N = 128), commits bar_sh[half];
+//   warps 9, 10 dq^T of one half each (SB^T[half] dO^T + K~^T[half] dP^T) into a double-buffered TMEM
+//               accumulator, commits bar_dq[buffer][half];
+//   warps 11-14 epilogue: the dq partial; the input loads two chunks ahead (double buffers, bar_free).
+// The next chunk's half-h pass waits only for the half-h MMAs, so half 0's MMAs overlap half 1's pass.
+// Barriers that one role waits on while another may run ahead are per buffer, so no wait can alias a later
+// phase of the same barrier.
 template <int K>
-struct DqCfg {
+struct Dq3Cfg {
+    static constexpr int KB = K / 64, NH = K / 128;
+    static constexpr uint32_t OP = KB * 8192;                  // [KB][64 t][128 B]  K~hi
+    static constexpr uint32_t OFF_K = 0;                       // 2 buffers
+    static constexpr uint32_t OFF_SB = 2 * OP;                 // [KB][128 v][128 B]
+    static constexpr uint32_t OFF_V = OFF_SB + KB * 16384;     // 2 buffers x [2][64 t][128 B]
+    static constexpr uint32_t OFF_D = OFF_V + 2 * 16384;       // 2 buffers x [2][64 t][128 B]
+    static constexpr uint32_t OFF_DP = OFF_D + 2 * 16384;      // 2 buffers x [64 t][128 B]
+    static constexpr uint32_t OFF_F = OFF_DP + 2 * 8192;       // fsb, fy, pend, red[4][K]
+    static constexpr uint32_t SMEM = OFF_F + 4 * 7 * K + 1024;
+    static_assert(SMEM <= 232448, "dynamic shared memory");
     static constexpr int NST = 256, NTHR = NST + 3 * 32 + 128;
-    static constexpr uint32_t DQB = 64 * (K / 128);          // columns of one dq^T buffer (K/128 halves)
-    static constexpr uint32_t COL_DQ = K;
+    static constexpr uint32_t DQB = 64 * NH, COL_DQ = K;
     static constexpr uint32_t TCOLS = K + 2 * DQB > 256 ? 512 : 256;
 };
 
 template <int K>
-__global__ void __launch_bounds__(DqCfg<K>::NTHR, 1)
-k_bwd_dq2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmDP,
+__global__ void __launch_bounds__(Dq3Cfg<K>::NTHR, 1)
+k_bwd_dq3(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmDP,
           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
           const float* __restrict__ stats, const float* __restrict__ h0, const float* __restrict__ dfinal,
           __nv_bfloat16* __restrict__ dqp, float* __restrict__ stdot, __nv_bfloat16* __restrict__ anch,
           const int* __restrict__ flag, int T, int V) {
-    using Cfg = BWalkCfg<K>;
-    using DC = DqCfg<K>;
+    using DC = Dq3Cfg<K>;
     if (*flag) return;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_align1k(smem_raw);
-    uint8_t* sK = sm + Cfg::OFF_K;
-    uint8_t* sSB = sm + Cfg::OFF_SB;
-    uint8_t* sV = sm + Cfg::OFF_V;
-    uint8_t* sD = sm + Cfg::OFF_D;
-    uint8_t* sdP = sm + Cfg::OFF_DP;
-    float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
+    uint8_t* sK = sm + DC::OFF_K;
+    uint8_t* sSB = sm + DC::OFF_SB;
+    uint8_t* sV = sm + DC::OFF_V;
+    uint8_t* sD = sm + DC::OFF_D;
+    uint8_t* sdP = sm + DC::OFF_DP;
+    float* fsb = reinterpret_cast<float*>(sm + DC::OFF_F);
     float* fy = fsb + K;
     float* pend = fy + K;
     float* red = pend + K;
-    __shared__ uint64_t bar_in, bar_sb, bar_m[3], bar_efree[2];
+    __shared__ uint64_t bar_in[2], bar_free[2], bar_sbh[2], bar_sh[2], bar_dq[2][2], bar_efree[2];
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int vt = blockIdx.x, bh = blockIdx.y, v0 = vt * VT, NC = T / CH;
     const int rowb = bh * T;
     const bool intra = vt == 0;
-    const uint32_t in_bytes = Cfg::OP + 32768 + (intra ? 8192 : 0);
+    const uint32_t in_bytes = DC::OP + 32768 + (intra ? 8192 : 0);
     auto load_inputs = [&](int i) {
-        const int row = rowb + i * CH;
-        mbar_expect_tx(&bar_in, in_bytes);
-        for (int c = 0; c < K / 64; ++c) tma_load_2d(sK + c * 8192, &tmK, &bar_in, 64 * c, row);
-        tma_load_2d(sV, &tmV, &bar_in, v0, row);
-        tma_load_2d(sV + 8192, &tmV, &bar_in, v0 + 64, row);
-        tma_load_2d(sD, &tmD, &bar_in, v0, row);
-        tma_load_2d(sD + 8192, &tmD, &bar_in, v0 + 64, row);
-        if (intra) tma_load_2d(sdP, &tmDP, &bar_in, 0, row);
+        const int row = rowb + i * CH, b = i & 1;
+        mbar_expect_tx(&bar_in[b], in_bytes);
+        for (int c = 0; c < K / 64; ++c) tma_load_2d(sK + b * DC::OP + c * 8192, &tmK, &bar_in[b], 64 * c, row);
+        tma_load_2d(sV + b * 16384, &tmV, &bar_in[b], v0, row);
+        tma_load_2d(sV + b * 16384 + 8192, &tmV, &bar_in[b], v0 + 64, row);
+        tma_load_2d(sD + b * 16384, &tmD, &bar_in[b], v0, row);
+        tma_load_2d(sD + b * 16384 + 8192, &tmD, &bar_in[b], v0 + 64, row);
+        if (intra) tma_load_2d(sdP + b * 8192, &tmDP, &bar_in[b], 0, row);
     };
     if (warp == 0) tmem_alloc(&tmem_base, DC::TCOLS);
     if (tid == 0) {
-        mbar_init(&bar_in, 1);
-        mbar_init(&bar_sb, 1);
-        for (int j = 0; j < 3; ++j) mbar_init(&bar_m[j], 1);
-        mbar_init(&bar_efree[0], 1);
-        mbar_init(&bar_efree[1], 1);
+        for (int j = 0; j < 2; ++j) {
+            mbar_init(&bar_in[j], 1);
+            mbar_init(&bar_free[j], 1 + DC::NH);
+            mbar_init(&bar_sbh[j], 1);
+            mbar_init(&bar_sh[j], 1);
+            mbar_init(&bar_dq[j][0], 1);
+            mbar_init(&bar_dq[j][1], 1);
+            mbar_init(&bar_efree[j], 1);
+        }
         fence_mbar_init();
         load_inputs(0);
+        if (NC > 1) load_inputs(1);
     }
     tc_fence_before();
     __syncthreads();
@@ -621,15 +636,13 @@ k_bwd_dq2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUten
     const int lq = warp & 3;
     const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
     const int vrow = 32 * lq + lane;
-    auto wait_mmas = [&](uint32_t ph) {
-        for (int j = 0; j < 3; ++j) mbar_wait(&bar_m[j], ph);
-    };
 
     if (warp < 8) {
         // ------------------------------------------------------------------ state warps
-        const int half = warp >> 2;
+        const int sub = warp >> 2;             // 64-channel share of each 128-channel half
         for (int m = tid; m < K; m += DC::NST) pend[m] = 0.f;
-        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+        for (int c0 = 0; c0 < K; c0 += 32) {
+            if (((c0 >> 6) & 1) != sub) continue;   // channels [128 h + 64 sub, +64)
             uint32_t r[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(h0 ? h0[((size_t)bh * K + c0 + j) * V + v0 + vrow] : 0.f);
@@ -653,23 +666,31 @@ k_bwd_dq2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUten
                 fy[tid] = fsb[tid];
                 pend[tid] = G_ - r_;
             }
-            if (i > 0) {                       // every MMA of chunk i-1 has completed (Y final, SB free)
-                wait_mmas((i - 1) & 1);
-                tc_fence_after();
-            }
-            named_bar_sync(1, DC::NST);
+            named_bar_sync(1, DC::NST);        // fsb / fy visible
             __nv_bfloat16* arow = (anch && i > 0 && i % ANCH == 0)   // (NULL: the forward saved them)
                 ? anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K : nullptr;
-            state_pass2<K>(tS, lane_base, half, vrow, fsb, fy, sSB, arow);
-            fence_async_smem();
-            tc_fence_before();
-            named_bar_sync(1, DC::NST);
-            if (tid == 0) mbar_arrive(&bar_sb);
+#pragma unroll 1
+            for (int hh = 0; hh < DC::NH; ++hh) {
+                if (i > 0) {                   // half hh of chunk i-1: Y final, SB half free
+                    mbar_wait(&bar_sh[hh], (i - 1) & 1);
+                    mbar_wait(&bar_dq[(i - 1) & 1][hh], ((i - 1) >> 1) & 1);
+                    tc_fence_after();
+                }
+                const int c0 = 128 * hh + 64 * sub;
+                state_pass_cols<1>(tS, lane_base, c0, vrow, fsb, fy, sSB, arow);
+                state_pass_cols<1>(tS, lane_base, c0 + 32, vrow, fsb, fy, sSB, arow);
+                tmem_wait_st();
+                fence_async_smem();
+                tc_fence_before();
+                named_bar_sync(1, DC::NST);
+                if (tid == 0) mbar_arrive(&bar_sbh[hh]);
+            }
         }
-        wait_mmas((NC - 1) & 1);
+        for (int hh = 0; hh < DC::NH; ++hh) mbar_wait(&bar_sh[hh], (NC - 1) & 1);
         tc_fence_after();
         if (dfinal) {   // S_T . dS_T partial over this V tile
-            for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+            for (int c0 = 0; c0 < K; c0 += 32) {
+                if (((c0 >> 6) & 1) != sub) continue;
                 uint32_t r[32];
                 tmem_ld32(tS + lane_base + c0, r);
                 tmem_wait_ld();
@@ -685,23 +706,39 @@ k_bwd_dq2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUten
             for (int m = tid; m < K; m += DC::NST)
                 stdot[((size_t)vt * gridDim.y + bh) * K + m] = red[m] + red[K + m] + red[2 * K + m] + red[3 * K + m];
         }
-    } else if (warp < 11) {
-        // ------------------------------------------------------------------ MMA issuers
-        const int role = warp - 8;
-        const uint32_t idDQ = idesc_bf16(128, 64, 1, 0), idS = idesc_bf16(128, K, 1, 1);
-        const uint32_t aK = smem_u32(sK), aSB = smem_u32(sSB), aV = smem_u32(sV), aD = smem_u32(sD), adP = smem_u32(sdP);
+    } else if (warp == 8) {
+        // ------------------------------------------------------------------ state MMA issuer (per half)
+        const uint32_t idS = idesc_bf16(128, 128, 1, 1);
         for (int i = 0; i < NC; ++i) {
             const int b = i & 1;
-            mbar_wait(&bar_sb, i & 1);
-            mbar_wait(&bar_in, i & 1);
-            if (role > 0 && i >= 2) mbar_wait(&bar_efree[b], ((i >> 1) - 1) & 1);
-            tc_fence_after();
-            if (role == 0) {
+            const uint32_t aK = smem_u32(sK + b * DC::OP), aV = smem_u32(sV + b * 16384);
+            for (int hh = 0; hh < DC::NH; ++hh) {
+                mbar_wait(&bar_sbh[hh], i & 1);
+                if (hh == 0) mbar_wait(&bar_in[b], (i >> 1) & 1);
+                tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < CH / 16; ++kk)
-                    mma_bf16_w(tS, sdesc_sw128(aV + kk * 2048, 8192, 1024), sdesc_sw128(aK + kk * 2048, 8192, 1024), idS, 1);
-            } else if (role - 1 < K / 128) {
-                const int hh = role - 1;
+                    mma_bf16_w(tS + 128 * hh, sdesc_sw128(aV + kk * 2048, 8192, 1024),
+                               sdesc_sw128(aK + 2 * hh * 8192 + kk * 2048, 8192, 1024), idS, 1);
+                mma_commit_w(&bar_sh[hh]);
+            }
+            mma_commit_w(&bar_free[b]);
+            __syncwarp();
+        }
+    } else if (warp < 11) {
+        // ------------------------------------------------------------------ dq^T issuers (one per half)
+        const int hh = warp - 9;
+        const uint32_t idDQ = idesc_bf16(128, 64, 1, 0);
+        const uint32_t aSB = smem_u32(sSB);
+        if (hh < DC::NH) {
+            for (int i = 0; i < NC; ++i) {
+                const int b = i & 1;
+                const uint32_t aK = smem_u32(sK + b * DC::OP), aD = smem_u32(sD + b * 16384),
+                               adP = smem_u32(sdP + b * 8192);
+                mbar_wait(&bar_sbh[hh], i & 1);
+                mbar_wait(&bar_in[b], (i >> 1) & 1);
+                if (i >= 2) mbar_wait(&bar_efree[b], ((i >> 1) - 1) & 1);
+                tc_fence_after();
                 const uint32_t td = tdq + DC::DQB * b + 64 * hh;
 #pragma unroll
                 for (int kk = 0; kk < VT / 16; ++kk) {   // dq^T[ch][t] = SB^T dO^T (this V tile)
@@ -714,9 +751,10 @@ k_bwd_dq2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUten
                     for (int kk = 0; kk < CH / 16; ++kk)   // + K~^T dP^T (the full intra term, V tile 0 only)
                         mma_bf16_w(td, sdesc_sw128(aK + 2 * hh * 8192 + kk * 2048, 8192, 1024),
                                    sdesc_sw128(adP + kk * 32, 16, 1024), idDQ, 1);
+                mma_commit_w(&bar_dq[b][hh]);
+                mma_commit_w(&bar_free[b]);
+                __syncwarp();
             }
-            mma_commit_w(&bar_m[role]);
-            __syncwarp();
         }
     } else {
         // ------------------------------------------------------------------ epilogue warps
@@ -724,12 +762,15 @@ k_bwd_dq2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUten
         __nv_bfloat16* out = dqp + (size_t)vt * gridDim.y * T * K;
         for (int i = 0; i < NC; ++i) {
             const int b = i & 1;
-            wait_mmas(i & 1);
+            if (et == 0 && i + 2 < NC) {       // inputs of chunk i+2 into buffer b once chunk i's MMAs are done
+                mbar_wait(&bar_free[b], (i >> 1) & 1);
+                load_inputs(i + 2);
+            }
+            for (int hh = 0; hh < DC::NH; ++hh) mbar_wait(&bar_dq[b][hh], (i >> 1) & 1);
             tc_fence_after();
-            if (et == 0 && i + 1 < NC) load_inputs(i + 1);   // every reader of the input tiles is done
             const size_t row0 = (size_t)rowb + (size_t)i * CH;
 #pragma unroll
-            for (int hh = 0; hh < K / 128; ++hh)
+            for (int hh = 0; hh < DC::NH; ++hh)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     uint32_t r[32];
@@ -1175,7 +1216,7 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     if ((e = make_map_2d(&mDV, p.dv, rows, p.V, false)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_bwd_prep<K, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BPrepCfg<K>::SMEM)))
         return e;
-    if ((e = cudaFuncSetAttribute(k_bwd_dq2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWalkCfg<K>::SMEM)))
+    if ((e = cudaFuncSetAttribute(k_bwd_dq3<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Dq3Cfg<K>::SMEM)))
         return e;
     if ((e = cudaFuncSetAttribute(k_bwd_dkv2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWalkCfg<K>::SMEM)))
         return e;
@@ -1225,7 +1266,7 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     }
     {
         GLA_PROF("tc::bwd_dq", sq);
-        k_bwd_dq2<K><<<grid, DqCfg<K>::NTHR, BWalkCfg<K>::SMEM, sq>>>(mK, mDP, mV, mD, stats, h0w, dfin, dqp,
+        k_bwd_dq3<K><<<grid, Dq3Cfg<K>::NTHR, Dq3Cfg<K>::SMEM, sq>>>(mK, mDP, mV, mD, stats, h0w, dfin, dqp,
                                                                     dfin ? stdot : nullptr,
                                                                     saved_anch ? nullptr : anch, flag, Tv, p.V);
     }
