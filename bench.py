@@ -342,7 +342,7 @@ def main():
 
     def traffic_of(name):
         key = {"tc::fwd_prep": "k_fwd_prep<", "tc::fwd_state": "k_fwd_state<",
-               "tc::bwd_prep": "k_bwd_prep<", "tc::bwd_dq": "k_bwd_dq3<", "tc::bwd_dkv": "k_bwd_dkv2<",
+               "tc::bwd_prep": "k_bwd_prep<", "tc::bwd_dq": "k_bwd_dq3<", "tc::bwd_dkv": "k_bwd_dkv3<",
                "tc::bwd_reduce": "k_bwd_reduce_tma<", "tc::bwd_dp": "k_bwd_dp"}.get(name)
         for n, v in ncu.items():
             if key and key in n.split("::")[-1] and (f"<{K}," in n or f"<{K}>" in n):

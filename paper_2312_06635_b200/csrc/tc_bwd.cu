@@ -14,7 +14,7 @@
 //   k_bwd_prep / k_bwd_dp : chunk-parallel operands (Q~hi, K~hi, P, dP, statistics; or only dP when the
 //                           forward's operands are reused, gla_chunk_bwd_saved)
 //   k_bwd_dq3  : forward walk, recomputes H in TMEM          -> dq partials, S_T . dS_T partials, anchors
-//   k_bwd_dkv2 : reverse walk, dH in TMEM                    -> dv (final), dk partials, anchor carries, dh0
+//   k_bwd_dkv3 : reverse walk, dH in TMEM                    -> dv (final), dk partials, anchor carries, dh0
 //   k_bwd_reduce_tma : per (b,h, 64 channels, segment)       -> dq, dk, d log alpha (carry across chunks)
 // If any chunk's half-chunk log decay exceeds the factorisation guard the prep (or the forward) raises a device
 // flag; the TC kernels that follow then do nothing and a gate kernel tail-launches the exact fp32 CUDA-core
@@ -536,20 +536,6 @@ k_bwd_dp(const __grid_constant__ CUtensorMap tmDP, const __grid_constant__ CUten
     if (warp == 0) tmem_dealloc(tmem_base, 64);
 }
 
-template <int K>
-struct BWalkCfg {
-    static constexpr int KB = K / 64;
-    static constexpr uint32_t OP = KB * 8192;             // [KB][64 t][128 B]
-    static constexpr uint32_t OFF_Q = 0, OFF_K = OP, OFF_SB = 2 * OP;
-    static constexpr uint32_t OFF_V = OFF_SB + KB * 16384;   // [2][64 t][128 B]
-    static constexpr uint32_t OFF_D = OFF_V + 16384;         // [2][64 t][128 B]
-    static constexpr uint32_t OFF_P = OFF_D + 16384;         // [64 t][128 B]
-    static constexpr uint32_t OFF_DP = OFF_P + 8192;         // [64 t][128 B]
-    static constexpr uint32_t OFF_STG = OFF_DP + 8192;       // dv staging [2][64 s][128 B]
-    static constexpr uint32_t OFF_F = OFF_STG + 16384;       // fsb, fy, pend, red[4][K]
-    static constexpr uint32_t SMEM = OFF_F + 4 * 7 * K + 1024;
-    static_assert(SMEM <= 232448, "dynamic shared memory");
-};
 
 // k_bwd_dq3: the dq walk pipelined over 128-channel halves with double-buffered inputs.
 //   warps 0-7   state pass, one channel half at a time (SB half -> smem, Y half decayed), each half signalled;
@@ -791,103 +777,122 @@ k_bwd_dq3(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUten
     if (warp == 0) tmem_dealloc(tmem_base, DC::TCOLS);
 }
 
-// Reverse walk with dH in TMEM: dv (final) and the dk partial of this V tile (+ intra term on V tile 0), dh0.
-// Warp roles (512 threads):
-//   warps 0-7   state pass dSB = bf16(dH_{i+1} e^{Gamma-r}) (smem, MN-major A operand of the dk MMAs),
-//               Z <- the same (TMEM); input loads; d log alpha anchors; dh0.
-//   warps 8-11  MMA issuers, one per independent accumulator stream (one thread issues at most one tcgen05.mma
-//               per ~110 cycles, profiles/r1_microbench.md):
-//                 8: dv^T_a = dSB[:, :K/2] K~[:, :K/2]^T + dO^T P          9: Z += dO^T Q~ ; dv^T_b = rest
-//                10: dk^T (channels 0-127) = dSB^T V^T (+ Q~^T dP)        11: dk^T (channels 128-255)
-//   warps 12-15 epilogue: dv = dv_a + dv_b -> bf16 -> TMA store; dk partial -> global.
+// k_bwd_dkv3: the dkv walk pipelined over 128-channel halves ("sides" A = channels 0-127, B = 128-255).
+//   warps 0-7   state pass per half: dSB half -> smem (MN-major A of dk^T), Z half decayed; anchor carries; dh0.
+//   warp 8  (A) Z half 0 += dO^T Q~[:, A];  dv = dSB[:, A] K~[:, A]^T + dO^T P        (dv double-buffered)
+//   warp 9  (A) dk^T half 0 = dSB^T[A] V^T (+ Q~^T[A] dP on V tile 0)
+//   warp 10 (B) Z half 1 += dO^T Q~[:, B];  dv += dSB[:, B] K~[:, B]^T (after side A's dv, fixed order)
+//   warp 11 (B) dk^T half 1
+//   warps 12-15 epilogue: dk partials and dv (direct global stores), and every TMA input load: the side-A
+//               tiles (K~, Q~ halves, P) of the next chunk as soon as side A's MMAs are done, side B's after side
+//               B, the shared tiles (V, dO, dP; double-buffered) two chunks ahead.
+// The next chunk's half-0 pass needs only side A's MMAs, so side A's MMAs overlap the half-1 pass and side B's
+// MMAs overlap the next half-0 pass.  Barriers that can be waited on while the producer runs ahead are per buffer.
 template <int K>
-struct DkvCfg {
+struct Dkv3Cfg {
+    static constexpr int KB = K / 64, NH = K / 128, CPH = 128;
+    static constexpr uint32_t OP = KB * 8192;                   // Q~hi or K~hi [KB][64 t][128 B]
+    static constexpr uint32_t OFF_SB = 0;                       // [KB][128 v][128 B]
+    static constexpr uint32_t OFF_Q = KB * 16384, OFF_K = OFF_Q + OP;
+    static constexpr uint32_t OFF_V = OFF_K + OP;               // 2 buffers x [2][64 t][128 B]
+    static constexpr uint32_t OFF_D = OFF_V + 2 * 16384;        // 2 buffers
+    static constexpr uint32_t OFF_P = OFF_D + 2 * 16384;        // [64 t][128 B]
+    static constexpr uint32_t OFF_DP = OFF_P + 8192;            // 2 buffers
+    static constexpr uint32_t OFF_F = OFF_DP + 2 * 8192;        // fsb, fy, pend, red[4][K]
+    static constexpr uint32_t SMEM = OFF_F + 4 * 7 * K + 1024;
+    static_assert(SMEM <= 232448, "dynamic shared memory");
     static constexpr int NST = 256, NTHR = 512;
-    static constexpr uint32_t COL_DK = K, COL_DVA = K + 64 * (K / 128), COL_DVB = COL_DVA + 64;
-    static constexpr uint32_t TCOLS = 512;
-    static_assert(COL_DVB + 64 <= TCOLS, "TMEM columns");
+    static constexpr uint32_t COL_DK = K, COL_DV = K + 64 * NH, TCOLS = 512;   // Z | dk^T halves | dv x 2
+    static_assert(COL_DV + 128 <= TCOLS, "TMEM columns");
 };
 
 template <int K>
-__global__ void __launch_bounds__(DkvCfg<K>::NTHR, 1)
-k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+__global__ void __launch_bounds__(Dkv3Cfg<K>::NTHR, 1)
+k_bwd_dkv3(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmDP,
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
-           const __grid_constant__ CUtensorMap tmDV, const float* __restrict__ stats,
-           const float* __restrict__ dfinal, __nv_bfloat16* __restrict__ dkp, float* __restrict__ dh0,
-           const __nv_bfloat16* __restrict__ anch, float* __restrict__ cpart, const int* __restrict__ flag, int T,
-           int V, int emit) {
-    // emit == 0: adjoint-only walk (segment summaries dh_loc): only the Z update runs and only dh0 is written.
-    using Cfg = BWalkCfg<K>;
-    using DC = DkvCfg<K>;
+           const float* __restrict__ stats, const float* __restrict__ dfinal, __nv_bfloat16* __restrict__ dv_out,
+           __nv_bfloat16* __restrict__ dkp, float* __restrict__ dh0, const __nv_bfloat16* __restrict__ anch,
+           float* __restrict__ cpart, const int* __restrict__ flag, int T, int V, int emit) {
+    // emit == 0: adjoint-only walk (segment summaries dh_loc): only the Z updates run and only dh0 is written.
+    using DC = Dkv3Cfg<K>;
+    constexpr int NH = DC::NH;
     if (*flag) return;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_align1k(smem_raw);
-    uint8_t* sQ = sm + Cfg::OFF_Q;
-    uint8_t* sK = sm + Cfg::OFF_K;
-    uint8_t* sSB = sm + Cfg::OFF_SB;
-    uint8_t* sV = sm + Cfg::OFF_V;
-    uint8_t* sD = sm + Cfg::OFF_D;
-    uint8_t* sP = sm + Cfg::OFF_P;
-    uint8_t* sdP = sm + Cfg::OFF_DP;
-    uint8_t* stg = sm + Cfg::OFF_STG;
-    float* fsb = reinterpret_cast<float*>(sm + Cfg::OFF_F);
+    uint8_t* sSB = sm + DC::OFF_SB;
+    uint8_t* sQ = sm + DC::OFF_Q;
+    uint8_t* sK = sm + DC::OFF_K;
+    uint8_t* sV = sm + DC::OFF_V;
+    uint8_t* sD = sm + DC::OFF_D;
+    uint8_t* sP = sm + DC::OFF_P;
+    uint8_t* sdP = sm + DC::OFF_DP;
+    float* fsb = reinterpret_cast<float*>(sm + DC::OFF_F);
     float* fy = fsb + K;
     float* pend = fy + K;
     float* red = pend + K;
-    __shared__ uint64_t bar_in, bar_sb, bar_m[4], bar_efree;
+    __shared__ uint64_t bar_inA, bar_inB, bar_inS[2], bar_sbh[2], bar_mA, bar_mB, bar_dva[2], bar_efdk[2],
+        bar_efdv[2];
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int vt = blockIdx.x, bh = blockIdx.y, v0 = vt * VT, NC = T / CH;
     const int rowb = bh * T;
     const bool intra = vt == 0;
-    const uint32_t in_bytes = 2 * Cfg::OP + 32768 + 8192 + (intra ? 8192 : 0);
-#ifdef GLA_PHASE_TIMING
-    __shared__ long long trc[8][16];
-#define TRB(ev, i) do { const int _j = NC - 1 - (i); if (_j < 16) trc[ev][_j] = clock64(); } while (0)
-#else
-#define TRB(ev, i) do {} while (0)
-#endif
-    auto load_inputs = [&](int i) {
-        const int row = rowb + i * CH;
-        mbar_expect_tx(&bar_in, in_bytes);
-        for (int c = 0; c < K / 64; ++c) {
-            tma_load_2d(sQ + c * 8192, &tmQ, &bar_in, 64 * c, row);
-            tma_load_2d(sK + c * 8192, &tmK, &bar_in, 64 * c, row);
+    // side-A tiles: K~ / Q~ channel blocks [0, 2 per side) (all blocks when NH = 1) and P; side B: blocks 2, 3
+    auto loadA = [&](int i) {
+        const int row = rowb + i * CH, nb = NH == 2 ? 2 : DC::KB;
+        mbar_expect_tx(&bar_inA, 2 * nb * 8192 + 8192);
+        for (int c = 0; c < nb; ++c) {
+            tma_load_2d(sQ + c * 8192, &tmQ, &bar_inA, 64 * c, row);
+            tma_load_2d(sK + c * 8192, &tmK, &bar_inA, 64 * c, row);
         }
-        tma_load_2d(sV, &tmV, &bar_in, v0, row);
-        tma_load_2d(sV + 8192, &tmV, &bar_in, v0 + 64, row);
-        tma_load_2d(sD, &tmD, &bar_in, v0, row);
-        tma_load_2d(sD + 8192, &tmD, &bar_in, v0 + 64, row);
-        tma_load_2d(sP, &tmP, &bar_in, 0, row);
-        if (intra) tma_load_2d(sdP, &tmDP, &bar_in, 0, row);
+        tma_load_2d(sP, &tmP, &bar_inA, 0, row);
+    };
+    auto loadB = [&](int i) {
+        const int row = rowb + i * CH;
+        mbar_expect_tx(&bar_inB, 4 * 8192);
+        for (int c = 2; c < 4; ++c) {
+            tma_load_2d(sQ + c * 8192, &tmQ, &bar_inB, 64 * c, row);
+            tma_load_2d(sK + c * 8192, &tmK, &bar_inB, 64 * c, row);
+        }
+    };
+    auto loadS = [&](int i) {                  // buffer = step parity (step = NC-1-i)
+        const int row = rowb + i * CH, b = (NC - 1 - i) & 1;
+        mbar_expect_tx(&bar_inS[b], 32768 + (intra ? 8192 : 0));
+        tma_load_2d(sV + b * 16384, &tmV, &bar_inS[b], v0, row);
+        tma_load_2d(sV + b * 16384 + 8192, &tmV, &bar_inS[b], v0 + 64, row);
+        tma_load_2d(sD + b * 16384, &tmD, &bar_inS[b], v0, row);
+        tma_load_2d(sD + b * 16384 + 8192, &tmD, &bar_inS[b], v0 + 64, row);
+        if (intra) tma_load_2d(sdP + b * 8192, &tmDP, &bar_inS[b], 0, row);
     };
     if (warp == 0) tmem_alloc(&tmem_base, DC::TCOLS);
     if (tid == 0) {
-        mbar_init(&bar_in, 1);
-        mbar_init(&bar_sb, 1);
-        for (int j = 0; j < 4; ++j) mbar_init(&bar_m[j], 1);
-        mbar_init(&bar_efree, 1);
+        mbar_init(&bar_inA, 1); mbar_init(&bar_inB, 1);
+        mbar_init(&bar_mA, 2); mbar_init(&bar_mB, 2);
+        for (int j = 0; j < 2; ++j) {
+            mbar_init(&bar_inS[j], 1); mbar_init(&bar_sbh[j], 1); mbar_init(&bar_dva[j], 1);
+            mbar_init(&bar_efdk[j], 1); mbar_init(&bar_efdv[j], 1);
+        }
         fence_mbar_init();
-        load_inputs(NC - 1);
+        loadA(NC - 1);
+        if (NH == 2) loadB(NC - 1);
+        loadS(NC - 1);
+        if (NC > 1) loadS(NC - 2);
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tZ = tmem_base, tdk = tmem_base + DC::COL_DK;
-    const uint32_t tdva = tmem_base + DC::COL_DVA, tdvb = tmem_base + DC::COL_DVB;
+    const uint32_t tZ = tmem_base, tdk = tmem_base + DC::COL_DK, tdv = tmem_base + DC::COL_DV;
     const int lq = warp & 3;
     const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
     const int vrow = 32 * lq + lane;
-    auto wait_mmas = [&](uint32_t ph) {
-        for (int j = 0; j < 4; ++j) mbar_wait(&bar_m[j], ph);
-    };
 
     if (warp < 8) {
         // ------------------------------------------------------------------ state warps
-        const int half = warp >> 2;
+        const int sub = warp >> 2;             // 64-channel share of each half
         for (int m = tid; m < K; m += DC::NST) pend[m] = 0.f;
-        for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+        for (int c0 = 0; c0 < K; c0 += 32) {
+            if (((c0 >> 6) & 1) != sub) continue;
             uint32_t r[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j)
@@ -902,6 +907,7 @@ k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         }
         named_bar_sync(1, DC::NST);
         for (int i = NC - 1; i >= 0; --i) {
+            const int j = NC - 1 - i;
             if (tid < K) {   // dSB = bf16(dH_{i+1} e^{Gamma - r}); Z <- same; next pending = r
                 const float r_ = st_r, G_ = st_G;
                 if (i > 0) {
@@ -912,202 +918,186 @@ k_bwd_dkv2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
                 fy[tid] = fsb[tid];
                 pend[tid] = r_;
             }
-            if (i < NC - 1) {                  // every MMA of chunk i+1 has completed
-                const int bd = i + 1;          // exact d log alpha carry at boundary bd over this V tile
-                const bool anc = anch != nullptr && bd % ANCH == 0;
-                const __nv_bfloat16* arow = anch + (((size_t)(bd / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K;
-                uint4 hv[2][4];
-                if (anc)                       // first two anchor slices in flight while the MMAs finish
-#pragma unroll
-                    for (int h2 = 0; h2 < 2; ++h2)
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            hv[h2][u] = __ldg(reinterpret_cast<const uint4*>(arow + half * (K / 2) + 32 * h2 + 8 * u));
-                wait_mmas((NC - 2 - i) & 1);
-                tc_fence_after();
-                if (tid == 0) TRB(0, i);
+            named_bar_sync(1, DC::NST);        // fsb / fy visible
+            const int bd = i + 1;              // exact d log alpha carry at boundary bd over this V tile
+            const bool anc = j > 0 && anch != nullptr && bd % ANCH == 0;
+#pragma unroll 1
+            for (int hh = 0; hh < NH; ++hh) {
+                if (j > 0) {                   // side hh's MMAs of chunk i+1 done: Z half final, dSB half free
+                    mbar_wait(hh == 0 ? &bar_mA : &bar_mB, (j - 1) & 1);
+                    tc_fence_after();
+                }
                 if (anc) {
-#pragma unroll
-                    for (int sl = 0; sl < K / 64; ++sl) {
-                        const int c0 = half * (K / 2) + 32 * sl;
+                    const __nv_bfloat16* arow =
+                        anch + (((size_t)(bd / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K;
+#pragma unroll 1
+                    for (int sl = 0; sl < 2; ++sl) {
+                        const int c0 = 128 * hh + 64 * sub + 32 * sl;
                         uint32_t r[32];
                         tmem_ld32(tZ + lane_base + c0, r);
-                        uint4 hcur[4];
+                        uint4 hv[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) hcur[u] = hv[sl & 1][u];
-                        if (sl + 2 < K / 64)           // slice sl+2 into the freed registers
-#pragma unroll
-                            for (int u = 0; u < 4; ++u)
-                                hv[sl & 1][u] = __ldg(reinterpret_cast<const uint4*>(arow + c0 + 64 + 8 * u));
-                        uint4* hvp = hcur;
+                        for (int u = 0; u < 4; ++u) hv[u] = __ldg(reinterpret_cast<const uint4*>(arow + c0 + 8 * u));
                         tmem_wait_ld();
                         float x[32];
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const uint32_t w = word(hvp[j >> 3], (j & 7) >> 1);
-                            x[j] = ((j & 1) ? bf16hi(w) : bf16lo(w)) * __uint_as_float(r[j]);
+                        for (int jj = 0; jj < 32; ++jj) {
+                            const uint32_t w = word(hv[jj >> 3], (jj & 7) >> 1);
+                            x[jj] = ((jj & 1) ? bf16hi(w) : bf16lo(w)) * __uint_as_float(r[jj]);
                         }
 #pragma unroll
                         for (int o = 16; o >= 1; o >>= 1) {
                             const bool up = (lane & o) != 0;
 #pragma unroll
-                            for (int j = 0; j < o; ++j) {
-                                const float send = up ? x[j] : x[j + o];
-                                const float keep = up ? x[j + o] : x[j];
-                                x[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                            for (int jj = 0; jj < o; ++jj) {
+                                const float send = up ? x[jj] : x[jj + o];
+                                const float keep = up ? x[jj + o] : x[jj];
+                                x[jj] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                             }
                         }
                         red[lq * K + c0 + lane] = x[0];
                     }
-                    named_bar_sync(1, DC::NST);
-                    for (int m = tid; m < K; m += DC::NST)
-                        cpart[(((size_t)(bd / ANCH - 1) * gridDim.x + vt) * gridDim.y + bh) * K + m] =
-                            red[m] + red[K + m] + red[2 * K + m] + red[3 * K + m];
                 }
+                const int c0 = 128 * hh + 64 * sub;
+                state_pass_cols<1>(tZ, lane_base, c0, vrow, fsb, fy, sSB, nullptr);
+                state_pass_cols<1>(tZ, lane_base, c0 + 32, vrow, fsb, fy, sSB, nullptr);
+                tmem_wait_st();
+                fence_async_smem();
+                tc_fence_before();
+                named_bar_sync(1, DC::NST);
+                if (tid == 0) mbar_arrive(&bar_sbh[hh]);
             }
-            named_bar_sync(1, DC::NST);        // fsb / fy visible; red consumed
-            if (tid == 0) TRB(1, i);
-            state_pass2<K>(tZ, lane_base, half, vrow, fsb, fy, sSB);
-            fence_async_smem();
-            tc_fence_before();
-            named_bar_sync(1, DC::NST);
-            if (tid == 0) { TRB(2, i); mbar_arrive(&bar_sb); }
+            if (anc) {                         // red complete (the last half's barrier)
+                for (int m = tid; m < K; m += DC::NST)
+                    cpart[(((size_t)(bd / ANCH - 1) * gridDim.x + vt) * gridDim.y + bh) * K + m] =
+                        red[m] + red[K + m] + red[2 * K + m] + red[3 * K + m];
+                named_bar_sync(1, DC::NST);    // red may be reused
+            }
         }
-        wait_mmas((NC - 1) & 1);
+        mbar_wait(&bar_mA, (NC - 1) & 1);
+        if (NH == 2) mbar_wait(&bar_mB, (NC - 1) & 1);
         tc_fence_after();
         if (dh0) {
-            for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32) {
+            for (int c0 = 0; c0 < K; c0 += 32) {
+                if (((c0 >> 6) & 1) != sub) continue;
                 uint32_t r[32];
                 tmem_ld32(tZ + lane_base + c0, r);
                 tmem_wait_ld();
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    dh0[((size_t)bh * K + c0 + j) * V + v0 + vrow] = __uint_as_float(r[j]) * ex2f(pend[c0 + j] * L2E);
+                for (int jj = 0; jj < 32; ++jj)
+                    dh0[((size_t)bh * K + c0 + jj) * V + v0 + vrow] = __uint_as_float(r[jj]) * ex2f(pend[c0 + jj] * L2E);
             }
         }
     } else if (warp < 12) {
         // ------------------------------------------------------------------ MMA issuers
-        const int role = warp - 8;
-        const uint32_t idZ = idesc_bf16(128, K, 1, 1);      // Z[v][ch] += dO^T Q~
+        const int role = warp - 8;             // 0: Z_A + dv_A, 1: dk_A, 2: Z_B + dv_B, 3: dk_B
+        const int hh = role >> 1;
+        const uint32_t idZ = idesc_bf16(128, NH == 2 ? 128 : K, 1, 1);   // Z[v][ch] += dO^T Q~ (one half)
         const uint32_t idV1 = idesc_bf16(128, 64, 0, 0);    // dv^T = dSB K~^T
         const uint32_t idV2 = idesc_bf16(128, 64, 1, 1);    // dv^T += dO^T P
         const uint32_t idK1 = idesc_bf16(128, 64, 1, 0);    // dk^T = dSB^T V^T
         const uint32_t idK2 = idesc_bf16(128, 64, 1, 1);    // dk^T += Q~^T dP
-        const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aSB = smem_u32(sSB), aV = smem_u32(sV), aD = smem_u32(sD),
-                       aP = smem_u32(sP), adP = smem_u32(sdP);
-        for (int i = NC - 1; i >= 0; --i) {
-            const uint32_t ph = (NC - 1 - i) & 1;
-            mbar_wait(&bar_sb, ph);
-            mbar_wait(&bar_in, ph);
-            if (i < NC - 1) mbar_wait(&bar_efree, (NC - 2 - i) & 1);
-            tc_fence_after();
-            if (lane == 0 && role == 0) TRB(3, i);
-            if (role == 0 && emit) {
-#pragma unroll
-                for (int kk = 0; kk < K / 32; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-                    mma_bf16_w(tdva, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aK + ob, 16, 1024), idV1, kk > 0);
-                }
-#pragma unroll
-                for (int kk = 0; kk < CH / 16; ++kk)
-                    mma_bf16_w(tdva, sdesc_sw128(aD + kk * 2048, 8192, 1024), sdesc_sw128(aP + kk * 2048, 8192, 1024), idV2, 1);
-            } else if (role == 1) {
-#pragma unroll
-                for (int kk = 0; kk < CH / 16; ++kk)
-                    mma_bf16_w(tZ, sdesc_sw128(aD + kk * 2048, 8192, 1024), sdesc_sw128(aQ + kk * 2048, 8192, 1024), idZ, 1);
-                if (emit)
-#pragma unroll
-                for (int kk = K / 32; kk < K / 16; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-                    mma_bf16_w(tdvb, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aK + ob, 16, 1024), idV1, kk > K / 32);
-                }
-            } else if (role - 2 < K / 128 && emit) {
-                const int hh = role - 2;
-#pragma unroll
-                for (int kk = 0; kk < VT / 16; ++kk) {
-                    const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-                    mma_bf16_w(tdk + 64 * hh, sdesc_sw128(aSB + 2 * hh * 16384 + kk * 2048, 16384, 1024),
-                               sdesc_sw128(aV + ob, 16, 1024), idK1, kk > 0);
-                }
-                if (intra)
+        const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aSB = smem_u32(sSB), aP = smem_u32(sP);
+        if (hh < NH) {
+            for (int i = NC - 1; i >= 0; --i) {
+                const int j = NC - 1 - i, bs = j & 1;
+                const uint32_t aV = smem_u32(sV + bs * 16384), aD = smem_u32(sD + bs * 16384),
+                               adP = smem_u32(sdP + bs * 8192);
+                mbar_wait(&bar_sbh[hh], j & 1);
+                mbar_wait(hh == 0 ? &bar_inA : &bar_inB, j & 1);
+                mbar_wait(&bar_inS[bs], (j >> 1) & 1);
+                if ((role & 1) == 0) {         // Z half (+ dv part)
+                    if (hh == 0 && emit && j >= 2) mbar_wait(&bar_efdv[bs], ((j >> 1) - 1) & 1);
+                    tc_fence_after();
 #pragma unroll
                     for (int kk = 0; kk < CH / 16; ++kk)
-                        mma_bf16_w(tdk + 64 * hh, sdesc_sw128(aQ + 2 * hh * 8192 + kk * 2048, 8192, 1024),
-                                   sdesc_sw128(adP + kk * 2048, 8192, 1024), idK2, 1);
+                        mma_bf16_w(tZ + 128 * hh, sdesc_sw128(aD + kk * 2048, 8192, 1024),
+                                   sdesc_sw128(aQ + 2 * hh * 8192 + kk * 2048, 8192, 1024), idZ, 1);
+                    if (emit) {
+                        if (hh == 1) {         // side A's dv MMAs of this buffer first (fixed accumulation order)
+                            mbar_wait(&bar_dva[bs], (j >> 1) & 1);
+                            tc_fence_after();
+                        }
+                        const int k0 = hh * (DC::CPH / 16), k1 = NH == 2 ? k0 + DC::CPH / 16 : K / 16;
+                        for (int kk = k0; kk < k1; ++kk) {
+                            const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+                            mma_bf16_w(tdv + 64 * bs, sdesc_sw128(aSB + o, 16, 1024), sdesc_sw128(aK + ob, 16, 1024),
+                                       idV1, kk > 0);
+                        }
+                        if (hh == 0)
+#pragma unroll
+                            for (int kk = 0; kk < CH / 16; ++kk)
+                                mma_bf16_w(tdv + 64 * bs, sdesc_sw128(aD + kk * 2048, 8192, 1024),
+                                           sdesc_sw128(aP + kk * 2048, 8192, 1024), idV2, 1);
+                    }
+                    if (hh == 0) mma_commit_w(&bar_dva[bs]);
+                } else if (emit) {             // dk^T half
+                    if (j >= 1) mbar_wait(&bar_efdk[hh], (j - 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < VT / 16; ++kk) {
+                        const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+                        mma_bf16_w(tdk + 64 * hh, sdesc_sw128(aSB + 2 * hh * 16384 + kk * 2048, 16384, 1024),
+                                   sdesc_sw128(aV + ob, 16, 1024), idK1, kk > 0);
+                    }
+                    if (intra)
+#pragma unroll
+                        for (int kk = 0; kk < CH / 16; ++kk)
+                            mma_bf16_w(tdk + 64 * hh, sdesc_sw128(aQ + 2 * hh * 8192 + kk * 2048, 8192, 1024),
+                                       sdesc_sw128(adP + kk * 2048, 8192, 1024), idK2, 1);
+                } else {
+                    tc_fence_after();
+                }
+                mma_commit_w(hh == 0 ? &bar_mA : &bar_mB);
+                __syncwarp();
             }
-            mma_commit_w(&bar_m[role]);
-            if (lane == 0 && role == 0) TRB(4, i);
-            __syncwarp();
         }
     } else {
         // ------------------------------------------------------------------ epilogue warps
         const int et = tid - DC::NST - 128;
+        __nv_bfloat16* dko = dkp + (size_t)vt * gridDim.y * T * K;
         for (int i = NC - 1; i >= 0; --i) {
-            const uint32_t ph = (NC - 1 - i) & 1;
-            const int trow = rowb + i * CH;
-            wait_mmas(ph);
-            tc_fence_after();
-            if (et == 0) {
-                TRB(5, i);
-                if (i > 0) load_inputs(i - 1); // every reader of the input tiles (the MMAs of chunk i) is done
-                tma_store_wait_read();         // dv staging of the previous chunk consumed
-            }
-            if (!emit) {                       // adjoint-only walk: no dv / dk to drain
+            const int j = NC - 1 - i, bs = j & 1;
+            const size_t row0 = (size_t)rowb + (size_t)i * CH;
+            for (int hh = 0; hh < NH; ++hh) {
+                mbar_wait(hh == 0 ? &bar_mA : &bar_mB, j & 1);
+                tc_fence_after();
+                if (et == 0 && i > 0) { if (hh == 0) loadA(i - 1); else loadB(i - 1); }
+                if (emit) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t r[32];
+                        tmem_ld32(tdk + 64 * hh + 32 * h + lane_base, r);
+                        tmem_wait_ld();
+                        const int ch = 128 * hh + vrow;
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj)
+                            dko[(row0 + 32 * h + jj) * K + ch] = __float2bfloat16_rn(__uint_as_float(r[jj]));
+                    }
+                }
                 tc_fence_before();
                 named_bar_sync(2, 128);
-                if (et == 0) mbar_arrive(&bar_efree);
-                continue;
+                if (et == 0) mbar_arrive(&bar_efdk[hh]);
             }
-            named_bar_sync(2, 128);
-            uint8_t* dst = stg + (vrow >> 6) * 8192 + (vrow & 63) * 2;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                uint32_t ra[32], rb[32];
-                tmem_ld32(tdva + 32 * h + lane_base, ra);
-                tmem_ld32(tdvb + 32 * h + lane_base, rb);
-                tmem_wait_ld();
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    *reinterpret_cast<__nv_bfloat16*>(dst + (32 * h + j) * 128) =
-                        __float2bfloat16_rn(__uint_as_float(ra[j]) + __uint_as_float(rb[j]));
-            }
-            __nv_bfloat16* out = dkp + (size_t)vt * gridDim.y * T * K;
-#pragma unroll
-            for (int hh = 0; hh < K / 128; ++hh)
+            if (et == 0 && i >= 2) loadS(i - 2);   // both sides done: shared buffer bs free
+            if (emit) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     uint32_t r[32];
-                    tmem_ld32(tdk + 64 * hh + 32 * h + lane_base, r);
+                    tmem_ld32(tdv + 64 * bs + 32 * h + lane_base, r);
                     tmem_wait_ld();
-                    const int ch = 128 * hh + vrow;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        out[((size_t)trow + 32 * h + j) * K + ch] = __float2bfloat16_rn(__uint_as_float(r[j]));
+                    for (int jj = 0; jj < 32; ++jj)
+                        dv_out[(row0 + 32 * h + jj) * V + v0 + vrow] = __float2bfloat16_rn(__uint_as_float(r[jj]));
                 }
-            tc_fence_before();
-            fence_async_smem();
-            named_bar_sync(2, 128);
-            if (et == 0) {
-                TRB(6, i);
-                mbar_arrive(&bar_efree);
-                tma_store_2d(&tmDV, stg, v0, trow);
-                tma_store_2d(&tmDV, stg + 8192, v0 + 64, trow);
-                tma_store_commit();
             }
+            tc_fence_before();
+            named_bar_sync(2, 128);
+            if (et == 0) mbar_arrive(&bar_efdv[bs]);
         }
-        if (et == 0) tma_store_wait_all();
     }
     tc_fence_before();
     __syncthreads();
-#ifdef GLA_PHASE_TIMING
-    if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
-        const long long t0 = trc[2][0];
-        printf("bwd_dkv trace: S0=mmas(i+1) seen S1=pass start S2=pass done M0=issue start M1=issued E0=mmas seen E1=epi done\n");
-        for (int j = 1; j < 16 && j < NC; ++j)
-            printf("  step %2d: S0 %7lld S1 %7lld S2 %7lld M0 %7lld M1 %7lld E0 %7lld E1 %7lld\n", j, trc[0][j] - t0,
-                   trc[1][j] - t0, trc[2][j] - t0, trc[3][j] - t0, trc[4][j] - t0, trc[5][j] - t0, trc[6][j] - t0);
-    }
-#endif
     if (warp == 0) tmem_dealloc(tmem_base, DC::TCOLS);
 }
 
@@ -1206,19 +1196,18 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     if (Smax > 1) used += 2 * (size_t)BH * Smax * K * p.V * 4;
     cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
-    CUtensorMap mQ, mK, mP, mDP, mV, mD, mDV;
+    CUtensorMap mQ, mK, mP, mDP, mV, mD;
     if ((e = make_map_2d(&mQ, Qt, rows, K, true)) != cudaSuccess) return e;
     if ((e = make_map_2d(&mK, Kt, rows, K, true)) != cudaSuccess) return e;
     if ((e = make_map_2d(&mP, Pm, rows, 64, true)) != cudaSuccess) return e;
     if ((e = make_map_2d(&mDP, dPm, rows, 64, true)) != cudaSuccess) return e;
     if ((e = make_map_2d(&mV, p.v, rows, p.V, true)) != cudaSuccess) return e;
     if ((e = make_map_2d(&mD, p.dO, rows, p.V, true)) != cudaSuccess) return e;
-    if ((e = make_map_2d(&mDV, p.dv, rows, p.V, false)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_bwd_prep<K, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BPrepCfg<K>::SMEM)))
         return e;
     if ((e = cudaFuncSetAttribute(k_bwd_dq3<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Dq3Cfg<K>::SMEM)))
         return e;
-    if ((e = cudaFuncSetAttribute(k_bwd_dkv2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWalkCfg<K>::SMEM)))
+    if ((e = cudaFuncSetAttribute(k_bwd_dkv3<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Dkv3Cfg<K>::SMEM)))
         return e;
     if (saved) {
         GLA_PROF("tc::bwd_dp", st);
@@ -1243,8 +1232,9 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         // gives every segment's true d_final_state (the segment-entry states h0v come from the forward)
         {
             GLA_PROF("tc::bwd_dstate_summary", st);
-            k_bwd_dkv2<K><<<grid, DkvCfg<K>::NTHR, BWalkCfg<K>::SMEM, st>>>(
-                mQ, mK, mP, mDP, mV, mD, mDV, stats, nullptr, dkp, dhv, nullptr, cpart, flag, Tv, p.V, 0);
+            k_bwd_dkv3<K><<<grid, Dkv3Cfg<K>::NTHR, Dkv3Cfg<K>::SMEM, st>>>(
+                mQ, mK, mP, mDP, mV, mD, stats, nullptr, (__nv_bfloat16*)p.dv, dkp, dhv, nullptr, cpart, flag, Tv,
+                p.V, 0);
         }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if ((e = seg_chain_bwd(stats, p.dfinal, dhv, dFv, BH, S, NC, K, p.V, st)) != cudaSuccess) return e;
@@ -1272,9 +1262,9 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     }
     {
         GLA_PROF("tc::bwd_dkv", st);
-        k_bwd_dkv2<K><<<grid, DkvCfg<K>::NTHR, BWalkCfg<K>::SMEM, st>>>(mQ, mK, mP, mDP, mV, mD, mDV, stats, dfin,
-                                                                      dkp, dh0w, saved_anch ? saved_anch : anch, cpart,
-                                                                      flag, Tv, p.V, 1);
+        k_bwd_dkv3<K><<<grid, Dkv3Cfg<K>::NTHR, Dkv3Cfg<K>::SMEM, st>>>(
+            mQ, mK, mP, mDP, mV, mD, stats, dfin, (__nv_bfloat16*)p.dv, dkp, dh0w, saved_anch ? saved_anch : anch,
+            cpart, flag, Tv, p.V, 1);
     }
     if (sq != st) {
         if ((e = cudaEventRecord(ev_out, sq)) != cudaSuccess) return e;
