@@ -81,7 +81,7 @@ struct RedCfg {
 };
 
 template <int K, int NVT, typename TG>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(288, 1)
 k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmDQP,
                  const __grid_constant__ CUtensorMap tmDKP, const float* __restrict__ stdot,
@@ -93,7 +93,7 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     uint8_t* sm = smem_align1k(smem_raw);
     __shared__ float sb[64][65];      // g -> b (chunk-local cumsum), then x -> suffix sums
     __shared__ float carry_s[64];
-    __shared__ uint64_t bar[2];
+    __shared__ uint64_t bar[2], empty[2];
     const int tid = threadIdx.x, t = tid >> 2, cg = tid & 3;
     const int m0 = blockIdx.x * 64, bh = blockIdx.y;
     const int mc = m0 + 16 * cg;      // this thread's 16 channels [mc, mc+16)
@@ -123,9 +123,22 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
+        mbar_init(&empty[0], 1);
+        mbar_init(&empty[1], 1);
         fence_mbar_init();
         prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmG); prefetch_tmap(&tmDQP); prefetch_tmap(&tmDKP);
-        for (int s2 = 0; s2 < RC::NS && i_hi - s2 >= i_lo; ++s2) issue(i_hi - s2);
+    }
+    __syncthreads();
+    if (tid >= 256) {                          // producer warp: keeps the ring of stages full (one lane issues)
+        if (tid == 256) {
+            uint32_t n = 0;
+            for (int c = i_hi; c >= i_lo; --c, ++n) {
+                const int slot = c % RC::NS;
+                if (n >= (uint32_t)RC::NS) mbar_wait(&empty[slot], ((n / RC::NS) - 1) & 1);
+                issue(c);
+            }
+        }
+        return;
     }
     if (tid < 64) {   // carry entering the segment from above: the final-state term, or the exact anchor
         float c0 = 0.f;
@@ -138,7 +151,7 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         }
         carry_s[tid] = c0;
     }
-    __syncthreads();
+    named_bar_sync(1, 256);
     uint32_t uses[2] = {0u, 0u};
     // byte offset of 8 consecutive bf16 channels [c, c+8) of row t in a SW128 [64][64] bf16 tile
     auto bf_off = [&](int c) { return (uint32_t)(t * 128 + ((((c >> 3) ^ (t & 7))) << 4)); };
@@ -178,12 +191,12 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 #pragma unroll
             for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = gv[u];
         }
-        __syncthreads();
+        named_bar_sync(1, 256);
         if (tid < 64) {
             float run = 0.f;
             for (int r = 0; r < CH; ++r) { run += sb[r][tid]; sb[r][tid] = run; }
         }
-        __syncthreads();
+        named_bar_sync(1, 256);
         float x[16], dqv[16], dkv[16];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -224,22 +237,22 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             *reinterpret_cast<uint4*>(dq + ix + 8 * u) = oq;
             *reinterpret_cast<uint4*>(dk + ix + 8 * u) = ok;
         }
-        __syncthreads();                   // everyone has read b and the stage buffers
-        if (tid == 0 && i - RC::NS >= i_lo) issue(i - RC::NS);   // refill this stage two chunks ahead
+        named_bar_sync(1, 256);            // everyone has read b and the stage buffers
+        if (tid == 0) mbar_arrive(&empty[sidx]);   // the producer may refill this stage
 #pragma unroll
         for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = x[u];
-        __syncthreads();
+        named_bar_sync(1, 256);
         if (tid < 64) {                    // reverse cumsum with the carry of all later chunks
             float run = carry_s[tid];
             for (int r = CH - 1; r >= 0; --r) { run += sb[r][tid]; sb[r][tid] = run; }
             carry_s[tid] = run;
         }
-        __syncthreads();
+        named_bar_sync(1, 256);
 #pragma unroll
         for (int u = 0; u < 16; u += 4)
             *reinterpret_cast<float4*>(dg + ix + u) =
                 make_float4(sb[t][16 * cg + u], sb[t][16 * cg + u + 1], sb[t][16 * cg + u + 2], sb[t][16 * cg + u + 3]);
-        __syncthreads();
+        named_bar_sync(1, 256);
     }
 }
 
@@ -1289,7 +1302,7 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         if ((e = cudaFuncSetAttribute(k_bwd_reduce_tma<K, N, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                                       (int)RedCfg<N, TG>::SMEM)) != cudaSuccess)                                    \
             return e;                                                                                               \
-        k_bwd_reduce_tma<K, N, TG><<<rg, 256, RedCfg<N, TG>::SMEM, st>>>(mQr, mKr, mGr, mDQP, mDKP, sd, dq_, dk_,   \
+        k_bwd_reduce_tma<K, N, TG><<<rg, 288, RedCfg<N, TG>::SMEM, st>>>(mQr, mKr, mGr, mDQP, mDKP, sd, dq_, dk_,   \
                                                                           p.dg, cpart, flag, Tv, BHv);              \
         break;
         switch (NVT) {
