@@ -264,7 +264,8 @@ template <int K>
 __global__ void __launch_bounds__(StateCfg<K>::NTHR, 1)
 k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmV,
-            const __grid_constant__ CUtensorMap tmO, const float* __restrict__ stats, const int* __restrict__ flags,
+            const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmA,
+            const float* __restrict__ stats, const int* __restrict__ flags,
             const float* __restrict__ h0, float* __restrict__ final_state, __nv_bfloat16* __restrict__ anch, int T,
             int V, int emit) {
     // emit == 0: state-only walk (segment summaries): the output MMAs, epilogue and Q~ loads are skipped and
@@ -507,19 +508,28 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 tma_store_wait_read1();         // staging buffer b (chunk i-2) has been read
             }
             if (anch && i > 0 && i % ANCH == 0) {   // exact state SB_i = bf16(H_i e^{r}) for the backward's anchors
-                __nv_bfloat16* arow = anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0 + vrow) * K;
+                // 64-channel pieces: TMEM -> the (free) staging buffer b in the SW128 layout -> one TMA store each
+                const int arow0 = (int)(((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0);
+                uint8_t* tile = stg + b * 16384;
 #pragma unroll 1
-                for (int c0 = 0; c0 < K / 2; c0 += 32) {   // TMEM column c holds channels 2c, 2c+1
+                for (int pc = 0; pc < K / 64; ++pc) {   // TMEM column c holds channels 2c, 2c+1
                     uint32_t r[32];
-                    tmem_ld32(tSB + lane_base + c0, r);
+                    tmem_ld32(tSB + lane_base + 32 * pc, r);
                     tmem_wait_ld();
 #pragma unroll
                     for (int u = 0; u < 8; ++u)
-                        *reinterpret_cast<uint4*>(arow + 2 * c0 + 8 * u) =
+                        *reinterpret_cast<uint4*>(tile + sw128_off(vrow, 8 * u)) =
                             make_uint4(r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]);
+                    fence_async_smem();
+                    named_bar_sync(2, 128);
+                    if (et == 0) {
+                        tma_store_2d(&tmA, tile, 64 * pc, arow0);
+                        tma_store_commit();
+                        tma_store_wait_read();  // the tile is rewritten by the next piece / the O staging
+                    }
+                    named_bar_sync(2, 128);
                 }
                 tc_fence_before();
-                named_bar_sync(2, 128);
                 if (et == 0) mbar_arrive(&bar_anch);
             }
             if (!emit) {                       // state-only walk: nothing to drain, keep the schedule
@@ -620,13 +630,17 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     const int S = fwd_segments((int)BH, p.V, (int)NC);
     float* h0v = (float*)w; w += S > 1 ? al(BH * S * K * p.V * 4) : 0;   // segment-entry states (saved for bwd)
     float* slv = (float*)w;                                              // segment summaries / final states
-    CUtensorMap mQ, mK, mP, mV, mO;
+    CUtensorMap mQ, mK, mP, mV, mO, mA;
     cudaError_t e;
     if ((e = make_map_2d(&mQ, Qt, rows, K, true)) != cudaSuccess) return e;
     if ((e = make_map_2d(&mK, Kt, rows, K, true)) != cudaSuccess) return e;
     if ((e = make_map_2d(&mP, Pm, rows, 64, true)) != cudaSuccess) return e;
     if ((e = make_map_2d(&mV, p.v, rows, p.V, true)) != cudaSuccess) return e;
     if ((e = make_map_2d(&mO, p.out, rows, p.V, false)) != cudaSuccess) return e;
+    const size_t n_arows = n_anch(p.T) * BH * p.V;   // anchor states [(anchor, b,h, v)][K] bf16
+    if ((e = make_map_2d_ex(&mA, n_arows ? (const void*)anch : (const void*)Qt, 2, n_arows ? n_arows : rows, K, 64, 128,
+                            true)) != cudaSuccess)
+        return e;
     if ((e = cudaFuncSetAttribute(k_fwd_prep<K, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)PrepCfg<K>::SMEM)))
         return e;
@@ -644,7 +658,7 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     if (S == 1) {
         GLA_PROF("tc::fwd_state", st);
         k_fwd_state<K><<<dim3(p.V / VT, (unsigned)BH), StateCfg<K>::NTHR, StateCfg<K>::SMEM, st>>>(
-            mQ, mK, mP, mV, mO, stats, flags, p.h0, p.final_state, an, p.T, p.V, 1);
+            mQ, mK, mP, mV, mO, mA, stats, flags, p.h0, p.final_state, an, p.T, p.V, 1);
         return cudaGetLastError();
     }
     // Long sequences: B*H*S virtual units of T/S tokens (same rows).  (1) state-only walks give each segment's
@@ -654,14 +668,14 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     const dim3 gv(p.V / VT, (unsigned)(BH * S));
     {
         GLA_PROF("tc::fwd_state_summary", st);
-        k_fwd_state<K><<<gv, StateCfg<K>::NTHR, StateCfg<K>::SMEM, st>>>(mQ, mK, mP, mV, mO, stats, flags, nullptr,
+        k_fwd_state<K><<<gv, StateCfg<K>::NTHR, StateCfg<K>::SMEM, st>>>(mQ, mK, mP, mV, mO, mA, stats, flags, nullptr,
                                                                          slv, nullptr, Tv, p.V, 0);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = seg_chain_fwd(stats, p.h0, slv, h0v, (int)BH, S, (int)NC, K, p.V, st)) != cudaSuccess) return e;
     {
         GLA_PROF("tc::fwd_state", st);
-        k_fwd_state<K><<<gv, StateCfg<K>::NTHR, StateCfg<K>::SMEM, st>>>(mQ, mK, mP, mV, mO, stats, flags, h0v,
+        k_fwd_state<K><<<gv, StateCfg<K>::NTHR, StateCfg<K>::SMEM, st>>>(mQ, mK, mP, mV, mO, mA, stats, flags, h0v,
                                                                          p.final_state ? slv : nullptr, an, Tv, p.V, 1);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
