@@ -130,3 +130,35 @@ def test_tc_segmented_long_sequence(B, H, T, K, V):
     for name, x, y in zip(("dq", "dk", "dv", "dlog_alpha", "dh0"), got, ref):
         e = nerr_slices(x.float().cpu().numpy(), y)
         assert e < TOL, (name, e)
+
+
+@pytest.mark.parametrize("B,H,T,K,V,nsamp", [(16, 4, 2048, 256, 512, 2),    # configs[2] (the bench workload)
+                                              (8, 4, 2048, 128, 256, 2),     # configs[1] (340M shapes)
+                                              (2, 4, 16384, 256, 512, 1)])   # configs[3] T=16K (segment split)
+def test_bench_path_full_size_sampled(B, H, T, K, V, nsamp):
+    """Exactly the bench's step at full size: gla_chunk_fwd with its workspace, then gla_chunk_bwd_saved (dP
+    kernel, concurrent dq / dkv walks, segment split where chosen).  Outputs and all gradients on sampled (b,h)
+    slices against the fp64 oracle; a second identical step is bitwise equal (determinism of the concurrent
+    path)."""
+    p = synth.problem(B, H, T, K, V, seed=2)
+    pc = {n: t.cuda() for n, t in p.items()}
+    wf = G.fwd_workspace(pc["q"], pc["v"], pc["g"], 64, 16, "tc")
+
+    def step():
+        o, fs = G.chunk_fwd(pc["q"], pc["k"], pc["v"], pc["g"], 64, 16, None, True, "tc", workspace=wf)
+        g_ = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, path="tc", fwd_workspace=wf)
+        return (o, fs) + tuple(g_[:4])
+    got = step()
+    again = step()
+    torch.cuda.synchronize()
+    for x, y in zip(got, again):
+        assert torch.equal(x, y)
+    rng = np.random.default_rng(3)
+    for _ in range(nsamp):
+        b, h = int(rng.integers(B)), int(rng.integers(H))
+        sl = {n: p[n][b:b + 1, h:h + 1].double().numpy() for n in ("q", "k", "v", "g", "do")}
+        ro, rfs = oracle.fwd(sl["q"], sl["k"], sl["v"], sl["g"])
+        ref = (ro, rfs) + tuple(oracle.bwd(sl["q"], sl["k"], sl["v"], sl["g"], sl["do"])[:4])
+        for name, x, y in zip(("o", "final_state", "dq", "dk", "dv", "dlog_alpha"), got, ref):
+            e = nerr_slices(x[b:b + 1, h:h + 1].float().cpu().numpy(), y)
+            assert e < TOL, (name, e)
