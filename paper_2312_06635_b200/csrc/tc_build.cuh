@@ -181,44 +181,5 @@ __device__ __forceinline__ void state_pass_cols(uint32_t tS, uint32_t lane_base,
     }
 }
 
-// TMEM state pass over this thread's columns: SB <- bf16(Y * fsb), Y <- Y * fy (fsb, fy per channel, smem).
-// Warp w handles TMEM lanes 32 (w%4) + [0,32) (one v per thread) and column half w/4 (K/2 columns).
-template <int K>
-__device__ __forceinline__ void state_pass2(uint32_t tS, uint32_t lane_base, int half, int vrow, const float* fsb,
-                                            const float* fy, uint8_t* sSB, __nv_bfloat16* anch_row = nullptr) {
-    constexpr int NL = 1;   // two loads in flight spill at 255 registers (measured slower)
-    for (int c0 = half * (K / 2); c0 < (half + 1) * (K / 2); c0 += 32 * NL)
-        state_pass_cols<NL>(tS, lane_base, c0, vrow, fsb, fy, sSB, anch_row);
-    tmem_wait_st();
-}
-
-// TMEM state pass over columns [c_begin, c_end) (multiples of 16) of this warp's lane quarter.
-__device__ __forceinline__ void state_pass16(uint32_t tS, uint32_t lane_base, int c_begin, int c_end, int vrow,
-                                             const float* fsb, const float* fy, uint8_t* sSB) {
-    for (int c0 = c_begin; c0 < c_end; c0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(tS + lane_base + c0, r);
-        tmem_wait_ld();
-        uint32_t pk[8];
-#pragma unroll
-        for (int j = 0; j < 16; j += 4) {
-            const float4 fs = *reinterpret_cast<const float4*>(fsb + c0 + j);
-            const float4 fyv = *reinterpret_cast<const float4*>(fy + c0 + j);
-            const float2 y0 = make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
-            const float2 y1 = make_float2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-            pk[j / 2] = pack2(mul2(y0, make_float2(fs.x, fs.y)));
-            pk[j / 2 + 1] = pack2(mul2(y1, make_float2(fs.z, fs.w)));
-            const float2 z0 = mul2(y0, make_float2(fyv.x, fyv.y)), z1 = mul2(y1, make_float2(fyv.z, fyv.w));
-            r[j] = __float_as_uint(z0.x); r[j + 1] = __float_as_uint(z0.y);
-            r[j + 2] = __float_as_uint(z1.x); r[j + 3] = __float_as_uint(z1.y);
-        }
-        tmem_st16(tS + lane_base + c0, r);
-        uint8_t* dst = sSB + (c0 >> 6) * 16384;
-        *reinterpret_cast<uint4*>(dst + sw128_off(vrow, (c0 & 63))) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4*>(dst + sw128_off(vrow, (c0 & 63) + 8)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-    }
-    tmem_wait_st();
-}
-
 }  // namespace tc
 }  // namespace gla
