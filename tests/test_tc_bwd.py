@@ -162,3 +162,27 @@ def test_bench_path_full_size_sampled(B, H, T, K, V, nsamp):
         for name, x, y in zip(("o", "final_state", "dq", "dk", "dv", "dlog_alpha"), got, ref):
             e = nerr_slices(x[b:b + 1, h:h + 1].float().cpu().numpy(), y)
             assert e < TOL, (name, e)
+
+
+@pytest.mark.parametrize("B,H,T,K,V", [(1, 1, 64, 256, 512),      # one chunk: no state passing, no anchors
+                                       (3, 5, 192, 128, 256),     # odd B*H, three chunks
+                                       (1, 2, 640, 256, 1024),    # 8 V tiles (single-stage reduce), 10 chunks
+                                       (1, 1, 1024, 256, 384),    # 3 V tiles: TC forward, CUDA-core backward
+                                       (1, 1, 8192, 128, 256)])   # one head, long: segment split S = 8
+def test_odd_shapes_fwd_and_saved_bwd(B, H, T, K, V):
+    """Rarely exercised shapes through the bench's entry points (forward with workspace + saved backward), with
+    h0 and d_final_state, against the fp64 oracle."""
+    p = problem(B, H, T, K, V, seed=51, h0=True, dfinal=True)
+    pc = cuda(p)
+    wf = G.fwd_workspace(pc["q"], pc["v"], pc["g"], 64, 16, "auto")
+    o, fs = G.chunk_fwd(pc["q"], pc["k"], pc["v"], pc["g"], 64, 16, pc["h0"], True, "auto", workspace=wf)
+    got = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, pc["h0"], pc["dfinal"], True, "auto",
+                      fwd_workspace=wf)
+    torch.cuda.synchronize()
+    ro, rfs = oracle_fwd(p)
+    assert nerr_slices(o.float().cpu().numpy(), ro) < TOL
+    assert nerr_slices(fs.cpu().numpy(), rfs) < TOL
+    ref = oracle_bwd(p)
+    for name, x, y in zip(("dq", "dk", "dv", "dlog_alpha", "dh0"), got, ref):
+        e = nerr_slices(x.float().cpu().numpy(), y)
+        assert e < TOL, (name, e)
