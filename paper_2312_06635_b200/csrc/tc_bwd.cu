@@ -1144,6 +1144,18 @@ size_t bwd_tc_ws(int B, int H, int T, int K, int V, int C) {
 
 
 // Split backward: prep + TMA-fed walks + reduce (+ exact CUDA-core fallback behind the guard flag).
+// dst[bh] = src[bh * S + 0] for [K, V] fp32 states (segment 0's d_initial_state), unless the exact fallback
+// (which writes dst itself) is running.
+__global__ void k_copy_seg0(float* __restrict__ dst, const float* __restrict__ src, int BH, int S, size_t KV,
+                            const int* __restrict__ flag) {
+    if (*flag) return;
+    const size_t n4 = (size_t)BH * KV / 4;
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n4) return;
+    const size_t e = 4 * i, bh = e / KV, off = e % KV;
+    *reinterpret_cast<float4*>(dst + e) = *reinterpret_cast<const float4*>(src + bh * S * KV + off);
+}
+
 // Per-device side stream (non-blocking, created once) and per-thread fork/join events for running the two
 // backward walks concurrently.  Returns nullptr if creation fails (the caller then stays on one stream).
 static cudaStream_t side_stream() {
@@ -1160,7 +1172,7 @@ static cudaStream_t side_stream() {
     return streams[dev];
 }
 static cudaEvent_t fork_event(int which) {
-    thread_local cudaEvent_t evs[64][2] = {};
+    thread_local cudaEvent_t evs[64][3] = {};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
     if (!evs[dev][which] && cudaEventCreateWithFlags(&evs[dev][which], cudaEventDisableTiming) != cudaSuccess)
@@ -1279,8 +1291,18 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
             mQ, mK, mP, mDP, mV, mD, stats, dfin, (__nv_bfloat16*)p.dv, dkp, dh0w, saved_anch ? saved_anch : anch,
             cpart, flag, Tv, p.V, 1);
     }
+    // The exact-fallback gate (one-warp kernel; tail-launches the CUDA-core backward only when a chunk failed
+    // the guard) runs on the dq stream right after the dq walk, overlapping the dkv walk and the reduce; the TC
+    // kernels return at once when the flag is set, so the fallback's writes never race with theirs.
+    BwdProblem sp = p;
+    sp.ws = ws + used;
+    sp.run_if = flag;
+    cudaEvent_t ev_gate = nullptr;
     if (sq != st) {
         if ((e = cudaEventRecord(ev_out, sq)) != cudaSuccess) return e;
+        if ((e = simt::bwd(sp, sq)) != cudaSuccess) return e;
+        if (!(ev_gate = fork_event(2))) return cudaErrorUnknown;
+        if ((e = cudaEventRecord(ev_gate, sq)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(st, ev_out, 0)) != cudaSuccess) return e;
     }
     {
@@ -1312,15 +1334,12 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
 #undef GLA_RED
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (S > 1 && p.dh0) {   // the first segment's d_initial_state of every (b,h)
-        const size_t KV = (size_t)K * p.V;
-        if ((e = cudaMemcpy2DAsync(p.dh0, KV * 4, dhv, S * KV * 4, KV * 4, BH, cudaMemcpyDeviceToDevice, st)) !=
-            cudaSuccess)
-            return e;
+    if (S > 1 && p.dh0) {   // the first segment's d_initial_state of every (b,h) (skipped when the fallback runs)
+        const size_t n4 = (size_t)BH * K * p.V / 4;
+        k_copy_seg0<<<(unsigned)((n4 + 255) / 256), 256, 0, st>>>(p.dh0, dhv, BH, S, (size_t)K * p.V, flag);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    BwdProblem sp = p;
-    sp.ws = ws + used;
-    sp.run_if = flag;
+    if (sq != st) return cudaStreamWaitEvent(st, ev_gate, 0);
     return simt::bwd(sp, st);
 }
 
