@@ -508,14 +508,20 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 tma_store_wait_read1();         // staging buffer b (chunk i-2) has been read
             }
             if (anch && i > 0 && i % ANCH == 0) {   // exact state SB_i = bf16(H_i e^{r}) for the backward's anchors
-                // 64-channel pieces: TMEM -> the (free) staging buffer b in the SW128 layout -> one TMA store each
+                // 64-channel pieces: TMEM -> alternately the two staging buffers (SW128) -> one TMA store each; a
+                // buffer is reused only once its store two pieces earlier has been read, so stores overlap staging
                 const int arow0 = (int)(((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0);
-                uint8_t* tile = stg + b * 16384;
+                if (et == 0) tma_store_wait_read();   // both staging buffers free (incl. chunk i-1's O store)
 #pragma unroll 1
                 for (int pc = 0; pc < K / 64; ++pc) {   // TMEM column c holds channels 2c, 2c+1
+                    uint8_t* tile = stg + (b ^ (pc & 1)) * 16384;
                     uint32_t r[32];
                     tmem_ld32(tSB + lane_base + 32 * pc, r);
                     tmem_wait_ld();
+                    if (pc >= 2) {             // this buffer's previous piece has been read by its store
+                        if (et == 0) tma_store_wait_read1();
+                        named_bar_sync(2, 128);
+                    }
 #pragma unroll
                     for (int u = 0; u < 8; ++u)
                         *reinterpret_cast<uint4*>(tile + sw128_off(vrow, 8 * u)) =
@@ -525,12 +531,15 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     if (et == 0) {
                         tma_store_2d(&tmA, tile, 64 * pc, arow0);
                         tma_store_commit();
-                        tma_store_wait_read();  // the tile is rewritten by the next piece / the O staging
                     }
-                    named_bar_sync(2, 128);
                 }
                 tc_fence_before();
-                if (et == 0) mbar_arrive(&bar_anch);
+                named_bar_sync(2, 128);        // every SB column has been read: the next pass may overwrite SB
+                if (et == 0) {
+                    mbar_arrive(&bar_anch);
+                    tma_store_wait_read();     // staging buffers free again for the O drain below
+                }
+                named_bar_sync(2, 128);
             }
             if (!emit) {                       // state-only walk: nothing to drain, keep the schedule
                 tc_fence_before();
