@@ -469,7 +469,7 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         const bool is_a = warp == 9;
         const uint32_t idO = idesc_bf16(128, 64, 0, 0);      // O^T[v][t] = SB . Q~hi^T  (SB from TMEM)
         const uint32_t idPV = idesc_bf16(128, 64, 1, 0);     // O^T += V^T P^T
-        const uint32_t tD = is_a ? tOa : tOb;
+        const uint32_t tD = tOa;                            // O_b accumulates onto O_a (after it, fixed order)
         const int k0 = is_a ? 0 : Cfg::NSB_A, k1 = is_a ? Cfg::NSB_A : Cfg::NSB;
         for (int i = 0; i < NC; ++i) {
             const int b = i & 1;
@@ -478,12 +478,13 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             if (emit) mbar_wait(&bar_q[b], (i >> 1) & 1);
             if (is_a) mbar_wait(&bar_vp[b], (i >> 1) & 1);
             if (i >= 1) mbar_wait(&bar_ofree, (i - 1) & 1);
+            if (!is_a) mbar_wait(&bar_oa, i & 1);   // O_a of this chunk complete: accumulate after it
             tc_fence_after();
             if (is_a && lane == 0) TR(3, i);
             if (emit)
                 for (int kk = k0; kk < k1; ++kk)
                     mma_bf16_ta_w(tD, tSB + 8 * kk, sdesc_sw128(aQ + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idO,
-                                  kk > k0);
+                                  !is_a || kk > k0);
             if (is_a && emit) {
                 const uint32_t aV = smem_u32(sV + b * 16384), aP = smem_u32(sP + b * 8192);
 #pragma unroll
@@ -550,14 +551,8 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             uint8_t* dst = stg + b * 16384 + (vrow >> 6) * 8192 + (vrow & 63) * 2;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                uint32_t ra[32], rb[32];
-                tmem_ld32(tOa + 32 * h + lane_base, ra);
-                if constexpr (Cfg::NSB_B > 0) {
-                    tmem_ld32(tOb + 32 * h + lane_base, rb);
-                } else {                       // (K = 64: O_b receives no MMAs)
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) rb[j] = 0u;
-                }
+                uint32_t ra[32];
+                tmem_ld32(tOa + 32 * h + lane_base, ra);   // O = O_a (O_b's MMAs accumulated onto it)
                 tmem_wait_ld();
                 if (h == 1) {
                     tc_fence_before();
@@ -567,7 +562,7 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
                     *reinterpret_cast<__nv_bfloat16*>(dst + (32 * h + j) * 128) =
-                        __float2bfloat16_rn(__uint_as_float(ra[j]) + __uint_as_float(rb[j]));
+                        __float2bfloat16_rn(__uint_as_float(ra[j]));
             }
             fence_async_smem();
             named_bar_sync(2, 128);
