@@ -250,9 +250,9 @@ struct StateCfg {
     static constexpr uint32_t OFF_F = OFF_STG + 2 * 16384;      // fsb, fy, pend [K]
     static constexpr uint32_t SMEM = OFF_F + 4 * 3 * K + 1024;
     static_assert(SMEM <= 232448, "dynamic shared memory");
-    // TMEM: Y [K] | SB bf16 pairs [K/2] | O_a [64] | O_b [64]   (O partials 64-column aligned)
-    static constexpr uint32_t COL_SB = K, COL_OA = (K + K / 2 + 63) / 64 * 64, COL_OB = COL_OA + 64;
-    static constexpr uint32_t TCOLS = COL_OB + 64 > 256 ? 512 : 256;
+    // TMEM: Y [K] | SB bf16 pairs [K/2] | O [64] (64-column aligned; both O issuers accumulate into it in turn)
+    static constexpr uint32_t COL_SB = K, COL_OA = (K + K / 2 + 63) / 64 * 64;
+    static constexpr uint32_t TCOLS = COL_OA + 64 > 256 ? 512 : 256;
     static constexpr int NST = 256, NTHR = NST + 3 * 32 + 128;  // state, 3 MMA issuers, epilogue
     static constexpr int NSB = K / 16;                           // K-steps of the SB Q~^T product
     static constexpr int NHALF = K >= 128 ? 2 : 1;               // channel halves of the pipelined state pass
@@ -330,7 +330,7 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     __syncthreads();
     tc_fence_after();
     const uint32_t tS = tmem_base, tSB = tmem_base + Cfg::COL_SB;
-    const uint32_t tOa = tmem_base + Cfg::COL_OA, tOb = tmem_base + Cfg::COL_OB;
+    const uint32_t tOa = tmem_base + Cfg::COL_OA;
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const int vrow = 32 * (warp & 3) + lane;
 
@@ -556,7 +556,7 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 tmem_wait_ld();
                 if (h == 1) {
                     tc_fence_before();
-                    named_bar_sync(2, 128);    // O_a / O_b drained; staging b free
+                    named_bar_sync(2, 128);    // O drained; staging b free
                     if (et == 0) mbar_arrive(&bar_ofree);
                 }
 #pragma unroll
