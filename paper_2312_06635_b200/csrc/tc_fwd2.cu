@@ -232,12 +232,12 @@ k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
 //                             SB = bf16(H_i e^{r}) written to TMEM as the A operand of the O MMAs;
 //                             the next chunks' K~ / V / P loads; at the end final_state.
 //   warp 8      ("mma S"):    the state update Y += V^T K~hi (N = K MMAs), commit bar_s.
-//   warps 9, 10 ("mma O"):    O^T = SB Q~hi^T split by channel range into two TMEM partials O_a, O_b, plus
-//                             V^T P^T (intra-chunk) into O_a; commits bar_oa / bar_ob.
-//   warps 11-14 ("epilogue"): O^T = O_a + O_b (TMEM) -> bf16 staging -> TMA store; the Q~ loads.
+//   warps 9, 10 ("mma O"):    O^T = SB Q~hi^T by channel half into one TMEM accumulator: warp 9 half 0 plus
+//                             V^T P^T (intra-chunk), commit bar_oa; warp 10 half 1 after bar_oa
+//                             (fixed accumulation order), commit bar_ob.
+//   warps 11-14 ("epilogue"): O^T (TMEM) -> bf16 staging -> TMA store; the Q~ loads.
 // Three issuing warps because one thread issues at most one tcgen05.mma per ~110 cycles whatever N is
-// (profiles/r1_microbench.md): the N = 64 output MMAs need several issuers in parallel to approach the
-// tensor pipe's rate.  Serial chain per chunk: state MMA -> state pass -> state MMA; the O MMAs overlap the
+// (profiles/r1_microbench.md): the state and output MMAs are issued from separate warps.  Serial chain per chunk: state MMA -> state pass -> state MMA; the O MMAs overlap the
 // next pass; epilogue, TMA loads and stores overlap everything.  SB never touches shared memory.
 template <int K>
 struct StateCfg {
