@@ -134,7 +134,8 @@ def test_tc_segmented_long_sequence(B, H, T, K, V):
 
 @pytest.mark.parametrize("B,H,T,K,V,nsamp", [(16, 4, 2048, 256, 512, 2),    # configs[2] (the bench workload)
                                               (8, 4, 2048, 128, 256, 2),     # configs[1] (340M shapes)
-                                              (2, 4, 16384, 256, 512, 1)])   # configs[3] T=16K (segment split)
+                                              (2, 4, 16384, 256, 512, 1),    # configs[3] T=16K (segment split)
+                                              (1, 4, 32768, 256, 512, 1)])   # configs[4] T=32K on one GPU (S = 8)
 def test_bench_path_full_size_sampled(B, H, T, K, V, nsamp):
     """Exactly the bench's step at full size: gla_chunk_fwd with its workspace, then gla_chunk_bwd_saved (dP
     kernel, concurrent dq / dkv walks, segment split where chosen).  Outputs and all gradients on sampled (b,h)

@@ -42,7 +42,8 @@ print("|---|---|---|---|---|")
 for name, (B, H, T, K, V) in [("340M (configs[1])", (8, 4, 2048, 128, 256)), ("1.3B (configs[2])", (16, 4, 2048, 256, 512)),
                               ("1.3B T=4K (configs[3])", (8, 4, 4096, 256, 512)),
                               ("1.3B T=8K (configs[3])", (4, 4, 8192, 256, 512)),
-                              ("1.3B T=16K (configs[3])", (2, 4, 16384, 256, 512))]:
+                              ("1.3B T=16K (configs[3])", (2, 4, 16384, 256, 512)),
+                              ("1.3B T=32K, one GPU (configs[4] shapes)", (1, 4, 32768, 256, 512))]:
     p = synth.problem(B, H, T, K, V, seed=1)
     q, k, v, g, do = (p[n].cuda() for n in ("q", "k", "v", "g", "do"))
     wf, wb = G.fwd_workspace(q, v, g), G.bwd_workspace(q, v, g)
