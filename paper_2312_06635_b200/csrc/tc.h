@@ -33,6 +33,12 @@ int fwd_segments(int BH, int V, int NC);
 // Sequential state chains over the segments of every (b,h): forward H_{s+1} = e^{D_s} H_s + S_loc_s
 // (writes H_s for every s; H_0 = h0 or 0), backward dF_{s-1} = e^{D_s} dF_s + dh_loc_s (dF_{S-1} = dfinal or 0).
 // D_s = sum of the chunk totals Gamma over segment s, read from the prep statistics.
+// Segment summaries as one tensor-core contraction per (128 channels, 256 values, segment) (tc_fwd2.cu):
+// adj = false: out = each segment's end state from a zero start (mA = K~hi map, mB = v map);
+// adj = true: out = each segment's d_initial_state with a zero d_final_state (mA = Q~hi map, mB = dO map).
+bool seg_summary_ok(int K, int V);
+cudaError_t seg_summary(const CUtensorMap& mB, const CUtensorMap& mA, const float* stats, const int* flags, float* out,
+                        int K, int V, int Tv, int S, int units, bool adj, cudaStream_t st);
 cudaError_t seg_chain_fwd(const float* stats, const float* h0, const float* S_loc, float* Hv, int BH, int S, int NC,
                           int K, int V, cudaStream_t st);
 cudaError_t seg_chain_bwd(const float* stats, const float* dfinal, const float* dh_loc, float* dFv, int BH, int S,

@@ -1255,7 +1255,10 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     if (S > 1) {
         // adjoint-only walks: every segment's d_initial_state with a zero d_final_state, then the reverse chain
         // gives every segment's true d_final_state (the segment-entry states h0v come from the forward)
-        {
+        if (seg_summary_ok(K, p.V)) {   // one tensor-core contraction per segment (A = Q~hi e^{r + carry}, B = dO)
+            GLA_PROF("tc::bwd_dstate_summary", st);
+            if ((e = seg_summary(mD, mQ, stats, fflags, dhv, K, p.V, Tv, S, BHv, true, st)) != cudaSuccess) return e;
+        } else {
             GLA_PROF("tc::bwd_dstate_summary", st);
             k_bwd_dkv3<K><<<grid, Dkv3Cfg<K>::NTHR, Dkv3Cfg<K>::SMEM, st>>>(
                 mQ, mK, mP, mDP, mV, mD, stats, nullptr, (__nv_bfloat16*)p.dv, dkp, dhv, nullptr, cpart, flag, Tv,

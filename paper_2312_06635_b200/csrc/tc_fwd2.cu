@@ -608,13 +608,19 @@ struct SumCfg {
     static constexpr uint32_t A_BYTES = 2 * 8192, B_BYTES = 4 * 8192, STAGE = A_BYTES + B_BYTES;
     static constexpr uint32_t SMEM = NS * STAGE + 1024;
 };
+// ADJ = 1: the adjoint summary of the backward (a segment's d_initial_state with a zero d_final_state),
+//     dh_loc[k][v] = sum_{t in seg} q_t[k] e^{sum_{u=start}^{t} log alpha_u[k]} dO_t[v],
+// the same contraction with A = Q~hi (.) e^{r + carry} (Q~hi = q e^{b - r}; exact-path chunks q e^{b}) walked from
+// the segment's start, B = dO.
+template <int ADJ>
 __global__ void __launch_bounds__(256, 1)
 k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK,
               const float* __restrict__ stats, const int* __restrict__ flags, float* __restrict__ S_loc, int K, int V,
               int Tv, int S) {
-    // A = K~hi (.) e^{Gamma - r + carry}: the prep kernel's K~hi = k e^{r - b} (exact-path chunks: k e^{Gamma - b})
-    // times a per-channel factor <= 1, so A_t = k_t e^{sum_{u > t} log alpha_u} (suffix to the segment's end);
-    // the carry (sum of Gamma over the later chunks) comes from the per-chunk statistics.
+    // ADJ = 0: A = K~hi (.) e^{Gamma - r + carry}: the prep kernel's K~hi = k e^{r - b} (exact-path chunks:
+    // k e^{Gamma - b}) times a per-channel factor <= 1, so A_t = k_t e^{sum_{u > t} log alpha_u} (suffix to the
+    // segment's end); the carry (sum of Gamma over the later chunks) comes from the per-chunk statistics.
+    // (tmK / tmV name the forward's operands; ADJ = 1 passes Q~hi / dO.)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_align1k(smem_raw);
     constexpr int NS = SumCfg::NS;
@@ -639,7 +645,7 @@ k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ C
     auto load_blk = [&](int j) {                       // K~hi and V of block j -> stage j % NS (one thread)
         uint8_t* sA = sm + (j % NS) * SumCfg::STAGE;
         uint64_t* bar = &bar_v[j % NS];
-        const int r0 = (int)(rowb + (size_t)(nb - 1 - j) * CH);
+        const int r0 = (int)(rowb + (size_t)(ADJ ? j : nb - 1 - j) * CH);
         mbar_expect_tx(bar, SumCfg::STAGE);
         tma_load_2d(sA, &tmK, bar, k0, r0);
         tma_load_2d(sA + 8192, &tmK, bar, k0 + 64, r0);
@@ -652,7 +658,7 @@ k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ C
     float nr = 0.f, nG = 0.f;                          // (r, Gamma, flag) of the next block, loaded one ahead
     int nf = 0;
     auto load_st = [&](int j) {
-        const size_t ci = (size_t)bh * NC + (size_t)seg * nb + (nb - 1 - j);
+        const size_t ci = (size_t)bh * NC + (size_t)seg * nb + (ADJ ? j : nb - 1 - j);
         nr = stats[ci * 2 * K + k0 + tid];
         nG = stats[ci * 2 * K + K + k0 + tid];
         nf = flags[ci];
@@ -669,7 +675,7 @@ k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ C
         }
         if (tid < 128) {
             const float r_ = nr, G_ = nG;
-            fac[tid] = ex2f(((nf ? 0.f : G_ - r_) + carry) * L2E);
+            fac[tid] = ex2f(((nf ? 0.f : (ADJ ? r_ : G_ - r_)) + carry) * L2E);
             carry += G_;
             if (j + 1 < nb) load_st(j + 1);
         }
@@ -723,12 +729,27 @@ k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ C
     if (warp == 0) tmem_dealloc(tD, 256);
 }
 
-static size_t al(size_t x) { return (x + 1023) & ~size_t(1023); }
+bool seg_summary_ok(int K, int V) { return K % 128 == 0 && V % 256 == 0 && !getenv("GLA_SUMMARY_WALK"); }
 
-static bool getenv_flag(const char* name) {
-    const char* e = getenv(name);
-    return e && e[0] == '1';
+cudaError_t seg_summary(const CUtensorMap& mB, const CUtensorMap& mA, const float* stats, const int* flags, float* out,
+                        int K, int V, int Tv, int S, int units, bool adj, cudaStream_t st) {
+    cudaError_t e;
+    const dim3 grid(K / 128, V / 256, (unsigned)units);
+    if (adj) {
+        if ((e = cudaFuncSetAttribute(k_seg_summary<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)SumCfg::SMEM)))
+            return e;
+        k_seg_summary<1><<<grid, 256, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S);
+    } else {
+        if ((e = cudaFuncSetAttribute(k_seg_summary<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)SumCfg::SMEM)))
+            return e;
+        k_seg_summary<0><<<grid, 256, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S);
+    }
+    return cudaGetLastError();
 }
+
+static size_t al(size_t x) { return (x + 1023) & ~size_t(1023); }
 
 static size_t n_anch(int T) { const int NC = T / CH; return NC > 1 ? (size_t)(NC - 1) / ANCH : 0; }
 
@@ -805,14 +826,11 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     // run all segments in parallel from those states (P:516-518's two-stage scan, inside one GPU).
     const int Tv = p.T / S;
     const dim3 gv(p.V / VT, (unsigned)(BH * S));
-    if (K % 128 == 0 && p.V % 256 == 0 && !getenv_flag("GLA_SUMMARY_WALK")) {
+    if (seg_summary_ok(K, p.V)) {
         // chunk-parallel summaries: one tensor-core contraction per (channel tile, value tile, segment)
-        if ((e = cudaFuncSetAttribute(k_seg_summary, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)SumCfg::SMEM)))
-            return e;
         GLA_PROF("tc::fwd_state_summary", st);
-        k_seg_summary<<<dim3(K / 128, p.V / 256, (unsigned)(BH * S)), 256, SumCfg::SMEM, st>>>(
-            mV, mK, stats, flags, slv, K, p.V, Tv, S);
+        if ((e = seg_summary(mV, mK, stats, flags, slv, K, p.V, Tv, S, (int)(BH * S), false, st)) != cudaSuccess)
+            return e;
     } else {
         GLA_PROF("tc::fwd_state_summary", st);
         k_fwd_state<K><<<gv, StateCfg<K>::NTHR, StateCfg<K>::SMEM, st>>>(mQ, mK, mP, mV, mO, mA, stats, flags, nullptr,
