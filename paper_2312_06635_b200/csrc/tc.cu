@@ -24,13 +24,14 @@ int num_sms() {
 }
 
 int fwd_segments(int BH, int V, int NC) {
-    static int off = -1;
-    if (off < 0) {
+    static int force = -1;   // GLA_SEGMENTS=1: never split; GLA_SEGMENTS=N (a power of two): N where valid
+    if (force < 0) {
         const char* e = getenv("GLA_SEGMENTS");
-        off = (e && e[0] == '1') ? 1 : 0;
+        force = e ? atoi(e) : 0;
     }
     int S = 1;
-    if (off) return S;
+    if (force == 1) return S;
+    if (force > 1) return (NC % force == 0 && NC / force >= 8) ? force : 1;
     // The summary walks cost ~0.8 of a full walk, so splitting pays only when the unsplit walk would use at most
     // a quarter of the SMs (measured: S = 2 at 64 CTAs was slower; S = 4 at 32 CTAs 1.5x faster end to end).
     const int nvt = V / 128 > 0 ? V / 128 : 1, ctas = BH * nvt;
