@@ -873,9 +873,14 @@ namespace gla {
 namespace tc {
 namespace {
 constexpr int SEG_CH = 64;
+// Sum of Gamma over segment s for channel k, by the whole warp (its 32 lanes share (bh, k): V/4 is a multiple
+// of 32): lane-strided partial sums, then a butterfly (every lane gets the same, fixed-order result).
 __device__ __forceinline__ float seg_decay(const float* stats, int bh, int s, int NCs, int NC, int K, int k) {
+    const int lane = threadIdx.x & 31;
     float d = 0.f;
-    for (int c = s * NCs; c < (s + 1) * NCs; ++c) d += stats[((size_t)bh * NC + c) * 2 * K + K + k];
+    for (int c = s * NCs + lane; c < (s + 1) * NCs; c += 32) d += stats[((size_t)bh * NC + c) * 2 * K + K + k];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
     return d;
 }
 __global__ void k_seg_chain_fwd(const float* __restrict__ stats, const float* __restrict__ h0,
