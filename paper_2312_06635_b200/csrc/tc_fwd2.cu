@@ -604,7 +604,7 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 // 128 x 256 x 64 MMA into a TMEM accumulator.  Blocks are independent apart from the carried suffix sum, so the
 // build of block j overlaps the MMA of block j-1 (two stages).
 struct SumCfg {
-    static constexpr int NS = 4;   // TMA stages: loads run NS-2 blocks ahead, a stage is refilled 2 blocks after use
+    static constexpr int NS = 4;   // TMA stages (loads run NS-1 blocks ahead of the scaling warps)
     static constexpr uint32_t A_BYTES = 2 * 8192, B_BYTES = 4 * 8192, STAGE = A_BYTES + B_BYTES;
     static constexpr uint32_t SMEM = NS * STAGE + 1024;
 };
@@ -613,7 +613,7 @@ struct SumCfg {
 // the same contraction with A = Q~hi (.) e^{r + carry} (Q~hi = q e^{b - r}; exact-path chunks q e^{b}) walked from
 // the segment's start, B = dO.
 template <int ADJ>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(288, 1)
 k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK,
               const float* __restrict__ stats, const int* __restrict__ flags, float* __restrict__ S_loc, int K, int V,
               int Tv, int S) {
@@ -621,19 +621,21 @@ k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ C
     // k e^{Gamma - b}) times a per-channel factor <= 1, so A_t = k_t e^{sum_{u > t} log alpha_u} (suffix to the
     // segment's end); the carry (sum of Gamma over the later chunks) comes from the per-chunk statistics.
     // (tmK / tmV name the forward's operands; ADJ = 1 passes Q~hi / dO.)
+    // Warps 0-7 scale the A tiles; warp 8 issues the TMA loads and the MMAs (handed over through bar_a), so the
+    // scaling warps never wait for the tensor pipe.
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_align1k(smem_raw);
     constexpr int NS = SumCfg::NS;
-    __shared__ uint64_t bar_v[NS], bar_free[NS];
+    __shared__ uint64_t bar_v[NS], bar_free[NS], bar_a[NS];
     __shared__ uint32_t tmem_base;
-    __shared__ float fac[128];
+    __shared__ float fac[2][128];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int k0 = 128 * blockIdx.x, v0 = 256 * blockIdx.y;
     const size_t unit = blockIdx.z, rowb = unit * (size_t)Tv;
     const int nb = Tv / CH, bh = (int)(unit / S), seg = (int)(unit % S), NC = nb * S;
     if (warp == 0) tmem_alloc(&tmem_base, 256);
     if (tid == 0) {
-        for (int j = 0; j < NS; ++j) { mbar_init(&bar_v[j], 1); mbar_init(&bar_free[j], 1); }
+        for (int j = 0; j < NS; ++j) { mbar_init(&bar_v[j], 1); mbar_init(&bar_free[j], 1); mbar_init(&bar_a[j], 256); }
         fence_mbar_init();
         prefetch_tmap(&tmV); prefetch_tmap(&tmK);
     }
@@ -641,74 +643,82 @@ k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ C
     __syncthreads();
     tc_fence_after();
     const uint32_t tD = tmem_base;
-    const uint32_t idS = idesc_bf16(128, 256, 1, 1);   // D[k][v] += A^T[k][t] B[t][v], both MN-major
-    auto load_blk = [&](int j) {                       // K~hi and V of block j -> stage j % NS (one thread)
-        uint8_t* sA = sm + (j % NS) * SumCfg::STAGE;
-        uint64_t* bar = &bar_v[j % NS];
-        const int r0 = (int)(rowb + (size_t)(ADJ ? j : nb - 1 - j) * CH);
-        mbar_expect_tx(bar, SumCfg::STAGE);
-        tma_load_2d(sA, &tmK, bar, k0, r0);
-        tma_load_2d(sA + 8192, &tmK, bar, k0 + 64, r0);
+    if (warp == 8) {
+        // ------------------------------------------------------------ producer + MMA issuer (one lane)
+        if (lane == 0) {
+            const uint32_t idS = idesc_bf16(128, 256, 1, 1);   // D[k][v] += A^T[k][t] B[t][v], both MN-major
+            auto load_blk = [&](int j) {                       // K~hi and V of block j -> stage j % NS
+                uint8_t* sA = sm + (j % NS) * SumCfg::STAGE;
+                uint64_t* bar = &bar_v[j % NS];
+                const int r0 = (int)(rowb + (size_t)(ADJ ? j : nb - 1 - j) * CH);
+                mbar_expect_tx(bar, SumCfg::STAGE);
+                tma_load_2d(sA, &tmK, bar, k0, r0);
+                tma_load_2d(sA + 8192, &tmK, bar, k0 + 64, r0);
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) tma_load_2d(sA + SumCfg::A_BYTES + q4 * 8192, &tmV, bar, v0 + 64 * q4, r0);
-    };
-    if (tid == 0)
-        for (int j = 0; j < NS - 2 && j < nb; ++j) load_blk(j);
-    float carry = 0.f;                                 // channel tid (< 128): sum of Gamma over the later chunks
-    float nr = 0.f, nG = 0.f;                          // (r, Gamma, flag) of the next block, loaded one ahead
-    int nf = 0;
-    auto load_st = [&](int j) {
-        const size_t ci = (size_t)bh * NC + (size_t)seg * nb + (ADJ ? j : nb - 1 - j);
-        nr = stats[ci * 2 * K + k0 + tid];
-        nG = stats[ci * 2 * K + K + k0 + tid];
-        nf = flags[ci];
-    };
-    if (tid < 128) load_st(0);
-    for (int j = 0; j < nb; ++j) {
-        const int bs = j % NS;
-        uint8_t* sA = sm + bs * SumCfg::STAGE;
-        uint8_t* sB = sA + SumCfg::A_BYTES;
-        if (tid == 0 && j + NS - 2 < nb) {   // block j+NS-2 into the stage block j-2 used (its MMAs are long done:
-            // waiting on block j-1's would stall the whole CTA behind the tensor pipe every block)
-            if (j >= 2) mbar_wait(&bar_free[(j - 2) % NS], ((j - 2) / NS) & 1);
-            load_blk(j + NS - 2);
+                for (int q4 = 0; q4 < 4; ++q4)
+                    tma_load_2d(sA + SumCfg::A_BYTES + q4 * 8192, &tmV, bar, v0 + 64 * q4, r0);
+            };
+            for (int j = 0; j < NS - 1 && j < nb; ++j) load_blk(j);
+            for (int j = 0; j < nb; ++j) {
+                const int bs = j % NS;
+                mbar_wait(&bar_a[bs], (j / NS) & 1);   // A of block j scaled
+                tc_fence_after();
+                const uint32_t aA = smem_u32(sm + bs * SumCfg::STAGE), aB = aA + SumCfg::A_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < CH / 16; ++kk)
+                    mma_bf16(tD, sdesc_sw128(aA + kk * 2048, 8192, 1024), sdesc_sw128(aB + kk * 2048, 8192, 1024),
+                             idS, (j | kk) > 0);
+                mma_commit(&bar_free[bs]);
+                if (j + NS - 1 < nb) {                 // block j+NS-1 into the stage block j-1 used
+                    if (j >= 1) mbar_wait(&bar_free[(j - 1) % NS], ((j - 1) / NS) & 1);
+                    load_blk(j + NS - 1);
+                }
+            }
         }
-        if (tid < 128) {
-            const float r_ = nr, G_ = nG;
-            fac[tid] = ex2f(((nf ? 0.f : (ADJ ? r_ : G_ - r_)) + carry) * L2E);
-            carry += G_;
-            if (j + 1 < nb) load_st(j + 1);
-        }
-        __syncthreads();
-        mbar_wait(&bar_v[bs], (j / NS) & 1);
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------------ scaling warps 0-7
+        float carry = 0.f;                             // channel tid (< 128): sum of Gamma over the passed chunks
+        float nr = 0.f, nG = 0.f;                      // (r, Gamma, flag) of the next block, loaded one ahead
+        int nf = 0;
+        auto load_st = [&](int j) {
+            const size_t ci = (size_t)bh * NC + (size_t)seg * nb + (ADJ ? j : nb - 1 - j);
+            nr = stats[ci * 2 * K + k0 + tid];
+            nG = stats[ci * 2 * K + K + k0 + tid];
+            nf = flags[ci];
+        };
+        if (tid < 128) load_st(0);
+        for (int j = 0; j < nb; ++j) {
+            const int bs = j % NS;
+            uint8_t* sA = sm + bs * SumCfg::STAGE;
+            float* fj = fac[j & 1];
+            if (tid < 128) {
+                const float r_ = nr, G_ = nG;
+                fj[tid] = ex2f(((nf ? 0.f : (ADJ ? r_ : G_ - r_)) + carry) * L2E);
+                carry += G_;
+                if (j + 1 < nb) load_st(j + 1);
+            }
+            named_bar_sync(1, 256);                    // fac[j & 1] written (its readers of block j-2 are done)
+            mbar_wait(&bar_v[bs], (j / NS) & 1);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {                  // 1024 16-byte chunks of the two SW128 blocks
-            const int id = tid + 256 * e, blk = id >> 9, row = (id >> 3) & 63, pos = id & 7;
-            const int cb = 64 * blk + 8 * (pos ^ (row & 7));
-            uint4* pch = reinterpret_cast<uint4*>(sA + blk * 8192 + row * 128 + pos * 16);
-            uint4 w = *pch;
-            uint32_t* u = reinterpret_cast<uint32_t*>(&w);
+            for (int e = 0; e < 4; ++e) {              // 1024 16-byte chunks of the two SW128 blocks
+                const int id = tid + 256 * e, blk = id >> 9, row = (id >> 3) & 63, pos = id & 7;
+                const int cb = 64 * blk + 8 * (pos ^ (row & 7));
+                uint4* pch = reinterpret_cast<uint4*>(sA + blk * 8192 + row * 128 + pos * 16);
+                uint4 w = *pch;
+                uint32_t* u = reinterpret_cast<uint32_t*>(&w);
 #pragma unroll
-            for (int m = 0; m < 4; ++m)
-                u[m] = pack_bf16(bf16lo(u[m]) * fac[cb + 2 * m], bf16hi(u[m]) * fac[cb + 2 * m + 1]);
-            *pch = w;
-        }
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();                               // A scaled; fac free
-        if (tid == 0) {
-            tc_fence_after();
-            const uint32_t aA = smem_u32(sA), aB = smem_u32(sB);
-#pragma unroll
-            for (int kk = 0; kk < CH / 16; ++kk)
-                mma_bf16(tD, sdesc_sw128(aA + kk * 2048, 8192, 1024), sdesc_sw128(aB + kk * 2048, 8192, 1024), idS,
-                         (j | kk) > 0);
-            mma_commit(&bar_free[bs]);
+                for (int m = 0; m < 4; ++m)
+                    u[m] = pack_bf16(bf16lo(u[m]) * fj[cb + 2 * m], bf16hi(u[m]) * fj[cb + 2 * m + 1]);
+                *pch = w;
+            }
+            fence_async_smem();
+            mbar_arrive(&bar_a[bs]);
         }
     }
     mbar_wait(&bar_free[(nb - 1) % NS], ((nb - 1) / NS) & 1);
     tc_fence_after();
-    {   // epilogue: warp w reads lanes 32 (w % 4) + [0, 32) (channels), columns 128 (w / 4) + [0, 128) (values)
+    if (warp < 8) {   // epilogue: warp w reads lanes 32 (w % 4) + [0, 32) (channels), columns 128 (w / 4) + [0, 128)
         const int kr = 32 * (warp & 3) + lane, cb = 128 * (warp >> 2);
         float* out = S_loc + (unit * K + k0 + kr) * (size_t)V + v0 + cb;
         const uint32_t lb = (uint32_t)(32 * (warp & 3)) << 16;
@@ -739,12 +749,12 @@ cudaError_t seg_summary(const CUtensorMap& mB, const CUtensorMap& mA, const floa
         if ((e = cudaFuncSetAttribute(k_seg_summary<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)SumCfg::SMEM)))
             return e;
-        k_seg_summary<1><<<grid, 256, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S);
+        k_seg_summary<1><<<grid, 288, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S);
     } else {
         if ((e = cudaFuncSetAttribute(k_seg_summary<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)SumCfg::SMEM)))
             return e;
-        k_seg_summary<0><<<grid, 256, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S);
+        k_seg_summary<0><<<grid, 288, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S);
     }
     return cudaGetLastError();
 }
