@@ -593,16 +593,15 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 }
 
 // ---------------------------------------------------------------------------------------------------------------
-// ---------------------------------------------------------------------------------------------------------------
 // k_seg_summary: the end state of one segment from a zero start, as ONE contraction over the segment's tokens
 // instead of a serial walk (segment split):
 //     S_loc[k][v] = sum_{t in seg} k_t[k] e^{sum_{u=t+1}^{end} log alpha_u[k]} v_t[v]
 // (the recurrence S_t = diag(alpha_t) S_{t-1} + k_t^T v_t of P:188-189 unrolled over the segment; every decay
 // factor is <= 1, so no normaliser and no exact path are needed).  One CTA per (128 channels, 256 values, unit):
-// it walks the segment's 64-token blocks from the end, builds A = bf16(k (.) e^{suffix sum}) in shared memory
-// (SIMT: the suffix sum is carried across blocks per channel), TMA-loads the V block, and issues the
-// 128 x 256 x 64 MMA into a TMEM accumulator.  Blocks are independent apart from the carried suffix sum, so the
-// build of block j overlaps the MMA of block j-1 (two stages).
+// it walks the segment's 64-token blocks, scales the TMA-loaded K~hi tile in shared memory by a per-channel factor
+// from the chunk statistics (see the kernel), and issues the 128 x 256 x 64 MMA of the block into a TMEM
+// accumulator.  Blocks are independent apart from the carried per-channel sum of Gamma, so the scaling of block j
+// overlaps the MMAs of earlier blocks and the loads of later ones.
 struct SumCfg {
     static constexpr int NS = 4;   // TMA stages (loads run NS-1 blocks ahead of the scaling warps)
     static constexpr uint32_t A_BYTES = 2 * 8192, B_BYTES = 4 * 8192, STAGE = A_BYTES + B_BYTES;
