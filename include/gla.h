@@ -7,7 +7,12 @@
  *   S_t = diag(exp(log_alpha_t)) S_{t-1} + k_t^T v_t,  o_t = q_t S_t        (beta == 1 per P:321)
  * The library computes this operator with the chunk-wise two-level algorithm: chunk size C
  * (`chunk`), sub-chunk size c (`subchunk`).  The result is the recurrence's (the method is exact);
- * `chunk`/`subchunk` only change the rounding.
+ * `chunk`/`subchunk` change only the rounding and the speed.  On the SIMT path both are honoured as given.
+ * On the tensor-core path C = 64 and `subchunk` must divide 64 but is otherwise ignored: the TC kernels form
+ * the whole 64 x 64 intra-chunk score block with one per-chunk normaliser under a range guard (R8/R9)
+ * instead of per-sub-chunk normalisers.  A chunk that fails the guard (some channel's half-chunk log decay
+ * exceeds 60) runs an exact fp32 log-space path in the forward, and sends the WHOLE backward call to the
+ * fp32 CUDA-core kernels (correct, but several times slower: the "guard cliff").
  *
  * Conventions shared by every entry point
  *   - Layout: row-major, [B, H, T, K] for q/k/log_alpha/dq/dk/d_log_alpha, [B, H, T, V] for v/out/d_out/dv,
@@ -17,8 +22,11 @@
  *     memory); `workspace` is caller-allocated scratch of at least the size the matching *_workspace_size
  *     function returns.  Inputs are never written.  Outputs are fully overwritten.
  *   - `stream` is a cudaStream_t (passed as void* so this header needs no CUDA include); every call is
- *     asynchronous on that stream.  Calls are thread-safe (no global mutable state besides a one-time
- *     per-device attribute cache).
+ *     asynchronous on that stream.  Calls are thread-safe.  Process-wide state, all mutex-protected: a
+ *     per-device attribute cache, the launch tracer (gla_profile_*), the saved-forward fingerprints of
+ *     gla_chunk_bwd_saved, and one library-owned side stream per (device, caller stream) on which the TC
+ *     backward runs its second walk concurrently (forked from and joined back into the caller's stream with
+ *     events, so it is also safe inside CUDA-graph stream capture).
  *   - q is NOT scaled by 1/sqrt(d_k): the paper has o_t = q_t S_t; the caller pre-scales.
  *   - log_alpha must be finite and <= 0 (sigma in (0,1) gives log alpha < 0; 0 = linear attention).
  *   - Determinism: fixed reduction order, no atomics: identical inputs give bitwise-identical outputs.
@@ -55,7 +63,9 @@ typedef enum { GLA_BF16 = 0, GLA_FP32 = 1 } gla_dtype;
  *                   otherwise the SIMT path.
  *   GLA_PATH_SIMT : fp32-arithmetic CUDA-core kernels (the "fp32 debug build": any C, c with c | C | T,
  *                   K <= 256, V <= 1024; parity 1e-5 vs the fp64 oracle with fp32 inputs).
- *   GLA_PATH_TC   : bf16 tensor-core kernels (C = 64, c = 16, K in {64,128,256}, V % 64 == 0). */
+ *   GLA_PATH_TC   : bf16 tensor-core kernels: qkv_dtype BF16, C = 64, c | 64 (ignored, see above),
+ *                   K in {64,128,256}, V % 128 == 0.  The TC backward needs K in {128,256} and
+ *                   V / 128 in {1,2,4,8}; other TC-forward shapes run the backward on the SIMT kernels. */
 typedef enum { GLA_PATH_AUTO = 0, GLA_PATH_SIMT = 1, GLA_PATH_TC = 2 } gla_path;
 
 typedef struct {
@@ -104,9 +114,15 @@ int gla_chunk_bwd(const gla_desc *d, const void *q, const void *k, const void *v
  * gla_chunk_bwd_saved -- gla_chunk_bwd reusing the per-chunk operands a preceding gla_chunk_fwd left in its
  * workspace (the "saved activations" of a training step): on the tensor-core path the backward then skips
  * recomputing the chunk-local cumsums, Q~, K~ and P = (Q~ K~^T) (.) M and only forms dP.
- * fwd_workspace: the workspace of a gla_chunk_fwd call with the same descriptor and the same q, k, log_alpha,
- *                not modified since (no ownership transfer; the caller keeps both buffers alive), or NULL
- *                (then identical to gla_chunk_bwd).  Ignored on the SIMT path.
+ * fwd_workspace: the workspace of a gla_chunk_fwd call with the same descriptor and the same q, k, v,
+ *                log_alpha and initial_state (same pointers, same contents), not modified since (no ownership
+ *                transfer; the caller keeps both buffers alive), or NULL (then identical to gla_chunk_bwd).
+ *                The forward's saved data depend on all five inputs (Q~, K~, P and the chunk statistics on
+ *                q, k, log_alpha; the saved anchor and segment-entry states also on v and initial_state).
+ *                The library records which pointers filled each forward workspace; if they differ from this
+ *                call's (or initial_state is present in one call only) the workspace is ignored and the
+ *                backward recomputes.  Contents changed behind identical pointers cannot be detected.
+ *                Ignored on the SIMT path.
  * Results are bitwise identical to gla_chunk_bwd's.  Other arguments, errors: as gla_chunk_bwd.
  */
 int gla_chunk_bwd_saved(const gla_desc *d, const void *q, const void *k, const void *v, const void *log_alpha,
@@ -136,6 +152,10 @@ int gla_recurrent_step(int B, int H, int K, int V, int dtype, int gate_dtype,
  *   gla_state_combine:  H_out = diag(e^{log_decay}) H_in + S_loc        (BH = B*H units; H_out may alias H_in)
  * so that, for consecutive segments r, the state entering r+1 is combine(H_r, D_r, S_loc_r) and the
  * adjoint leaving r-1 is combine(dF_r, D_r, dh0_loc_r).
+ * Paths: when the descriptor resolves to GLA_PATH_TC and K in {128,256}, V % 256 == 0, both summaries run on
+ * the tensor cores (the forward's prep kernel, then one tcgen05 contraction per (b,h) unit) and need
+ * `workspace` of at least gla_fwd_workspace_size(d) bytes (else GLA_ERR_WORKSPACE); otherwise they run the
+ * fp32 CUDA-core kernels and workspace may be NULL.  In gla_dstate_summary the descriptor's V is d_out's.
  */
 int gla_state_summary(const gla_desc *d, const void *k, const void *v, const void *log_alpha,
                       float *S_loc, float *log_decay, void *workspace, size_t workspace_bytes, void *stream);

@@ -104,6 +104,47 @@ def _stream(dev):
     return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
 
+def _same_device(dev, named):
+    for n, t in named:
+        if t is not None and t.device != dev:
+            raise RuntimeError(f"{n} is on {t.device}, expected {dev} (all tensors of one call share a device)")
+
+
+def _shape(t, shape, name):
+    if t is not None and tuple(t.shape) != tuple(shape):
+        raise RuntimeError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+def _check_problem(q, k, v, log_alpha, d_out=None, initial_state=None, d_final_state=None, grads=None):
+    """Shapes and devices of one call.  The C ABI receives only pointers and the descriptor built from q and v,
+    so a mismatched tensor would make the kernels (and their TMA maps) read or write past its end: reject it
+    here, before any launch."""
+    if q.dim() != 4 or v.dim() != 4:
+        raise RuntimeError(f"q and v must be [B,H,T,K] / [B,H,T,V] (got {tuple(q.shape)}, {tuple(v.shape)})")
+    B, H, T, K = q.shape
+    V = v.shape[-1]
+    _shape(k, (B, H, T, K), "k")
+    _shape(log_alpha, (B, H, T, K), "log_alpha")
+    _shape(v, (B, H, T, V), "v")
+    _shape(d_out, (B, H, T, V), "d_out")
+    _shape(initial_state, (B, H, K, V), "initial_state")
+    _shape(d_final_state, (B, H, K, V), "d_final_state")
+    named = [("k", k), ("v", v), ("log_alpha", log_alpha), ("d_out", d_out), ("initial_state", initial_state),
+             ("d_final_state", d_final_state)]
+    if grads is not None:
+        for n, t, shp in zip(("dq", "dk", "dv", "d_log_alpha", "d_initial_state"), grads,
+                             ((B, H, T, K), (B, H, T, K), (B, H, T, V), (B, H, T, K), (B, H, K, V))):
+            _shape(t, shp, n)
+            named.append((n, t))
+    for n, t in named:
+        if t is not None:
+            _check(t, n)
+    for n, t in (("initial_state", initial_state), ("d_final_state", d_final_state)):
+        if t is not None and t.dtype != torch.float32:
+            raise RuntimeError(f"{n} must be fp32")
+    _same_device(q.device, named)
+
+
 def desc(q, v, log_alpha, chunk, subchunk, path) -> _Desc:
     B, H, T, K = q.shape
     return _Desc(B, H, T, K, v.shape[-1], chunk, subchunk, _dt(q), _dt(log_alpha), PATHS[path])
@@ -133,10 +174,13 @@ def bwd_workspace(q, v, log_alpha, chunk=64, subchunk=16, path="auto") -> torch.
 def chunk_fwd(q, k, v, log_alpha, chunk: int = 64, subchunk: int = 16, initial_state=None,
               output_final_state: bool = False, path: str = "auto", out=None, final_state=None, workspace=None):
     """o [B,H,T,V] (q's dtype) and final_state [B,H,K,V] fp32 (or None).  gla_chunk_fwd."""
-    for t, n in ((q, "q"), (k, "k"), (v, "v"), (log_alpha, "log_alpha")):
-        _check(t, n)
+    _check(q, "q")
+    _check_problem(q, k, v, log_alpha, initial_state=initial_state)
     B, H, T, K = q.shape
     V = v.shape[-1]
+    _shape(out, (B, H, T, V), "out")
+    _shape(final_state, (B, H, K, V), "final_state")
+    _same_device(q.device, [("out", out), ("final_state", final_state), ("workspace", workspace)])
     d = desc(q, v, log_alpha, chunk, subchunk, path)
     if out is None:
         out = torch.empty((B, H, T, V), dtype=q.dtype, device=q.device)
@@ -144,9 +188,10 @@ def chunk_fwd(q, k, v, log_alpha, chunk: int = 64, subchunk: int = 16, initial_s
         final_state = torch.empty((B, H, K, V), dtype=torch.float32, device=q.device)
     if workspace is None:
         workspace = fwd_workspace(q, v, log_alpha, chunk, subchunk, path)
-    _call(lib().gla_chunk_fwd, "gla_chunk_fwd", ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(log_alpha),
-          _ptr(initial_state), _ptr(out), _ptr(final_state), _ptr(workspace), workspace.numel(),
-          _stream(q.device))
+    with torch.cuda.device(q.device):
+        _call(lib().gla_chunk_fwd, "gla_chunk_fwd", ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(log_alpha),
+              _ptr(initial_state), _ptr(out), _ptr(final_state), _ptr(workspace), workspace.numel(),
+              _stream(q.device))
     return out, final_state
 
 
@@ -155,8 +200,8 @@ def chunk_bwd(q, k, v, log_alpha, d_out, chunk: int = 64, subchunk: int = 16, in
               workspace=None, fwd_workspace=None):
     """(dq, dk, dv, d_log_alpha fp32, d_initial_state fp32 or None).  gla_chunk_bwd, or gla_chunk_bwd_saved when
     ``fwd_workspace`` (the workspace a chunk_fwd call on the same q, k, log_alpha filled) is given."""
-    for t, n in ((q, "q"), (k, "k"), (v, "v"), (log_alpha, "log_alpha"), (d_out, "d_out")):
-        _check(t, n)
+    _check(q, "q")
+    _check_problem(q, k, v, log_alpha, d_out, initial_state, d_final_state, grads)
     B, H, T, K = q.shape
     d = desc(q, v, log_alpha, chunk, subchunk, path)
     if grads is None:
@@ -168,15 +213,18 @@ def chunk_bwd(q, k, v, log_alpha, d_out, chunk: int = 64, subchunk: int = 16, in
         dq, dk, dv, dg, dh0 = grads
     if workspace is None:
         workspace = bwd_workspace(q, v, log_alpha, chunk, subchunk, path)
-    if fwd_workspace is not None:
-        _check(fwd_workspace, "fwd_workspace")
-        _call(lib().gla_chunk_bwd_saved, "gla_chunk_bwd_saved", ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v),
-              _ptr(log_alpha), _ptr(initial_state), _ptr(d_out), _ptr(d_final_state), _ptr(dq), _ptr(dk), _ptr(dv),
-              _ptr(dg), _ptr(dh0), _ptr(workspace), workspace.numel(), _ptr(fwd_workspace), _stream(q.device))
-        return dq, dk, dv, dg, dh0
-    _call(lib().gla_chunk_bwd, "gla_chunk_bwd", ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(log_alpha),
-          _ptr(initial_state), _ptr(d_out), _ptr(d_final_state), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dg),
-          _ptr(dh0), _ptr(workspace), workspace.numel(), _stream(q.device))
+    _same_device(q.device, [("workspace", workspace), ("fwd_workspace", fwd_workspace)])
+    with torch.cuda.device(q.device):
+        if fwd_workspace is not None:
+            _check(fwd_workspace, "fwd_workspace")
+            _call(lib().gla_chunk_bwd_saved, "gla_chunk_bwd_saved", ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v),
+                  _ptr(log_alpha), _ptr(initial_state), _ptr(d_out), _ptr(d_final_state), _ptr(dq), _ptr(dk),
+                  _ptr(dv), _ptr(dg), _ptr(dh0), _ptr(workspace), workspace.numel(), _ptr(fwd_workspace),
+                  _stream(q.device))
+            return dq, dk, dv, dg, dh0
+        _call(lib().gla_chunk_bwd, "gla_chunk_bwd", ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(log_alpha),
+              _ptr(initial_state), _ptr(d_out), _ptr(d_final_state), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dg),
+              _ptr(dh0), _ptr(workspace), workspace.numel(), _stream(q.device))
     return dq, dk, dv, dg, dh0
 
 
@@ -186,43 +234,70 @@ def recurrent_step(q_t, k_t, v_t, log_alpha_t, state, out=None):
         _check(t, n)
     B, H, K = q_t.shape
     V = v_t.shape[-1]
+    _shape(k_t, (B, H, K), "k_t")
+    _shape(log_alpha_t, (B, H, K), "log_alpha_t")
+    _shape(v_t, (B, H, V), "v_t")
+    _shape(state, (B, H, K, V), "state")
+    if state.dtype != torch.float32:
+        raise RuntimeError("state must be fp32")
     if out is None:
         out = torch.empty((B, H, V), dtype=q_t.dtype, device=q_t.device)
-    _call(lib().gla_recurrent_step, "gla_recurrent_step", B, H, K, V, _dt(q_t), _dt(log_alpha_t), _ptr(q_t),
-          _ptr(k_t), _ptr(v_t), _ptr(log_alpha_t), _ptr(state), _ptr(out), _stream(q_t.device))
+    _shape(out, (B, H, V), "out")
+    _same_device(q_t.device, [("k_t", k_t), ("v_t", v_t), ("log_alpha_t", log_alpha_t), ("state", state),
+                              ("out", out)])
+    with torch.cuda.device(q_t.device):
+        _call(lib().gla_recurrent_step, "gla_recurrent_step", B, H, K, V, _dt(q_t), _dt(log_alpha_t), _ptr(q_t),
+              _ptr(k_t), _ptr(v_t), _ptr(log_alpha_t), _ptr(state), _ptr(out), _stream(q_t.device))
     return out
 
 
-def state_summary(k, v, log_alpha, chunk: int = 64, subchunk: int = 16):
-    """(S_loc [B,H,K,V] fp32, log_decay [B,H,K] fp32) of a segment with zero initial state."""
+def state_summary(k, v, log_alpha, chunk: int = 64, subchunk: int = 16, path: str = "auto", workspace=None):
+    """(S_loc [B,H,K,V] fp32, log_decay [B,H,K] fp32) of a segment with zero initial state (tensor cores when the
+    descriptor resolves to the TC path; the workspace is then a forward workspace)."""
+    _check(k, "k")
+    _check_problem(k, k, v, log_alpha)
     B, H, T, K = k.shape
     V = v.shape[-1]
-    d = desc(k, v, log_alpha, chunk, subchunk, "simt")
+    d = desc(k, v, log_alpha, chunk, subchunk, path)
     S = torch.empty((B, H, K, V), dtype=torch.float32, device=k.device)
     D = torch.empty((B, H, K), dtype=torch.float32, device=k.device)
-    _call(lib().gla_state_summary, "gla_state_summary", ctypes.byref(d), _ptr(k), _ptr(v), _ptr(log_alpha),
-          _ptr(S), _ptr(D), None, 0, _stream(k.device))
+    if workspace is None:
+        workspace = fwd_workspace(k, v, log_alpha, chunk, subchunk, path)
+    with torch.cuda.device(k.device):
+        _call(lib().gla_state_summary, "gla_state_summary", ctypes.byref(d), _ptr(k), _ptr(v), _ptr(log_alpha),
+              _ptr(S), _ptr(D), _ptr(workspace), workspace.numel(), _stream(k.device))
     return S, D
 
 
-def dstate_summary(q, d_out, log_alpha, chunk: int = 64, subchunk: int = 16):
+def dstate_summary(q, d_out, log_alpha, chunk: int = 64, subchunk: int = 16, path: str = "auto", workspace=None):
     """dh0_loc [B,H,K,V] fp32 = d_initial_state of a segment when d_final_state = 0."""
+    _check(q, "q")
+    _check_problem(q, q, d_out, log_alpha)
     B, H, T, K = q.shape
     V = d_out.shape[-1]
-    d = desc(q, d_out, log_alpha, chunk, subchunk, "simt")
+    d = desc(q, d_out, log_alpha, chunk, subchunk, path)
     out = torch.empty((B, H, K, V), dtype=torch.float32, device=q.device)
-    _call(lib().gla_dstate_summary, "gla_dstate_summary", ctypes.byref(d), _ptr(q), _ptr(d_out),
-          _ptr(log_alpha), _ptr(out), None, 0, _stream(q.device))
+    if workspace is None:
+        workspace = fwd_workspace(q, d_out, log_alpha, chunk, subchunk, path)
+    with torch.cuda.device(q.device):
+        _call(lib().gla_dstate_summary, "gla_dstate_summary", ctypes.byref(d), _ptr(q), _ptr(d_out),
+              _ptr(log_alpha), _ptr(out), _ptr(workspace), workspace.numel(), _stream(q.device))
     return out
 
 
 def state_combine(H_in, log_decay, S_loc, out=None):
     """H_out = diag(e^{log_decay}) H_in + S_loc (per (b,h) unit)."""
     B, H, K, V = H_in.shape
+    _shape(log_decay, (B, H, K), "log_decay")
+    _shape(S_loc, (B, H, K, V), "S_loc")
+    for t, n in ((H_in, "H_in"), (log_decay, "log_decay"), (S_loc, "S_loc")):
+        _check(t, n)
     if out is None:
         out = torch.empty_like(H_in)
-    _call(lib().gla_state_combine, "gla_state_combine", B * H, K, V, _ptr(H_in), _ptr(log_decay), _ptr(S_loc),
-          _ptr(out), _stream(H_in.device))
+    _same_device(H_in.device, [("log_decay", log_decay), ("S_loc", S_loc), ("out", out)])
+    with torch.cuda.device(H_in.device):
+        _call(lib().gla_state_combine, "gla_state_combine", B * H, K, V, _ptr(H_in), _ptr(log_decay), _ptr(S_loc),
+              _ptr(out), _stream(H_in.device))
     return out
 
 

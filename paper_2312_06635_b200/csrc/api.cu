@@ -2,6 +2,9 @@
 // No compute here: every step of the method runs in the kernels of simt.cu / tc_*.cu.
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+
 #include "../../include/gla.h"
 #include "simt.h"
 #include "tc.h"
@@ -71,6 +74,37 @@ int copy_or_zero(float* dst, const float* src, size_t n, cudaStream_t st) {
     return cuda_status(e);
 }
 
+// Saved-forward fingerprints (gla_chunk_bwd_saved): the backward reuses per-chunk operands of the forward that
+// depend on q, k, log_alpha (Q~, K~, P, statistics) and, through the saved anchor / segment-entry states, on v and
+// initial_state as well.  Every TC gla_chunk_fwd records which inputs filled its workspace; a saved backward
+// whose inputs differ (another pointer, a different descriptor, h0 present in one call only) ignores the
+// workspace and recomputes instead.  Host-side map keyed by the workspace pointer (mutex-protected).
+struct FwdPrint {
+    const void *q, *k, *v, *g;
+    const float* h0;
+    int B, H, T, K, V, C, c, qt, gt;
+    bool operator==(const FwdPrint& o) const {
+        return q == o.q && k == o.k && v == o.v && g == o.g && h0 == o.h0 && B == o.B && H == o.H && T == o.T &&
+               K == o.K && V == o.V && C == o.C && c == o.c && qt == o.qt && gt == o.gt;
+    }
+};
+std::mutex g_print_mu;
+std::map<const void*, FwdPrint> g_prints;
+
+FwdPrint make_print(const gla_desc* d, const void* q, const void* k, const void* v, const void* g, const float* h0) {
+    return FwdPrint{q, k, v, g, h0, d->B, d->H, d->T, d->K, d->V, d->chunk, d->subchunk, d->qkv_dtype, d->gate_dtype};
+}
+void record_print(const void* ws, const FwdPrint& f) {
+    std::lock_guard<std::mutex> lock(g_print_mu);
+    if (g_prints.size() > 4096) g_prints.clear();   // bounded: stale entries only cost a recompute
+    g_prints[ws] = f;
+}
+bool print_matches(const void* ws, const FwdPrint& f) {
+    std::lock_guard<std::mutex> lock(g_print_mu);
+    auto it = g_prints.find(ws);
+    return it != g_prints.end() && it->second == f;
+}
+
 }  // namespace
 
 extern "C" {
@@ -132,6 +166,7 @@ int gla_chunk_fwd(const gla_desc* d, const void* q, const void* k, const void* v
     gla::Problem p = make_fwd(d, 0);
     p.q = q; p.k = k; p.v = v; p.g = log_alpha; p.h0 = initial_state; p.out = out;
     p.final_state = final_state; p.ws = workspace;
+    if (path == GLA_PATH_TC) record_print(workspace, make_print(d, q, k, v, log_alpha, initial_state));
     return cuda_status(path == GLA_PATH_TC ? gla::tc::fwd(p, st) : gla::simt::fwd(p, st));
 }
 
@@ -157,7 +192,9 @@ int gla_chunk_bwd_saved(const gla_desc* d, const void* q, const void* k, const v
     gla::BwdProblem p = make_bwd(d, 0);
     p.q = q; p.k = k; p.v = v; p.g = log_alpha; p.dO = d_out; p.h0 = initial_state; p.dfinal = d_final_state;
     p.dq = dq; p.dk = dk; p.dv = dv; p.dg = d_log_alpha; p.dh0 = d_initial_state; p.ws = workspace;
-    p.fwd_ws = fwd_workspace;
+    // reuse the forward's operands only if that workspace was filled by a forward on these very inputs
+    p.fwd_ws = (fwd_workspace && print_matches(fwd_workspace, make_print(d, q, k, v, log_alpha, initial_state)))
+                   ? fwd_workspace : nullptr;
     return cuda_status(path == GLA_PATH_TC ? gla::tc::bwd(p, st) : gla::simt::bwd(p, st));
 }
 
@@ -193,6 +230,13 @@ int gla_state_summary(const gla_desc* d, const void* k, const void* v, const voi
         s = copy_or_zero(S_loc, nullptr, BHK * d->V, st);
         return s ? s : copy_or_zero(log_decay, nullptr, BHK, st);
     }
+    if (resolve(d) == GLA_PATH_TC && gla::tc::summary_tc_ok(d->K, d->V)) {
+        // tensor-core contraction (prep + one k_seg_summary per unit); needs the forward's workspace
+        if (workspace_bytes < gla_fwd_workspace_size(d) || !workspace) return GLA_ERR_WORKSPACE;
+        gla::Problem p = make_fwd(d, 0);
+        p.q = k; p.k = k; p.v = v; p.g = log_alpha; p.ws = workspace;
+        return cuda_status(gla::tc::summary_tc(p, v, S_loc, log_decay, false, st));
+    }
     gla::Problem p = make_fwd(d, 1);
     p.q = nullptr; p.k = k; p.v = v; p.g = log_alpha; p.h0 = nullptr; p.out = nullptr;
     p.final_state = S_loc; p.log_decay = log_decay; p.ws = workspace;
@@ -208,6 +252,12 @@ int gla_dstate_summary(const gla_desc* d, const void* q, const void* d_out, cons
     cudaStream_t st = (cudaStream_t)stream;
     if ((size_t)d->B * d->H == 0) return GLA_OK;
     if (d->T == 0) return copy_or_zero(dh0_loc, nullptr, (size_t)d->B * d->H * d->K * d->V, st);
+    if (resolve(d) == GLA_PATH_TC && gla::tc::summary_tc_ok(d->K, d->V)) {
+        if (workspace_bytes < gla_fwd_workspace_size(d) || !workspace) return GLA_ERR_WORKSPACE;
+        gla::Problem pf = make_fwd(d, 0);
+        pf.q = q; pf.k = q; pf.v = d_out; pf.g = log_alpha; pf.ws = workspace;
+        return cuda_status(gla::tc::summary_tc(pf, d_out, dh0_loc, nullptr, true, st));
+    }
     gla::BwdProblem p = make_bwd(d, 1);
     p.q = q; p.k = q; p.g = log_alpha; p.dO = d_out; p.dh0 = dh0_loc; p.ws = workspace;
     return cuda_status(gla::simt::bwd(p, st));

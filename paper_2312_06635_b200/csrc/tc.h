@@ -43,6 +43,10 @@ cudaError_t seg_chain_fwd(const float* stats, const float* h0, const float* S_lo
                           int K, int V, cudaStream_t st);
 cudaError_t seg_chain_bwd(const float* stats, const float* dfinal, const float* dh_loc, float* dFv, int BH, int S,
                           int NC, int K, int V, cudaStream_t st);
+// TC segment summaries of a whole [B,H,T] call (gla_state_summary / gla_dstate_summary): p.q, p.k, p.g as in the
+// forward (adj: p.k may alias p.q), B_op = v (adj = false) or d_out (adj = true); workspace p.ws of fwd_ws size.
+bool summary_tc_ok(int K, int V);
+cudaError_t summary_tc(const Problem& p, const void* B_op, float* out, float* log_decay, bool adj, cudaStream_t st);
 FwdSaved fwd2_saved(const void* ws, int B, int H, int T, int K, int V);
 bool fwd_is_split();              // the forward leaves its per-chunk operands in the workspace (always)
 bool saved_anchors();             // false when GLA_SERIAL_WALKS=1: the forward saves no anchor states and the

@@ -21,7 +21,9 @@
 // backward (simt.cu), which produces every gradient instead (no host synchronisation).
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <utility>
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -1156,20 +1158,22 @@ __global__ void k_copy_seg0(float* __restrict__ dst, const float* __restrict__ s
     *reinterpret_cast<float4*>(dst + e) = *reinterpret_cast<const float4*>(src + bh * S * KV + off);
 }
 
-// Per-device side stream (non-blocking, created once) and per-thread fork/join events for running the two
-// backward walks concurrently.  Returns nullptr if creation fails (the caller then stays on one stream).
-static cudaStream_t side_stream() {
-    static cudaStream_t streams[64] = {};
+// Side stream for running the two backward walks concurrently: one non-blocking stream per (device, caller
+// stream), created on first use, so callers on different streams never fence into each other's walks (and a
+// stream being captured into a CUDA graph forks only onto its own side stream).  Fork/join events are
+// per thread.  Returns nullptr if creation fails (the caller then stays on one stream).
+static cudaStream_t side_stream(cudaStream_t caller) {
+    static std::map<std::pair<int, cudaStream_t>, cudaStream_t> streams;
     static std::mutex mu;
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> lock(mu);
-    if (!streams[dev]) {
-        cudaStream_t s = nullptr;
-        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-        streams[dev] = s;
-    }
-    return streams[dev];
+    auto it = streams.find({dev, caller});
+    if (it != streams.end()) return it->second;
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    streams[{dev, caller}] = s;
+    return s;
 }
 static cudaEvent_t fork_event(int which) {
     thread_local cudaEvent_t evs[64][3] = {};
@@ -1275,7 +1279,7 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     cudaStream_t sq = st;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     if (saved_anch && !prof::enabled()) {   // (the launch tracer times kernels one at a time)
-        sq = side_stream();
+        sq = side_stream(st);
         if (!sq || !(ev_in = fork_event(0)) || !(ev_out = fork_event(1))) sq = st;
     }
     if (sq != st) {

@@ -862,6 +862,74 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// Standalone segment summaries (gla_state_summary / gla_dstate_summary on the TC path, the per-rank step of the
+// sequence-parallel scan): the prep kernel forms the chunk statistics and the factorised operands
+// (K~hi, Q~hi) once, then one k_seg_summary contraction per (b,h) unit (a single segment) gives
+//   adj = false: S_loc = sum_t (k_t (.) e^{LA_T - LA_t})^T v_t     and log_decay = LA_T (sum of the chunk totals)
+//   adj = true : dh_loc = sum_t (q_t (.) e^{LA_t})^T dO_t
+// The prep's other outputs (P, the exact-path cumsums) are written to the workspace and not used.
+__global__ void k_sum_gamma(const float* __restrict__ stats, float* __restrict__ log_decay, int BH, int NC, int K) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= BH * K) return;
+    const int bh = i / K, m = i % K;
+    float d = 0.f;
+    for (int c = 0; c < NC; ++c) d += stats[((size_t)bh * NC + c) * 2 * K + K + m];
+    log_decay[i] = d;
+}
+
+template <int K, typename TG>
+static cudaError_t launch_summary(const Problem& p, const void* B_op, float* out, float* log_decay, bool adj,
+                                  cudaStream_t st) {
+    const size_t BH = (size_t)p.B * p.H, NC = p.T / CH, rows = BH * p.T;
+    uint8_t* w = (uint8_t*)p.ws;
+    __nv_bfloat16* Qt = (__nv_bfloat16*)w; w += al(rows * K * 2);
+    __nv_bfloat16* Kt = (__nv_bfloat16*)w; w += al(rows * K * 2);
+    __nv_bfloat16* Pm = (__nv_bfloat16*)w; w += al(rows * 64 * 2);
+    float* stats = (float*)w; w += al(BH * NC * 2 * K * 4);
+    int* flags = (int*)w; w += al(BH * NC * 4);
+    float* bws = (float*)w;
+    CUtensorMap mQ, mK, mP, mB;
+    cudaError_t e;
+    if ((e = make_map_2d(&mQ, Qt, rows, K, true)) != cudaSuccess) return e;
+    if ((e = make_map_2d(&mK, Kt, rows, K, true)) != cudaSuccess) return e;
+    if ((e = make_map_2d(&mP, Pm, rows, 64, true)) != cudaSuccess) return e;
+    if ((e = make_map_2d(&mB, B_op, rows, p.V, true)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_fwd_prep<K, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)PrepCfg<K>::SMEM)))
+        return e;
+    {
+        GLA_PROF("tc::fwd_prep", st);
+        const int nitems = (int)(NC * BH);
+        k_fwd_prep<K, TG><<<(unsigned)(nitems < num_sms() ? nitems : num_sms()), NTH, PrepCfg<K>::SMEM, st>>>(
+            mQ, mK, mP, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k, (const TG*)p.g, stats, flags, bws, p.T,
+            (int)NC, nitems);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    {
+        GLA_PROF(adj ? "tc::dstate_summary" : "tc::state_summary", st);
+        if ((e = seg_summary(mB, adj ? mQ : mK, stats, flags, out, K, p.V, p.T, 1, (int)BH, adj, st)) != cudaSuccess)
+            return e;
+    }
+    if (!adj && log_decay) {
+        const int n = (int)(BH * K);
+        k_sum_gamma<<<(n + 255) / 256, 256, 0, st>>>(stats, log_decay, (int)BH, (int)NC, K);
+    }
+    return cudaGetLastError();
+}
+
+bool summary_tc_ok(int K, int V) { return (K == 128 || K == 256) && seg_summary_ok(K, V); }
+
+cudaError_t summary_tc(const Problem& p, const void* B_op, float* out, float* log_decay, bool adj, cudaStream_t st) {
+    const bool gf = p.gate_dtype == 1;
+    switch (p.K) {
+        case 128: return gf ? launch_summary<128, float>(p, B_op, out, log_decay, adj, st)
+                            : launch_summary<128, __nv_bfloat16>(p, B_op, out, log_decay, adj, st);
+        case 256: return gf ? launch_summary<256, float>(p, B_op, out, log_decay, adj, st)
+                            : launch_summary<256, __nv_bfloat16>(p, B_op, out, log_decay, adj, st);
+        default: return cudaErrorNotSupported;
+    }
+}
+
 cudaError_t fwd2_tc(const Problem& p, cudaStream_t st) {
     const bool gf = p.gate_dtype == 1;
     switch (p.K) {

@@ -52,10 +52,15 @@ def check_bwd(p, C, c, path, tol):
     den = np.maximum(np.abs(b).reshape(BH, -1).max(1), dg_scale(p, ref))
     errs["dlog_alpha"] = float(np.max(np.abs(a - b).reshape(BH, -1).max(1) / den))
     errs["dlog_alpha_strict"] = nerr_slices(a, b)
+    print(f"check_bwd path={path} gate={p.get('gate_kind', 'std')} " +
+          " ".join(f"{n}={e:.2e}" for n, e in errs.items()))
     bad = {n: e for n, e in errs.items() if e >= tol and n != "dlog_alpha_strict"}
     assert not bad, bad
-    if p.get("gate_kind") not in ("extreme", "mixed", "strong"):
-        assert errs["dlog_alpha_strict"] < tol, errs   # plain normwise where the result is well-conditioned
+    # The plain normwise bar holds for every gate except `extreme` (log alpha = -30): there the true d log alpha
+    # is ~1e-13 while its defining summands q.dq, k.dk are O(1) (ratio ~1e13, measured with the oracle), so only
+    # the summand-relative bar above is meaningful (R12).
+    if p.get("gate_kind") != "extreme":
+        assert errs["dlog_alpha_strict"] < tol, errs
     return errs
 
 

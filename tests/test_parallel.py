@@ -56,7 +56,7 @@ def full_problem():
     return p
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, schedule="chain"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     p = full_problem()
@@ -64,8 +64,9 @@ def _worker(rank, world, port, out):
     sl = slice(rank * seg, (rank + 1) * seg)
     q, k, v, g, do = (p[n][:, :, sl].contiguous() for n in ("q", "k", "v", "g", "do"))
     ops = oracle_ops()
-    o, fs, ctx = P.sp_forward(q, k, v, g, ops, initial_state=p["h0"] if rank == 0 else None)
-    grads = P.sp_backward(q, k, v, g, do, ctx, ops, d_final_state=p["dfin"] if rank == world - 1 else None)
+    o, fs, ctx = P.sp_forward(q, k, v, g, ops, initial_state=p["h0"] if rank == 0 else None, schedule=schedule)
+    grads = P.sp_backward(q, k, v, g, do, ctx, ops, d_final_state=p["dfin"] if rank == world - 1 else None,
+                          schedule=schedule)
     torch.save({"o": o, "fs": fs, "grads": grads}, os.path.join(out, f"r{rank}.pt"))
     dist.barrier()
     dist.destroy_process_group()
@@ -79,9 +80,11 @@ def _free_port():
     return port
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sp_scan_gloo(tmp_path, world):
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+@pytest.mark.parametrize("world,schedule", [(2, "chain"), (4, "chain"), (4, "pipelined"), (4, "allgather"),
+                                            (2, "allgather")])
+def test_sp_scan_gloo(tmp_path, world, schedule):
+    """Every exchange schedule reproduces the single-pass oracle on the whole sequence."""
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), schedule), nprocs=world, join=True)
     res = [torch.load(os.path.join(tmp_path, f"r{r}.pt")) for r in range(world)]
     p = full_problem()
     f = {n: _np(p[n]) for n in ("q", "k", "v", "g", "do", "h0", "dfin")}
@@ -94,6 +97,12 @@ def test_sp_scan_gloo(tmp_path, world):
         got = np.concatenate([_np(r["grads"][i]) for r in res], axis=2)
         np.testing.assert_allclose(got, ref, rtol=1e-10, atol=1e-10)
     np.testing.assert_allclose(_np(res[0]["grads"][4]), rdh0, rtol=1e-10, atol=1e-10)
+
+
+def test_shard_seq_whole_chunks():
+    assert [P.shard_seq(32768, r, 8) for r in (0, 7)] == [(0, 4096), (28672, 32768)]
+    with pytest.raises(ValueError):
+        P.shard_seq(1000, 0, 8)
 
 
 def test_shard_bh_covers_batch():
@@ -139,3 +148,50 @@ def test_sp_virtual_ranks_cuda(R):
     for i in range(3):
         got = torch.cat([gr[i] for gr in grads], 2).float().cpu().numpy()
         assert nerr_slices(got, rg[i]) < 2e-2, i
+
+
+def _cuda_worker(rank, world, port, out, schedule):
+    """Two processes on cuda:0 (gloo, host-staged exchange): the CUDA operators across a process boundary."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    Bc, Hc, Tc, Kc, Vc = 1, 2, 1024, 256, 512
+    p = synth.problem(Bc, Hc, Tc, Kc, Vc, seed=5)
+    h0 = synth.state(Bc, Hc, Kc, Vc, 6).cuda()
+    dfin = synth.state(Bc, Hc, Kc, Vc, 7, scale=0.5).cuda()
+    t0, t1 = P.shard_seq(Tc, rank, world)
+    x = {n: p[n][:, :, t0:t1].contiguous().cuda() for n in p}
+    ops = P.cuda_ops()
+    o, fs, ctx = P.sp_forward(x["q"], x["k"], x["v"], x["g"], ops, initial_state=h0 if rank == 0 else None,
+                              schedule=schedule)
+    grads = P.sp_backward(x["q"], x["k"], x["v"], x["g"], x["do"], ctx, ops,
+                          d_final_state=dfin if rank == world - 1 else None, schedule=schedule)
+    torch.cuda.synchronize()
+    torch.save({"o": o.float().cpu(), "fs": fs.cpu(), "grads": [g_.float().cpu() for g_ in grads]},
+               os.path.join(out, f"c{rank}.pt"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("schedule", ["chain", "allgather"])
+def test_sp_two_processes_cuda(tmp_path, schedule):
+    """World size 2, both ranks on cuda:0: the TC summaries, the exchange and the TC fwd/bwd with the received
+    states, against the single-pass fp64 oracle with h0 and d_final_state."""
+    from tests.helpers import nerr_slices
+    world = 2
+    mp.spawn(_cuda_worker, args=(world, _free_port(), str(tmp_path), schedule), nprocs=world, join=True)
+    res = [torch.load(os.path.join(tmp_path, f"c{r}.pt")) for r in range(world)]
+    p = synth.problem(1, 2, 1024, 256, 512, seed=5)
+    f = {n: p[n].double().numpy() for n in p}
+    h0 = synth.state(1, 2, 256, 512, 6).double().numpy()
+    dfin = synth.state(1, 2, 256, 512, 7, scale=0.5).double().numpy()
+    ro, rfs = oracle.fwd(f["q"], f["k"], f["v"], f["g"], h0=h0)
+    rg = oracle.bwd(f["q"], f["k"], f["v"], f["g"], f["do"], h0=h0, d_final=dfin)
+    o = np.concatenate([r["o"].numpy() for r in res], axis=2)
+    assert nerr_slices(o, ro) < 2e-2
+    assert nerr_slices(res[-1]["fs"].numpy(), rfs) < 2e-2
+    for i, name in enumerate(("dq", "dk", "dv", "dlog_alpha")):
+        got = np.concatenate([r["grads"][i].numpy() for r in res], axis=2)
+        assert nerr_slices(got, rg[i]) < 2e-2, name
+    assert nerr_slices(res[0]["grads"][4].numpy(), rg[4]) < 2e-2

@@ -1,0 +1,11 @@
+# Round 2: GPU tests, default bench, multi-rank bench modes on one B200 (ranks share the device).
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -6 | tee gpurun_out/r2_gputests.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 600 python bench.py > gpurun_out/r2_bench.json 2> gpurun_out/r2_bench.err; tail -c 4000 gpurun_out/r2_bench.json
+timeout 600 python bench.py --gpus 2 --steps 5 --warmup 3 --no-e2e > gpurun_out/r2_bench_g2.json 2> gpurun_out/r2_bench_g2.err; tail -c 1500 gpurun_out/r2_bench_g2.json; tail -5 gpurun_out/r2_bench_g2.err
+timeout 600 python bench.py --gpus 2 --steps 5 --warmup 3 --scaling strong --no-e2e > gpurun_out/r2_bench_g2s.json 2>&1; tail -c 600 gpurun_out/r2_bench_g2s.json
+timeout 900 python bench.py --config sp32k --steps 5 --warmup 3 > gpurun_out/r2_sp1.json 2>&1; tail -c 1500 gpurun_out/r2_sp1.json
+for s in chain pipelined allgather; do timeout 900 python bench.py --gpus 2 --config sp32k --schedule $s --steps 5 --warmup 3 --no-e2e > gpurun_out/r2_sp2_$s.json 2>&1; tail -c 1500 gpurun_out/r2_sp2_$s.json; done
