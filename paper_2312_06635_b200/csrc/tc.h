@@ -37,6 +37,13 @@ int fwd_segments(int BH, int V, int NC);
 // adj = false: out = each segment's end state from a zero start (mA = K~hi map, mB = v map);
 // adj = true: out = each segment's d_initial_state with a zero d_final_state (mA = Q~hi map, mB = dO map).
 bool seg_summary_ok(int K, int V);
+// The K-tiled dq walk (tc_kwalk.cu): channels on the TMEM lanes, value halves of 256 paired in a 2-CTA cluster
+// whose DSMEM exchange completes dq inside the walk.  Writes dq (bf16, final) and, with dfinal, the final-state
+// row sums stdot [V/256][units][K] (one partial per value half).
+bool dq_kwalk_ok(int K, int V);
+cudaError_t dq_kwalk(int K, int V, bool gate_f32, const CUtensorMap& mK, const CUtensorMap& mDP,
+                     const CUtensorMap& mV, const CUtensorMap& mD, const float* stats, const void* g, const float* h0,
+                     const float* dfinal, void* dq, float* stdot, const int* flag, int T, int units, cudaStream_t st);
 cudaError_t seg_summary(const CUtensorMap& mB, const CUtensorMap& mA, const float* stats, const int* flags, float* out,
                         int K, int V, int Tv, int S, int units, bool adj, cudaStream_t st);
 cudaError_t seg_chain_fwd(const float* stats, const float* h0, const float* S_loc, float* Hv, int BH, int S, int NC,

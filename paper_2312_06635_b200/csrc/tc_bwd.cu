@@ -73,23 +73,26 @@ __device__ __forceinline__ void m64_epilogue(uint32_t tcol, uint32_t lane_base, 
 // partials, q, k, log alpha ([64 rows x 64 channels] each) -- staged in shared memory by TMA (SWIZZLE_128B) two
 // chunks ahead, so the HBM latency of the partials overlaps the scans of the chunks in between (the register-
 // prefetched version waited on its loads: ncu long-scoreboard stalls at the first use of every partial).
-template <int NVT, typename TG>
+// DQF: dq arrives final (the K-tiled dq walk, tc_kwalk.cu): one dq tile, no e^{b-r} scaling, dq not written.
+template <int NVT, typename TG, bool DQF = false>
 struct RedCfg {
+    static constexpr int NQ = DQF ? 1 : NVT;                             // dq tiles per chunk
     static constexpr uint32_t TILE = 8192;                               // [64 rows][64 bf16] or [64][32 fp32]
     static constexpr uint32_t GT = 64 * 64 * sizeof(TG);                 // log alpha tile bytes
-    static constexpr uint32_t STAGE = (2 * NVT + 2) * TILE + GT;
+    static constexpr uint32_t STAGE = (NQ + NVT + 2) * TILE + GT;
     static constexpr int NS = 2 * STAGE + 64 * 65 * 4 + 1024 <= 232448 ? 2 : 1;
     static constexpr uint32_t SMEM = NS * STAGE + 1024;
 };
 
-template <int K, int NVT, typename TG>
+template <int K, int NVT, typename TG, bool DQF>
 __global__ void __launch_bounds__(288, 1)
 k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmDQP,
-                 const __grid_constant__ CUtensorMap tmDKP, const float* __restrict__ stdot,
+                 const __grid_constant__ CUtensorMap tmDKP, const float* __restrict__ stdot, int n_stdot,
                  __nv_bfloat16* __restrict__ dq, __nv_bfloat16* __restrict__ dk, float* __restrict__ dg,
                  const float* __restrict__ cpart, const int* __restrict__ flag, int T, int BH) {
-    using RC = RedCfg<NVT, TG>;
+    using RC = RedCfg<NVT, TG, DQF>;
+    constexpr int NQ = RC::NQ;
     if (*flag) return;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_align1k(smem_raw);
@@ -109,17 +112,15 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         uint64_t* b = &bar[i % RC::NS];
         const int row = (int)(head_row + (size_t)i * CH);
         mbar_expect_tx(b, RC::STAGE);
-        for (int j = 0; j < NVT; ++j) {
-            tma_load_2d(st + j * RC::TILE, &tmDQP, b, m0, row + j * BH * T);
-            tma_load_2d(st + (NVT + j) * RC::TILE, &tmDKP, b, m0, row + j * BH * T);
-        }
-        tma_load_2d(st + 2 * NVT * RC::TILE, &tmQ, b, m0, row);
-        tma_load_2d(st + (2 * NVT + 1) * RC::TILE, &tmK, b, m0, row);
+        for (int j = 0; j < NQ; ++j) tma_load_2d(st + j * RC::TILE, &tmDQP, b, m0, row + j * BH * T);
+        for (int j = 0; j < NVT; ++j) tma_load_2d(st + (NQ + j) * RC::TILE, &tmDKP, b, m0, row + j * BH * T);
+        tma_load_2d(st + (NQ + NVT) * RC::TILE, &tmQ, b, m0, row);
+        tma_load_2d(st + (NQ + NVT + 1) * RC::TILE, &tmK, b, m0, row);
         if (sizeof(TG) == 4) {
-            tma_load_2d(st + (2 * NVT + 2) * RC::TILE, &tmG, b, m0, row);
-            tma_load_2d(st + (2 * NVT + 2) * RC::TILE + 8192, &tmG, b, m0 + 32, row);
+            tma_load_2d(st + (NQ + NVT + 2) * RC::TILE, &tmG, b, m0, row);
+            tma_load_2d(st + (NQ + NVT + 2) * RC::TILE + 8192, &tmG, b, m0 + 32, row);
         } else {
-            tma_load_2d(st + (2 * NVT + 2) * RC::TILE, &tmG, b, m0, row);
+            tma_load_2d(st + (NQ + NVT + 2) * RC::TILE, &tmG, b, m0, row);
         }
     };
     if (tid == 0) {
@@ -146,7 +147,7 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         float c0 = 0.f;
         if (i_hi == NC - 1) {
             if (stdot)
-                for (int j = 0; j < NVT; ++j) c0 += stdot[((size_t)j * BH + bh) * K + m0 + tid];
+                for (int j = 0; j < n_stdot; ++j) c0 += stdot[((size_t)j * BH + bh) * K + m0 + tid];
         } else {
             const size_t a2 = (i_hi + 1) / ANCH - 1;
             for (int j = 0; j < NVT; ++j) c0 += cpart[((a2 * NVT + j) * BH + bh) * K + m0 + tid];
@@ -169,7 +170,7 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         mbar_wait(&bar[sidx], (uses[sidx]++) & 1);
         // (a1) chunk-local cumsum: stage g, one thread per channel scans the 64 rows
         {
-            const uint8_t* gt = st + (2 * NVT + 2) * RC::TILE;
+            const uint8_t* gt = st + (NQ + NVT + 2) * RC::TILE;
             float gv[16];
             if (sizeof(TG) == 4) {
                 const uint8_t* box = gt + (cg >> 1) * 8192;
@@ -207,22 +208,24 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 #pragma unroll
             for (int w = 0; w < 8; ++w) { sq[w] = 0.f; sk[w] = 0.f; }
 #pragma unroll
-            for (int j = 0; j < NVT; ++j) {
+            for (int j = 0; j < NQ; ++j) {
                 const uint4 a = *reinterpret_cast<const uint4*>(st + j * RC::TILE + o);
-                const uint4 b = *reinterpret_cast<const uint4*>(st + (NVT + j) * RC::TILE + o);
 #pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    sq[2 * w] += bf16lo(word(a, w)); sq[2 * w + 1] += bf16hi(word(a, w));
-                    sk[2 * w] += bf16lo(word(b, w)); sk[2 * w + 1] += bf16hi(word(b, w));
-                }
+                for (int w = 0; w < 4; ++w) { sq[2 * w] += bf16lo(word(a, w)); sq[2 * w + 1] += bf16hi(word(a, w)); }
             }
-            const uint4 qv = *reinterpret_cast<const uint4*>(st + 2 * NVT * RC::TILE + o);
-            const uint4 kv = *reinterpret_cast<const uint4*>(st + (2 * NVT + 1) * RC::TILE + o);
+#pragma unroll
+            for (int j = 0; j < NVT; ++j) {
+                const uint4 b = *reinterpret_cast<const uint4*>(st + (NQ + j) * RC::TILE + o);
+#pragma unroll
+                for (int w = 0; w < 4; ++w) { sk[2 * w] += bf16lo(word(b, w)); sk[2 * w + 1] += bf16hi(word(b, w)); }
+            }
+            const uint4 qv = *reinterpret_cast<const uint4*>(st + (NQ + NVT) * RC::TILE + o);
+            const uint4 kv = *reinterpret_cast<const uint4*>(st + (NQ + NVT + 1) * RC::TILE + o);
 #pragma unroll
             for (int w = 0; w < 8; ++w) {
                 const int u = 8 * c + w;
                 const float b = sb[t][16 * cg + u], r = sb[CH / 2 - 1][16 * cg + u];
-                dqv[u] = sq[w] * ex2f((b - r) * L2E);
+                dqv[u] = DQF ? sq[w] : sq[w] * ex2f((b - r) * L2E);
                 dkv[u] = sk[w] * ex2f((r - b) * L2E);
                 const float qf = (w & 1) ? bf16hi(word(qv, w >> 1)) : bf16lo(word(qv, w >> 1));
                 const float kf = (w & 1) ? bf16hi(word(kv, w >> 1)) : bf16lo(word(kv, w >> 1));
@@ -236,7 +239,7 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                                         pack_bf16(dqv[8 * u + 4], dqv[8 * u + 5]), pack_bf16(dqv[8 * u + 6], dqv[8 * u + 7]));
             const uint4 ok = make_uint4(pack_bf16(dkv[8 * u], dkv[8 * u + 1]), pack_bf16(dkv[8 * u + 2], dkv[8 * u + 3]),
                                         pack_bf16(dkv[8 * u + 4], dkv[8 * u + 5]), pack_bf16(dkv[8 * u + 6], dkv[8 * u + 7]));
-            *reinterpret_cast<uint4*>(dq + ix + 8 * u) = oq;
+            if (!DQF) *reinterpret_cast<uint4*>(dq + ix + 8 * u) = oq;
             *reinterpret_cast<uint4*>(dk + ix + 8 * u) = ok;
         }
         named_bar_sync(1, 256);            // everyone has read b and the stage buffers
@@ -1286,11 +1289,20 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         if ((e = cudaEventRecord(ev_in, st)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(sq, ev_in, 0)) != cudaSuccess) return e;
     }
+    // With the forward's anchors the dq walk is the K-tiled one (tc_kwalk.cu): dq leaves it complete (no V-tile
+    // partials); the reduce then only sums the dk partials and forms d log alpha.
+    const bool kw = saved_anch && dq_kwalk_ok(K, p.V);
     {
         GLA_PROF("tc::bwd_dq", sq);
-        k_bwd_dq3<K><<<grid, Dq3Cfg<K>::NTHR, Dq3Cfg<K>::SMEM, sq>>>(mK, mDP, mV, mD, stats, h0w, dfin, dqp,
-                                                                    dfin ? stdot : nullptr,
-                                                                    saved_anch ? nullptr : anch, flag, Tv, p.V);
+        if (kw) {
+            if ((e = dq_kwalk(K, p.V, sizeof(TG) == 4, mK, mDP, mV, mD, stats, p.g, h0w, dfin, p.dq,
+                              dfin ? stdot : nullptr, flag, Tv, BHv, sq)) != cudaSuccess)
+                return e;
+        } else {
+            k_bwd_dq3<K><<<grid, Dq3Cfg<K>::NTHR, Dq3Cfg<K>::SMEM, sq>>>(mK, mDP, mV, mD, stats, h0w, dfin, dqp,
+                                                                        dfin ? stdot : nullptr,
+                                                                        saved_anch ? nullptr : anch, flag, Tv, p.V);
+        }
     }
     {
         GLA_PROF("tc::bwd_dkv", st);
@@ -1320,23 +1332,31 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         if ((e = make_map_2d_ex(&mKr, p.k, 2, rows, K, 64, 64, true)) != cudaSuccess) return e;
         if ((e = make_map_2d_ex(&mGr, p.g, (int)sizeof(TG), rows, K, sizeof(TG) == 4 ? 32 : 64, 64, true)) != cudaSuccess)
             return e;
-        if ((e = make_map_2d_ex(&mDQP, dqp, 2, prow, K, 64, 64, true)) != cudaSuccess) return e;
+        if ((e = make_map_2d_ex(&mDQP, kw ? p.dq : (const void*)dqp, 2, kw ? rows : prow, K, 64, 64, true)) != cudaSuccess)
+            return e;
         if ((e = make_map_2d_ex(&mDKP, dkp, 2, prow, K, 64, 64, true)) != cudaSuccess) return e;
         const float* sd = dfin ? stdot : nullptr;
         __nv_bfloat16 *dq_ = (__nv_bfloat16*)p.dq, *dk_ = (__nv_bfloat16*)p.dk;
         const int NCv = NC / S;
         const dim3 rg(K / 64, BHv, (NCv + ANCH - 1) / ANCH);
-#define GLA_RED(N)                                                                                                  \
+#define GLA_RED(N, DQF)                                                                                            \
     case N:                                                                                                         \
-        if ((e = cudaFuncSetAttribute(k_bwd_reduce_tma<K, N, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                                      (int)RedCfg<N, TG>::SMEM)) != cudaSuccess)                                    \
+        if ((e = cudaFuncSetAttribute(k_bwd_reduce_tma<K, N, TG, DQF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                      (int)RedCfg<N, TG, DQF>::SMEM)) != cudaSuccess)                               \
             return e;                                                                                               \
-        k_bwd_reduce_tma<K, N, TG><<<rg, 288, RedCfg<N, TG>::SMEM, st>>>(mQr, mKr, mGr, mDQP, mDKP, sd, dq_, dk_,   \
-                                                                          p.dg, cpart, flag, Tv, BHv);              \
+        k_bwd_reduce_tma<K, N, TG, DQF><<<rg, 288, RedCfg<N, TG, DQF>::SMEM, st>>>(                                 \
+            mQr, mKr, mGr, mDQP, mDKP, sd, DQF ? p.V / 256 : NVT, dq_, dk_, p.dg, cpart, flag, Tv, BHv);            \
         break;
-        switch (NVT) {
-            GLA_RED(1) GLA_RED(2) GLA_RED(4) GLA_RED(8)
-            default: return cudaErrorNotSupported;
+        if (kw) {
+            switch (NVT) {
+                GLA_RED(1, true) GLA_RED(2, true) GLA_RED(4, true)
+                default: return cudaErrorNotSupported;
+            }
+        } else {
+            switch (NVT) {
+                GLA_RED(1, false) GLA_RED(2, false) GLA_RED(4, false) GLA_RED(8, false)
+                default: return cudaErrorNotSupported;
+            }
         }
 #undef GLA_RED
     }
