@@ -94,6 +94,8 @@ def kernel_algo(name, K, V, C, c, g=4, e=2):
         "tc::bwd_dp": ((C + c) * V, e * V + e * V),                             # dP = dO V^T; reads dO, v
         "tc::bwd_prep": ((C + c) * V, e * V + e * V),
         "tc::bwd_dq": (2 * K * V + (C + 1) * K, 0),                             # dq inter + intra
+        "tc::bwd_dk": (2 * K * V + (C + 1) * K, 0),                             # dk inter + intra (K-tiled walk)
+        "tc::bwd_dv": (4 * K * V + (C + c) * V, e * V),                         # dH update, dv inter + intra; writes dv
         "tc::bwd_dkv": (6 * K * V + (C + 1) * K + (C + c) * V, e * V),          # dk, dv inter + intra, dH; writes dv
         "tc::bwd_reduce": (0, 2 * e * K + g * K + 2 * e * K + g * K),           # reads q, k, g; writes dq, dk, dg
     }

@@ -37,13 +37,16 @@ int fwd_segments(int BH, int V, int NC);
 // adj = false: out = each segment's end state from a zero start (mA = K~hi map, mB = v map);
 // adj = true: out = each segment's d_initial_state with a zero d_final_state (mA = Q~hi map, mB = dO map).
 bool seg_summary_ok(int K, int V);
-// The K-tiled dq walk (tc_kwalk.cu): channels on the TMEM lanes, value halves of 256 paired in a 2-CTA cluster
-// whose DSMEM exchange completes dq inside the walk.  Writes dq (bf16, final) and, with dfinal, the final-state
-// row sums stdot [V/256][units][K] (one partial per value half).
-bool dq_kwalk_ok(int K, int V);
-cudaError_t dq_kwalk(int K, int V, bool gate_f32, const CUtensorMap& mK, const CUtensorMap& mDP,
-                     const CUtensorMap& mV, const CUtensorMap& mD, const float* stats, const void* g, const float* h0,
-                     const float* dfinal, void* dq, float* stdot, const int* flag, int T, int units, cudaStream_t st);
+// The K-tiled walks (tc_kwalk.cu): channels on the TMEM lanes, value halves of 256 per CTA.  Each writes its
+// unscaled fp32 partials [V/256][units*T][K] (dq: forward walk, with dfinal also the final-state row sums
+// stdot [V/256][units][K]; dk: reverse walk).  The reduce kernel sums them and applies e^{+-(b - r)}.
+bool kwalk_ok(int K, int V);
+cudaError_t dq_kwalk(int K, int V, const CUtensorMap& mK, const CUtensorMap& mDP, const CUtensorMap& mV,
+                     const CUtensorMap& mD, const float* stats, const float* h0, const float* dfinal, float* dq32,
+                     float* stdot, const int* flag, int T, int units, cudaStream_t st);
+cudaError_t dk_kwalk(int K, int V, const CUtensorMap& mQ, const CUtensorMap& mDP, const CUtensorMap& mD,
+                     const CUtensorMap& mV, const float* stats, const float* dfinal, float* dk32, const int* flag,
+                     int T, int units, cudaStream_t st);
 cudaError_t seg_summary(const CUtensorMap& mB, const CUtensorMap& mA, const float* stats, const int* flags, float* out,
                         int K, int V, int Tv, int S, int units, bool adj, cudaStream_t st);
 cudaError_t seg_chain_fwd(const float* stats, const float* h0, const float* S_loc, float* Hv, int BH, int S, int NC,

@@ -73,26 +73,31 @@ __device__ __forceinline__ void m64_epilogue(uint32_t tcol, uint32_t lane_base, 
 // partials, q, k, log alpha ([64 rows x 64 channels] each) -- staged in shared memory by TMA (SWIZZLE_128B) two
 // chunks ahead, so the HBM latency of the partials overlaps the scans of the chunks in between (the register-
 // prefetched version waited on its loads: ncu long-scoreboard stalls at the first use of every partial).
-// DQF: dq arrives final (the K-tiled dq walk, tc_kwalk.cu): one dq tile, no e^{b-r} scaling, dq not written.
-template <int NVT, typename TG, bool DQF = false>
+// NQ32 > 0: dq and dk arrive as NQ32 unscaled fp32 partials each (one per 256-value half, the K-tiled walks in
+// tc_kwalk.cu), a [64 t][64 k] fp32 tile (two [64][32] SW128 boxes); NQ32 = 0: NVT bf16 V-tile partials each.
+template <int NVT, typename TG, int NQ32 = 0>
 struct RedCfg {
-    static constexpr int NQ = DQF ? 1 : NVT;                             // dq tiles per chunk
+    static constexpr int NQ = NQ32 ? NQ32 : NVT;                         // dq (and dk) partial tiles per chunk
     static constexpr uint32_t TILE = 8192;                               // [64 rows][64 bf16] or [64][32 fp32]
+    static constexpr uint32_t QT = NQ32 ? 2 * TILE : TILE;               // bytes of one partial tile
+    static constexpr uint32_t OFF_DK = NQ * QT;                          // dk partials, then q, k, log alpha
+    static constexpr uint32_t OFF_Q = 2 * NQ * QT;
     static constexpr uint32_t GT = 64 * 64 * sizeof(TG);                 // log alpha tile bytes
-    static constexpr uint32_t STAGE = (NQ + NVT + 2) * TILE + GT;
+    static constexpr uint32_t STAGE = OFF_Q + 2 * TILE + GT;
     static constexpr int NS = 2 * STAGE + 64 * 65 * 4 + 1024 <= 232448 ? 2 : 1;
     static constexpr uint32_t SMEM = NS * STAGE + 1024;
 };
 
-template <int K, int NVT, typename TG, bool DQF>
+template <int K, int NVT, typename TG, int NQ32>
 __global__ void __launch_bounds__(288, 1)
 k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmDQP,
                  const __grid_constant__ CUtensorMap tmDKP, const float* __restrict__ stdot, int n_stdot,
                  __nv_bfloat16* __restrict__ dq, __nv_bfloat16* __restrict__ dk, float* __restrict__ dg,
                  const float* __restrict__ cpart, const int* __restrict__ flag, int T, int BH) {
-    using RC = RedCfg<NVT, TG, DQF>;
+    using RC = RedCfg<NVT, TG, NQ32>;
     constexpr int NQ = RC::NQ;
+    constexpr uint32_t ODK = RC::OFF_DK, OQ = RC::OFF_Q;
     if (*flag) return;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_align1k(smem_raw);
@@ -112,15 +117,21 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         uint64_t* b = &bar[i % RC::NS];
         const int row = (int)(head_row + (size_t)i * CH);
         mbar_expect_tx(b, RC::STAGE);
-        for (int j = 0; j < NQ; ++j) tma_load_2d(st + j * RC::TILE, &tmDQP, b, m0, row + j * BH * T);
-        for (int j = 0; j < NVT; ++j) tma_load_2d(st + (NQ + j) * RC::TILE, &tmDKP, b, m0, row + j * BH * T);
-        tma_load_2d(st + (NQ + NVT) * RC::TILE, &tmQ, b, m0, row);
-        tma_load_2d(st + (NQ + NVT + 1) * RC::TILE, &tmK, b, m0, row);
+        for (int j = 0; j < NQ; ++j) {
+            tma_load_2d(st + j * RC::QT, &tmDQP, b, m0, row + j * BH * T);
+            if (NQ32) tma_load_2d(st + j * RC::QT + RC::TILE, &tmDQP, b, m0 + 32, row + j * BH * T);
+        }
+        for (int j = 0; j < NQ; ++j) {
+            tma_load_2d(st + ODK + j * RC::QT, &tmDKP, b, m0, row + j * BH * T);
+            if (NQ32) tma_load_2d(st + ODK + j * RC::QT + RC::TILE, &tmDKP, b, m0 + 32, row + j * BH * T);
+        }
+        tma_load_2d(st + OQ, &tmQ, b, m0, row);
+        tma_load_2d(st + OQ + RC::TILE, &tmK, b, m0, row);
         if (sizeof(TG) == 4) {
-            tma_load_2d(st + (NQ + NVT + 2) * RC::TILE, &tmG, b, m0, row);
-            tma_load_2d(st + (NQ + NVT + 2) * RC::TILE + 8192, &tmG, b, m0 + 32, row);
+            tma_load_2d(st + OQ + 2 * RC::TILE, &tmG, b, m0, row);
+            tma_load_2d(st + OQ + 2 * RC::TILE + 8192, &tmG, b, m0 + 32, row);
         } else {
-            tma_load_2d(st + (NQ + NVT + 2) * RC::TILE, &tmG, b, m0, row);
+            tma_load_2d(st + OQ + 2 * RC::TILE, &tmG, b, m0, row);
         }
     };
     if (tid == 0) {
@@ -170,7 +181,7 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         mbar_wait(&bar[sidx], (uses[sidx]++) & 1);
         // (a1) chunk-local cumsum: stage g, one thread per channel scans the 64 rows
         {
-            const uint8_t* gt = st + (NQ + NVT + 2) * RC::TILE;
+            const uint8_t* gt = st + OQ + 2 * RC::TILE;
             float gv[16];
             if (sizeof(TG) == 4) {
                 const uint8_t* box = gt + (cg >> 1) * 8192;
@@ -209,23 +220,39 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             for (int w = 0; w < 8; ++w) { sq[w] = 0.f; sk[w] = 0.f; }
 #pragma unroll
             for (int j = 0; j < NQ; ++j) {
-                const uint4 a = *reinterpret_cast<const uint4*>(st + j * RC::TILE + o);
+                if (NQ32) {   // fp32 [64 t][32 k] boxes: channels 16 cg + 8 c .. +8 are chunks 4 (cg & 1) + 2 c, +1
+                    const uint8_t* box = st + j * RC::QT + (cg >> 1) * RC::TILE + t * 128;
+                    const float4 x0 = *reinterpret_cast<const float4*>(box + ((((cg & 1) * 4 + 2 * c) ^ (t & 7)) << 4));
+                    const float4 x1 = *reinterpret_cast<const float4*>(box + ((((cg & 1) * 4 + 2 * c + 1) ^ (t & 7)) << 4));
+                    sq[0] += x0.x; sq[1] += x0.y; sq[2] += x0.z; sq[3] += x0.w;
+                    sq[4] += x1.x; sq[5] += x1.y; sq[6] += x1.z; sq[7] += x1.w;
+                } else {
+                    const uint4 a = *reinterpret_cast<const uint4*>(st + j * RC::TILE + o);
 #pragma unroll
-                for (int w = 0; w < 4; ++w) { sq[2 * w] += bf16lo(word(a, w)); sq[2 * w + 1] += bf16hi(word(a, w)); }
+                    for (int w = 0; w < 4; ++w) { sq[2 * w] += bf16lo(word(a, w)); sq[2 * w + 1] += bf16hi(word(a, w)); }
+                }
             }
 #pragma unroll
-            for (int j = 0; j < NVT; ++j) {
-                const uint4 b = *reinterpret_cast<const uint4*>(st + (NQ + j) * RC::TILE + o);
+            for (int j = 0; j < NQ; ++j) {
+                if (NQ32) {
+                    const uint8_t* box = st + ODK + j * RC::QT + (cg >> 1) * RC::TILE + t * 128;
+                    const float4 x0 = *reinterpret_cast<const float4*>(box + ((((cg & 1) * 4 + 2 * c) ^ (t & 7)) << 4));
+                    const float4 x1 = *reinterpret_cast<const float4*>(box + ((((cg & 1) * 4 + 2 * c + 1) ^ (t & 7)) << 4));
+                    sk[0] += x0.x; sk[1] += x0.y; sk[2] += x0.z; sk[3] += x0.w;
+                    sk[4] += x1.x; sk[5] += x1.y; sk[6] += x1.z; sk[7] += x1.w;
+                } else {
+                    const uint4 b = *reinterpret_cast<const uint4*>(st + ODK + j * RC::TILE + o);
 #pragma unroll
-                for (int w = 0; w < 4; ++w) { sk[2 * w] += bf16lo(word(b, w)); sk[2 * w + 1] += bf16hi(word(b, w)); }
+                    for (int w = 0; w < 4; ++w) { sk[2 * w] += bf16lo(word(b, w)); sk[2 * w + 1] += bf16hi(word(b, w)); }
+                }
             }
-            const uint4 qv = *reinterpret_cast<const uint4*>(st + (NQ + NVT) * RC::TILE + o);
-            const uint4 kv = *reinterpret_cast<const uint4*>(st + (NQ + NVT + 1) * RC::TILE + o);
+            const uint4 qv = *reinterpret_cast<const uint4*>(st + OQ + o);
+            const uint4 kv = *reinterpret_cast<const uint4*>(st + OQ + RC::TILE + o);
 #pragma unroll
             for (int w = 0; w < 8; ++w) {
                 const int u = 8 * c + w;
                 const float b = sb[t][16 * cg + u], r = sb[CH / 2 - 1][16 * cg + u];
-                dqv[u] = DQF ? sq[w] : sq[w] * ex2f((b - r) * L2E);
+                dqv[u] = sq[w] * ex2f((b - r) * L2E);
                 dkv[u] = sk[w] * ex2f((r - b) * L2E);
                 const float qf = (w & 1) ? bf16hi(word(qv, w >> 1)) : bf16lo(word(qv, w >> 1));
                 const float kf = (w & 1) ? bf16hi(word(kv, w >> 1)) : bf16lo(word(kv, w >> 1));
@@ -239,7 +266,7 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                                         pack_bf16(dqv[8 * u + 4], dqv[8 * u + 5]), pack_bf16(dqv[8 * u + 6], dqv[8 * u + 7]));
             const uint4 ok = make_uint4(pack_bf16(dkv[8 * u], dkv[8 * u + 1]), pack_bf16(dkv[8 * u + 2], dkv[8 * u + 3]),
                                         pack_bf16(dkv[8 * u + 4], dkv[8 * u + 5]), pack_bf16(dkv[8 * u + 6], dkv[8 * u + 7]));
-            if (!DQF) *reinterpret_cast<uint4*>(dq + ix + 8 * u) = oq;
+            *reinterpret_cast<uint4*>(dq + ix + 8 * u) = oq;
             *reinterpret_cast<uint4*>(dk + ix + 8 * u) = ok;
         }
         named_bar_sync(1, 256);            // everyone has read b and the stage buffers
@@ -824,15 +851,19 @@ struct Dkv3Cfg {
     static_assert(COL_DV + 128 <= TCOLS, "TMEM columns");
 };
 
-template <int K>
+template <int K, int EMIT>
 __global__ void __launch_bounds__(Dkv3Cfg<K>::NTHR, 1)
 k_bwd_dkv3(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmDP,
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
            const float* __restrict__ stats, const float* __restrict__ dfinal, __nv_bfloat16* __restrict__ dv_out,
            __nv_bfloat16* __restrict__ dkp, float* __restrict__ dh0, const __nv_bfloat16* __restrict__ anch,
-           float* __restrict__ cpart, const int* __restrict__ flag, int T, int V, int emit) {
+           float* __restrict__ cpart, const int* __restrict__ flag, int T, int V) {
+    constexpr int emit = EMIT;   // compile-time: the unused roles' code is removed
     // emit == 0: adjoint-only walk (segment summaries dh_loc): only the Z updates run and only dh0 is written.
+    // emit == 2: dv, the anchor carries and dh0 but no dk (dk comes from the K-tiled dk walk, tc_kwalk.cu).
+    // (Keeping dSB in TMEM, in the then free dk^T columns, as the A operand of TS-mode dv MMAs measured slower:
+    // 188 vs 177 us at 1.3B -- the operand reads compete with the state pass for TMEM bandwidth.)
     using DC = Dkv3Cfg<K>;
     constexpr int NH = DC::NH;
     if (*flag) return;
@@ -876,12 +907,15 @@ k_bwd_dkv3(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     };
     auto loadS = [&](int i) {                  // buffer = step parity (step = NC-1-i)
         const int row = rowb + i * CH, b = (NC - 1 - i) & 1;
-        mbar_expect_tx(&bar_inS[b], 32768 + (intra ? 8192 : 0));
-        tma_load_2d(sV + b * 16384, &tmV, &bar_inS[b], v0, row);
-        tma_load_2d(sV + b * 16384 + 8192, &tmV, &bar_inS[b], v0 + 64, row);
+        const bool dk = emit == 1;             // V and dP feed only the dk MMAs
+        mbar_expect_tx(&bar_inS[b], 16384 + (dk ? 16384 + (intra ? 8192 : 0) : 0));
+        if (dk) {
+            tma_load_2d(sV + b * 16384, &tmV, &bar_inS[b], v0, row);
+            tma_load_2d(sV + b * 16384 + 8192, &tmV, &bar_inS[b], v0 + 64, row);
+        }
         tma_load_2d(sD + b * 16384, &tmD, &bar_inS[b], v0, row);
         tma_load_2d(sD + b * 16384 + 8192, &tmD, &bar_inS[b], v0 + 64, row);
-        if (intra) tma_load_2d(sdP + b * 8192, &tmDP, &bar_inS[b], 0, row);
+        if (dk && intra) tma_load_2d(sdP + b * 8192, &tmDP, &bar_inS[b], 0, row);
     };
     if (warp == 0) tmem_alloc(&tmem_base, DC::TCOLS);
     if (tid == 0) {
@@ -1049,7 +1083,7 @@ k_bwd_dkv3(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
                                            sdesc_sw128(aP + kk * 2048, 8192, 1024), idV2, 1);
                     }
                     if (hh == 0) mma_commit_w(&bar_dva[bs]);
-                } else if (emit) {             // dk^T half
+                } else if (emit == 1) {        // dk^T half
                     if (j >= 1) mbar_wait(&bar_efdk[hh], (j - 1) & 1);
                     tc_fence_after();
 #pragma unroll
@@ -1081,7 +1115,7 @@ k_bwd_dkv3(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
                 mbar_wait(hh == 0 ? &bar_mA : &bar_mB, j & 1);
                 tc_fence_after();
                 if (et == 0 && i > 0) { if (hh == 0) loadA(i - 1); else loadB(i - 1); }
-                if (emit) {
+                if (emit == 1) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         uint32_t r[32];
@@ -1165,21 +1199,22 @@ __global__ void k_copy_seg0(float* __restrict__ dst, const float* __restrict__ s
 // stream), created on first use, so callers on different streams never fence into each other's walks (and a
 // stream being captured into a CUDA graph forks only onto its own side stream).  Fork/join events are
 // per thread.  Returns nullptr if creation fails (the caller then stays on one stream).
-static cudaStream_t side_stream(cudaStream_t caller) {
-    static std::map<std::pair<int, cudaStream_t>, cudaStream_t> streams;
+static cudaStream_t side_stream(cudaStream_t caller, int idx = 0) {
+    static std::map<std::pair<int, std::pair<cudaStream_t, int>>, cudaStream_t> streams;
     static std::mutex mu;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> lock(mu);
-    auto it = streams.find({dev, caller});
+    const auto key = std::make_pair(dev, std::make_pair(caller, idx));
+    auto it = streams.find(key);
     if (it != streams.end()) return it->second;
     cudaStream_t s = nullptr;
     if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-    streams[{dev, caller}] = s;
+    streams[key] = s;
     return s;
 }
 static cudaEvent_t fork_event(int which) {
-    thread_local cudaEvent_t evs[64][3] = {};
+    thread_local cudaEvent_t evs[64][4] = {};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
     if (!evs[dev][which] && cudaEventCreateWithFlags(&evs[dev][which], cudaEventDisableTiming) != cudaSuccess)
@@ -1239,7 +1274,11 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         return e;
     if ((e = cudaFuncSetAttribute(k_bwd_dq3<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Dq3Cfg<K>::SMEM)))
         return e;
-    if ((e = cudaFuncSetAttribute(k_bwd_dkv3<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Dkv3Cfg<K>::SMEM)))
+    if ((e = cudaFuncSetAttribute(k_bwd_dkv3<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Dkv3Cfg<K>::SMEM)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_bwd_dkv3<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Dkv3Cfg<K>::SMEM)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_bwd_dkv3<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Dkv3Cfg<K>::SMEM)))
         return e;
     if (saved) {
         GLA_PROF("tc::bwd_dp", st);
@@ -1267,9 +1306,9 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
             if ((e = seg_summary(mD, mQ, stats, fflags, dhv, K, p.V, Tv, S, BHv, true, st)) != cudaSuccess) return e;
         } else {
             GLA_PROF("tc::bwd_dstate_summary", st);
-            k_bwd_dkv3<K><<<grid, Dkv3Cfg<K>::NTHR, Dkv3Cfg<K>::SMEM, st>>>(
+            k_bwd_dkv3<K, 0><<<grid, Dkv3Cfg<K>::NTHR, Dkv3Cfg<K>::SMEM, st>>>(
                 mQ, mK, mP, mDP, mV, mD, stats, nullptr, (__nv_bfloat16*)p.dv, dkp, dhv, nullptr, cpart, flag, Tv,
-                p.V, 0);
+                p.V);
         }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if ((e = seg_chain_bwd(stats, p.dfinal, dhv, dFv, BH, S, NC, K, p.V, st)) != cudaSuccess) return e;
@@ -1291,12 +1330,14 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     }
     // With the forward's anchors the dq walk is the K-tiled one (tc_kwalk.cu): dq leaves it complete (no V-tile
     // partials); the reduce then only sums the dk partials and forms d log alpha.
-    const bool kw = saved_anch && dq_kwalk_ok(K, p.V);
+    const bool kw = saved_anch && kwalk_ok(K, p.V);
+    float* dq32 = reinterpret_cast<float*>(dqp);   // (V/256) fp32 partials: the same bytes as NVT bf16 ones
+    float* dk32 = reinterpret_cast<float*>(dkp);
     {
         GLA_PROF("tc::bwd_dq", sq);
         if (kw) {
-            if ((e = dq_kwalk(K, p.V, sizeof(TG) == 4, mK, mDP, mV, mD, stats, p.g, h0w, dfin, p.dq,
-                              dfin ? stdot : nullptr, flag, Tv, BHv, sq)) != cudaSuccess)
+            if ((e = dq_kwalk(K, p.V, mK, mDP, mV, mD, stats, h0w, dfin, dq32, dfin ? stdot : nullptr, flag, Tv,
+                              BHv, sq)) != cudaSuccess)
                 return e;
         } else {
             k_bwd_dq3<K><<<grid, Dq3Cfg<K>::NTHR, Dq3Cfg<K>::SMEM, sq>>>(mK, mDP, mV, mD, stats, h0w, dfin, dqp,
@@ -1304,11 +1345,34 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
                                                                         saved_anch ? nullptr : anch, flag, Tv, p.V);
         }
     }
+    if (kw) {
+        GLA_PROF("tc::bwd_dk", st);
+        if ((e = dk_kwalk(K, p.V, mQ, mDP, mD, mV, stats, dfin, dk32, flag, Tv, BHv, st)) != cudaSuccess) return e;
+    }
+    // K-tiled walks: the dv walk runs on a second side stream, concurrently with the dq and dk walks (three
+    // independent 1-CTA-per-SM kernels of ~256 CTAs each fill the 148 SMs better together than one by one).
+    cudaStream_t sv = st;
+    cudaEvent_t ev_dv = nullptr;
+    static const bool dv_side = !getenv("GLA_DV_MAIN");
+    if (kw && sq != st && dv_side) {
+        sv = side_stream(st, 1);
+        if (!sv || !(ev_dv = fork_event(3))) sv = st;
+        else if ((e = cudaStreamWaitEvent(sv, ev_in, 0)) != cudaSuccess) return e;
+    }
     {
-        GLA_PROF("tc::bwd_dkv", st);
-        k_bwd_dkv3<K><<<grid, Dkv3Cfg<K>::NTHR, Dkv3Cfg<K>::SMEM, st>>>(
-            mQ, mK, mP, mDP, mV, mD, stats, dfin, (__nv_bfloat16*)p.dv, dkp, dh0w, saved_anch ? saved_anch : anch,
-            cpart, flag, Tv, p.V, 1);
+        GLA_PROF(kw ? "tc::bwd_dv" : "tc::bwd_dkv", sv);
+        if (kw)
+            k_bwd_dkv3<K, 2><<<grid, Dkv3Cfg<K>::NTHR, Dkv3Cfg<K>::SMEM, sv>>>(
+                mQ, mK, mP, mDP, mV, mD, stats, dfin, (__nv_bfloat16*)p.dv, dkp, dh0w, saved_anch ? saved_anch : anch,
+                cpart, flag, Tv, p.V);
+        else
+            k_bwd_dkv3<K, 1><<<grid, Dkv3Cfg<K>::NTHR, Dkv3Cfg<K>::SMEM, sv>>>(
+                mQ, mK, mP, mDP, mV, mD, stats, dfin, (__nv_bfloat16*)p.dv, dkp, dh0w, saved_anch ? saved_anch : anch,
+                cpart, flag, Tv, p.V);
+    }
+    if (sv != st) {
+        if ((e = cudaEventRecord(ev_dv, sv)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(st, ev_dv, 0)) != cudaSuccess) return e;
     }
     // The exact-fallback gate (one-warp kernel; tail-launches the CUDA-core backward only when a chunk failed
     // the guard) runs on the dq stream right after the dq walk, overlapping the dkv walk and the reduce; the TC
@@ -1332,29 +1396,38 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         if ((e = make_map_2d_ex(&mKr, p.k, 2, rows, K, 64, 64, true)) != cudaSuccess) return e;
         if ((e = make_map_2d_ex(&mGr, p.g, (int)sizeof(TG), rows, K, sizeof(TG) == 4 ? 32 : 64, 64, true)) != cudaSuccess)
             return e;
-        if ((e = make_map_2d_ex(&mDQP, kw ? p.dq : (const void*)dqp, 2, kw ? rows : prow, K, 64, 64, true)) != cudaSuccess)
+        if (kw) {   // fp32 partials [V/256][BH*T][K], boxes [64 rows][32 fp32]
+            if ((e = make_map_2d_ex(&mDQP, dq32, 4, (uint64_t)(p.V / 256) * rows, K, 32, 64, true)) != cudaSuccess)
+                return e;
+        } else if ((e = make_map_2d_ex(&mDQP, dqp, 2, prow, K, 64, 64, true)) != cudaSuccess) {
             return e;
-        if ((e = make_map_2d_ex(&mDKP, dkp, 2, prow, K, 64, 64, true)) != cudaSuccess) return e;
+        }
+        if (kw) {
+            if ((e = make_map_2d_ex(&mDKP, dk32, 4, (uint64_t)(p.V / 256) * rows, K, 32, 64, true)) != cudaSuccess)
+                return e;
+        } else if ((e = make_map_2d_ex(&mDKP, dkp, 2, prow, K, 64, 64, true)) != cudaSuccess) {
+            return e;
+        }
         const float* sd = dfin ? stdot : nullptr;
         __nv_bfloat16 *dq_ = (__nv_bfloat16*)p.dq, *dk_ = (__nv_bfloat16*)p.dk;
         const int NCv = NC / S;
         const dim3 rg(K / 64, BHv, (NCv + ANCH - 1) / ANCH);
-#define GLA_RED(N, DQF)                                                                                            \
+#define GLA_RED(N, NQ32)                                                                                           \
     case N:                                                                                                         \
-        if ((e = cudaFuncSetAttribute(k_bwd_reduce_tma<K, N, TG, DQF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                      (int)RedCfg<N, TG, DQF>::SMEM)) != cudaSuccess)                               \
+        if ((e = cudaFuncSetAttribute(k_bwd_reduce_tma<K, N, TG, NQ32>, cudaFuncAttributeMaxDynamicSharedMemorySize,\
+                                      (int)RedCfg<N, TG, NQ32>::SMEM)) != cudaSuccess)                              \
             return e;                                                                                               \
-        k_bwd_reduce_tma<K, N, TG, DQF><<<rg, 288, RedCfg<N, TG, DQF>::SMEM, st>>>(                                 \
-            mQr, mKr, mGr, mDQP, mDKP, sd, DQF ? p.V / 256 : NVT, dq_, dk_, p.dg, cpart, flag, Tv, BHv);            \
+        k_bwd_reduce_tma<K, N, TG, NQ32><<<rg, 288, RedCfg<N, TG, NQ32>::SMEM, st>>>(                               \
+            mQr, mKr, mGr, mDQP, mDKP, sd, NQ32 ? NQ32 : NVT, dq_, dk_, p.dg, cpart, flag, Tv, BHv);                \
         break;
-        if (kw) {
+        if (kw) {   // V = 256 (NVT 2, one fp32 partial) or V = 512 (NVT 4, two)
             switch (NVT) {
-                GLA_RED(1, true) GLA_RED(2, true) GLA_RED(4, true)
+                GLA_RED(2, 1) GLA_RED(4, 2)
                 default: return cudaErrorNotSupported;
             }
         } else {
             switch (NVT) {
-                GLA_RED(1, false) GLA_RED(2, false) GLA_RED(4, false) GLA_RED(8, false)
+                GLA_RED(1, 0) GLA_RED(2, 0) GLA_RED(4, 0) GLA_RED(8, 0)
                 default: return cudaErrorNotSupported;
             }
         }
