@@ -165,6 +165,38 @@ int gla_state_combine(int BH, int K, int V, const float *H_in, const float *log_
                       float *H_out, void *stream);
 
 /*
+ * GLA layer: the elementwise stages of a full multi-head GLA layer around the core
+ * (P:298-307 multi-head GLA layer with per-head LayerNorm and Swish output gate; P:321-326 low-rank gate with
+ * beta == 1; P:177 log-space temperature tau).  The projections x W are plain GEMMs done by the caller (cuBLAS).
+ * All pointers are device pointers, 16-byte aligned; P is the projection output [B*T][ldP] bf16 with column
+ * blocks q (H*K) | k (H*K) | v (H*V) | r (H*V) (ldP >= 2HK + 2HV, ldP % 8 == 0); z_alpha [B*T][H*K] bf16 is the
+ * low-rank gate pre-activation x W1 W2; parameters are fp32.  Constraints: K % 8 == 0, V in {256,512,768,1024},
+ * H <= 32.  Errors as the core's; workspace-taking calls need gla_layer_bwd_workspace_size() bytes.
+ *
+ * gla_layer_prep:  q, k [B,H,T,K], v [B,H,T,V] (bf16, transposed out of P) and
+ *                  log_alpha [B,H,T,K] fp32 = logsigmoid(z_alpha + b_alpha) / tau.
+ * gla_layer_out:   Z [B*T][H*V] bf16 = concat_h(LN(O^h) * ln_w + ln_b) (.) Swish(r + b_r), O [B,H,T,V] bf16 the
+ *                  core's output, LN over each head's V values (eps); r = P[:, r_off : r_off + H*V].  Saves the
+ *                  per-(row, head) mean and rstd [B*T*H] fp32 for the backward.
+ * gla_layer_out_bwd: from dZ: dO [B,H,T,V] bf16 (the core's d_out), d r written into dP's r block (bf16), and
+ *                  d ln_w, d ln_b, d b_r [H*V] fp32 (deterministic fixed-order reductions).
+ * gla_layer_prep_bwd: from the core's dq, dk, dv (bf16) and d_log_alpha (fp32): dP's q | k | v blocks (bf16),
+ *                  d z_alpha [B*T][H*K] bf16 and d b_alpha [H*K] fp32.
+ */
+size_t gla_layer_bwd_workspace_size(int B, int T, int H, int K, int V);
+int gla_layer_prep(int B, int T, int H, int K, int V, float tau, const void *P, int ldP, const void *z_alpha,
+                   const float *b_alpha, void *q, void *k, void *v, float *log_alpha, void *stream);
+int gla_layer_out(int B, int T, int H, int V, const void *O, const void *P, int ldP, int r_off, const float *b_r,
+                  const float *ln_w, const float *ln_b, float eps, void *Z, float *mean, float *rstd, void *stream);
+int gla_layer_out_bwd(int B, int T, int H, int V, const void *dZ, const void *O, const void *P, int ldP, int r_off,
+                      const float *b_r, const float *ln_w, const float *ln_b, const float *mean, const float *rstd,
+                      void *dO, void *dP, float *d_ln_w, float *d_ln_b, float *d_b_r, void *workspace,
+                      size_t workspace_bytes, void *stream);
+int gla_layer_prep_bwd(int B, int T, int H, int K, int V, float tau, const void *dq, const void *dk, const void *dv,
+                       const float *d_log_alpha, const void *z_alpha, const float *b_alpha, void *dP, int ldP,
+                       void *d_z_alpha, float *d_b_alpha, void *workspace, size_t workspace_bytes, void *stream);
+
+/*
  * Launch tracing (the library's own profiler, used by bench.py for the live roofline numbers).
  * When enabled, every kernel launch is bracketed by two cudaEvents recorded on its launching stream.
  * gla_profile_get aggregates by kernel name: fills names[i*64 .. i*64+63] (NUL-terminated), total_ms[i]

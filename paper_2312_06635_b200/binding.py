@@ -58,6 +58,14 @@ def lib():
         L.gla_state_summary.argtypes = [dp, vp, vp, vp, vp, vp, vp, sz, vp]
         L.gla_dstate_summary.argtypes = [dp, vp, vp, vp, vp, vp, sz, vp]
         L.gla_state_combine.argtypes = [ip, ip, ip, vp, vp, vp, vp, vp]
+        fl = ctypes.c_float
+        L.gla_layer_bwd_workspace_size.argtypes = [ip, ip, ip, ip, ip]
+        L.gla_layer_bwd_workspace_size.restype = sz
+        L.gla_layer_prep.argtypes = [ip, ip, ip, ip, ip, fl, vp, ip, vp, vp, vp, vp, vp, vp, vp]
+        L.gla_layer_out.argtypes = [ip, ip, ip, ip, vp, vp, ip, ip, vp, vp, vp, fl, vp, vp, vp, vp]
+        L.gla_layer_out_bwd.argtypes = [ip, ip, ip, ip, vp, vp, vp, ip, ip, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                        vp, sz, vp]
+        L.gla_layer_prep_bwd.argtypes = [ip, ip, ip, ip, ip, fl, vp, vp, vp, vp, vp, vp, vp, ip, vp, vp, vp, sz, vp]
         L.gla_status_string.argtypes = [ip]
         L.gla_status_string.restype = ctypes.c_char_p
         L.gla_resolve_path.argtypes = [dp]
@@ -69,7 +77,7 @@ def lib():
         L.gla_profile_get.restype = ip
         for f in (L.gla_chunk_fwd, L.gla_chunk_bwd, L.gla_recurrent_step, L.gla_state_summary,
                   L.gla_dstate_summary, L.gla_state_combine, L.gla_last_cuda_error, L.gla_version,
-                  L.gla_resolve_path):
+                  L.gla_resolve_path, L.gla_layer_prep, L.gla_layer_out, L.gla_layer_out_bwd, L.gla_layer_prep_bwd):
             f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -78,7 +86,8 @@ def lib():
 EXPORTS = ("gla_fwd_workspace_size", "gla_bwd_workspace_size", "gla_chunk_fwd", "gla_chunk_bwd", "gla_chunk_bwd_saved",
            "gla_recurrent_step", "gla_state_summary", "gla_dstate_summary", "gla_state_combine",
            "gla_status_string", "gla_last_cuda_error", "gla_resolve_path", "gla_version", "gla_profile_enable",
-           "gla_profile_reset", "gla_profile_count", "gla_profile_get")
+           "gla_profile_reset", "gla_profile_count", "gla_profile_get", "gla_layer_bwd_workspace_size",
+           "gla_layer_prep", "gla_layer_out", "gla_layer_out_bwd", "gla_layer_prep_bwd")
 
 
 def _dt(t: torch.Tensor) -> int:
@@ -301,13 +310,102 @@ def state_combine(H_in, log_decay, S_loc, out=None):
     return out
 
 
+# ---- GLA layer stages (include/gla.h "GLA layer"; the module is paper_2312_06635_b200/layer.py) ------------------
+def _need(t, name, dtype, shape=None):
+    _check(t, name)
+    if t.dtype != dtype:
+        raise RuntimeError(f"{name} must be {dtype}")
+    if shape is not None:
+        _shape(t, shape, name)
+
+
+def layer_prep(P, z_alpha, b_alpha, H: int, K: int, V: int, tau: float = 16.0):
+    """q, k [B,H,T,K], v [B,H,T,V] (bf16) and log alpha [B,H,T,K] fp32 from the projection output P [B,T,ldP]
+    (blocks q | k | v | r) and the low-rank gate pre-activation z_alpha [B,T,H*K] (gla_layer_prep)."""
+    B, T, ldP = P.shape
+    _need(P, "P", torch.bfloat16)
+    _need(z_alpha, "z_alpha", torch.bfloat16, (B, T, H * K))
+    _need(b_alpha, "b_alpha", torch.float32, (H * K,))
+    dev = P.device
+    q = torch.empty((B, H, T, K), dtype=torch.bfloat16, device=dev)
+    k = torch.empty_like(q)
+    v = torch.empty((B, H, T, V), dtype=torch.bfloat16, device=dev)
+    g = torch.empty((B, H, T, K), dtype=torch.float32, device=dev)
+    _same_device(dev, [("z_alpha", z_alpha), ("b_alpha", b_alpha)])
+    with torch.cuda.device(dev):
+        _call(lib().gla_layer_prep, "gla_layer_prep", B, T, H, K, V, float(tau), _ptr(P), ldP, _ptr(z_alpha),
+              _ptr(b_alpha), _ptr(q), _ptr(k), _ptr(v), _ptr(g), _stream(dev))
+    return q, k, v, g
+
+
+def layer_out(O, P, r_off: int, b_r, ln_w, ln_b, eps: float = 1e-5):
+    """Z [B,T,H*V] bf16 = concat_h(LN(O^h) ln_w + ln_b) (.) Swish(r + b_r), plus the LN mean / rstd (gla_layer_out)."""
+    B, H, T, V = O.shape
+    _need(O, "O", torch.bfloat16)
+    _need(P, "P", torch.bfloat16)
+    for t, n in ((b_r, "b_r"), (ln_w, "ln_w"), (ln_b, "ln_b")):
+        _need(t, n, torch.float32, (H * V,))
+    dev = O.device
+    Z = torch.empty((B, T, H * V), dtype=torch.bfloat16, device=dev)
+    mean = torch.empty((B, T, H), dtype=torch.float32, device=dev)
+    rstd = torch.empty_like(mean)
+    with torch.cuda.device(dev):
+        _call(lib().gla_layer_out, "gla_layer_out", B, T, H, V, _ptr(O), _ptr(P), P.shape[-1], r_off, _ptr(b_r),
+              _ptr(ln_w), _ptr(ln_b), float(eps), _ptr(Z), _ptr(mean), _ptr(rstd), _stream(dev))
+    return Z, mean, rstd
+
+
+def layer_bwd_workspace(B, T, H, K, V, device):
+    n = lib().gla_layer_bwd_workspace_size(B, T, H, K, V)
+    return torch.empty(max(n, 16), dtype=torch.uint8, device=device)
+
+
+def layer_out_bwd(dZ, O, P, r_off: int, b_r, ln_w, ln_b, mean, rstd, dP, workspace=None):
+    """dO [B,H,T,V] bf16 and (d ln_w, d ln_b, d b_r); d r is written into dP's r block (gla_layer_out_bwd)."""
+    B, H, T, V = O.shape
+    _need(dZ, "dZ", torch.bfloat16, (B, T, H * V))
+    _need(dP, "dP", torch.bfloat16, P.shape)
+    dev = O.device
+    dO = torch.empty_like(O)
+    dw, db, dbr = (torch.empty(H * V, dtype=torch.float32, device=dev) for _ in range(3))
+    if workspace is None:
+        workspace = layer_bwd_workspace(B, T, H, 8, V, dev)
+    with torch.cuda.device(dev):
+        _call(lib().gla_layer_out_bwd, "gla_layer_out_bwd", B, T, H, V, _ptr(dZ), _ptr(O), _ptr(P), P.shape[-1], r_off,
+              _ptr(b_r), _ptr(ln_w), _ptr(ln_b), _ptr(mean), _ptr(rstd), _ptr(dO), _ptr(dP), _ptr(dw), _ptr(db),
+              _ptr(dbr), _ptr(workspace), workspace.numel(), _stream(dev))
+    return dO, dw, db, dbr
+
+
+def layer_prep_bwd(dq, dk, dv, d_log_alpha, z_alpha, b_alpha, dP, tau: float = 16.0, workspace=None):
+    """d z_alpha [B,T,H*K] bf16 and d b_alpha [H*K] fp32; dq, dk, dv go into dP's q | k | v blocks
+    (gla_layer_prep_bwd)."""
+    B, H, T, K = dq.shape
+    V = dv.shape[-1]
+    _need(d_log_alpha, "d_log_alpha", torch.float32, (B, H, T, K))
+    _need(dP, "dP", torch.bfloat16)
+    dev = dq.device
+    dZa = torch.empty((B, T, H * K), dtype=torch.bfloat16, device=dev)
+    dba = torch.empty(H * K, dtype=torch.float32, device=dev)
+    if workspace is None:
+        workspace = layer_bwd_workspace(B, T, H, K, V, dev)
+    with torch.cuda.device(dev):
+        _call(lib().gla_layer_prep_bwd, "gla_layer_prep_bwd", B, T, H, K, V, float(tau), _ptr(dq), _ptr(dk), _ptr(dv),
+              _ptr(d_log_alpha), _ptr(z_alpha), _ptr(b_alpha), _ptr(dP), dP.shape[-1], _ptr(dZa), _ptr(dba),
+              _ptr(workspace), workspace.numel(), _stream(dev))
+    return dZa, dba
+
+
 class GLAFunction(torch.autograd.Function):
-    """Autograd wrapper: forward gla_chunk_fwd, backward gla_chunk_bwd (recomputes, stores no state)."""
+    """Autograd wrapper: forward gla_chunk_fwd, backward gla_chunk_bwd_saved (the forward's workspace -- its
+    per-chunk operands and anchor states -- is kept as the saved activation of the step)."""
 
     @staticmethod
     def forward(ctx, q, k, v, log_alpha, initial_state, chunk, subchunk, path):
-        o, fs = chunk_fwd(q, k, v, log_alpha, chunk, subchunk, initial_state, True, path)
+        ws = fwd_workspace(q, v, log_alpha, chunk, subchunk, path)
+        o, fs = chunk_fwd(q, k, v, log_alpha, chunk, subchunk, initial_state, True, path, workspace=ws)
         ctx.save_for_backward(q, k, v, log_alpha, initial_state)
+        ctx.ws = ws
         ctx.cfg = (chunk, subchunk, path)
         return o, fs
 
@@ -316,7 +414,9 @@ class GLAFunction(torch.autograd.Function):
         q, k, v, g, h0 = ctx.saved_tensors
         chunk, subchunk, path = ctx.cfg
         dq, dk, dv, dg, dh0 = chunk_bwd(q, k, v, g, do.contiguous(), chunk, subchunk, h0,
-                                        None if dfs is None else dfs.contiguous(), h0 is not None, path)
+                                        None if dfs is None else dfs.contiguous(), h0 is not None, path,
+                                        fwd_workspace=ctx.ws)
+        ctx.ws = None
         return dq, dk, dv, dg.to(g.dtype), dh0, None, None, None
 
 

@@ -107,6 +107,10 @@ bool print_matches(const void* ws, const FwdPrint& f) {
 
 }  // namespace
 
+namespace gla {
+void set_last_cuda(int e) { g_last_cuda = e; }
+}  // namespace gla
+
 extern "C" {
 
 int gla_version(void) { return 100; }
