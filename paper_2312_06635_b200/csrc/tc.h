@@ -37,9 +37,10 @@ int fwd_segments(int BH, int V, int NC);
 // adj = false: out = each segment's end state from a zero start (mA = K~hi map, mB = v map);
 // adj = true: out = each segment's d_initial_state with a zero d_final_state (mA = Q~hi map, mB = dO map).
 bool seg_summary_ok(int K, int V);
-// The K-tiled walks (tc_kwalk.cu): channels on the TMEM lanes, value halves of 256 per CTA.  Each writes its
-// unscaled fp32 partials [V/256][units*T][K] (dq: forward walk, with dfinal also the final-state row sums
-// stdot [V/256][units][K]; dk: reverse walk).  The reduce kernel sums them and applies e^{+-(b - r)}.
+// The K-tiled walks (tc_kwalk.cu): channels on the TMEM lanes, value halves of 256 per CTA (a 2-CTA cluster at
+// V = 512 that sums the halves through distributed shared memory).  Each writes the unscaled fp32 rows
+// [units*T][K] summed over all values (dq: forward walk, with dfinal also the final-state row sums
+// stdot [V/256][units][K]; dk: reverse walk).  The reduce kernel applies e^{+-(b - r)} and forms d log alpha.
 bool kwalk_ok(int K, int V);
 cudaError_t dq_kwalk(int K, int V, const CUtensorMap& mK, const CUtensorMap& mDP, const CUtensorMap& mV,
                      const CUtensorMap& mD, const float* stats, const float* h0, const float* dfinal, float* dq32,

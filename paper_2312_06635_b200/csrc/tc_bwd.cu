@@ -1396,14 +1396,14 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         if ((e = make_map_2d_ex(&mKr, p.k, 2, rows, K, 64, 64, true)) != cudaSuccess) return e;
         if ((e = make_map_2d_ex(&mGr, p.g, (int)sizeof(TG), rows, K, sizeof(TG) == 4 ? 32 : 64, 64, true)) != cudaSuccess)
             return e;
-        if (kw) {   // fp32 partials [V/256][BH*T][K], boxes [64 rows][32 fp32]
-            if ((e = make_map_2d_ex(&mDQP, dq32, 4, (uint64_t)(p.V / 256) * rows, K, 32, 64, true)) != cudaSuccess)
+        if (kw) {   // fp32 [BH*T][K], boxes [64 rows][32 fp32]
+            if ((e = make_map_2d_ex(&mDQP, dq32, 4, (uint64_t)rows, K, 32, 64, true)) != cudaSuccess)
                 return e;
         } else if ((e = make_map_2d_ex(&mDQP, dqp, 2, prow, K, 64, 64, true)) != cudaSuccess) {
             return e;
         }
         if (kw) {
-            if ((e = make_map_2d_ex(&mDKP, dk32, 4, (uint64_t)(p.V / 256) * rows, K, 32, 64, true)) != cudaSuccess)
+            if ((e = make_map_2d_ex(&mDKP, dk32, 4, (uint64_t)rows, K, 32, 64, true)) != cudaSuccess)
                 return e;
         } else if ((e = make_map_2d_ex(&mDKP, dkp, 2, prow, K, 64, 64, true)) != cudaSuccess) {
             return e;
@@ -1418,11 +1418,11 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
                                       (int)RedCfg<N, TG, NQ32>::SMEM)) != cudaSuccess)                              \
             return e;                                                                                               \
         k_bwd_reduce_tma<K, N, TG, NQ32><<<rg, 288, RedCfg<N, TG, NQ32>::SMEM, st>>>(                               \
-            mQr, mKr, mGr, mDQP, mDKP, sd, NQ32 ? NQ32 : NVT, dq_, dk_, p.dg, cpart, flag, Tv, BHv);                \
+            mQr, mKr, mGr, mDQP, mDKP, sd, NQ32 ? p.V / 256 : NVT, dq_, dk_, p.dg, cpart, flag, Tv, BHv);            \
         break;
-        if (kw) {   // V = 256 (NVT 2, one fp32 partial) or V = 512 (NVT 4, two)
+        if (kw) {   // one combined fp32 dq and dk per element (the walks sum the value halves)
             switch (NVT) {
-                GLA_RED(2, 1) GLA_RED(4, 2)
+                GLA_RED(2, 1) GLA_RED(4, 1)
                 default: return cudaErrorNotSupported;
             }
         } else {

@@ -8,20 +8,25 @@
 //   * SB = bf16(X) stays in TMEM as the A operand (K-major: k rows, v packed in pairs) of the output MMAs
 //     out^T[k][t] = SB[k][v] B^T[v][t] (TS mode) -- SB never touches shared memory;
 //   * the state update X[k][v] += A^T[k][s] B[s][v] is one N = 128 MMA per value half and 16-token step.
-// Each CTA writes its unscaled fp32 partial out^T rows (one partial per value half: 2 at V = 512), which the
-// reduce kernel sums in fp32 and scales by e^{+-(b - r)}; d log alpha is then formed from fp32 dq and dk.
+// At V = 512 the two value halves of a channel group run as a 2-CTA cluster and combine their partials through
+// distributed shared memory: each CTA pushes its partial of the other half's 32 tokens of every chunk into the
+// peer's shared memory (st.async, completion counted on the peer's mbarrier), adds the peer's partial of its own
+// 32 tokens (own + peer: fixed order, deterministic) and writes the combined unscaled fp32 rows of those tokens.
+// The reduce kernel then reads ONE fp32 dq and one dk per element, scales by e^{+-(b - r)} and forms d log alpha.
 //   dq walk (REV = 0): A = K~hi, state B = V, output B = dO (K-major), intra + K~^T dP^T; X_0 = h0; f = e^{pend + r}
 //   dk walk (REV = 1): A = Q~hi, state B = dO, output B = V (K-major), intra + Q~^T dP;  X = dfinal; f = e^{pend + Gamma - r}
 //   warps 0-7   state pass, one value half at a time (X half scaled in place, SB half written), signalled per half
 //   warp 8      state MMA per value half, commits bar_sh[half]
 //   warps 9, 10 out^T = SB[:, half 0] B^T (+ the intra term on value half 0) then += SB[:, half 1] B^T (fixed
 //               order) into a double-buffered TMEM accumulator
-//   warps 11-14 epilogue: accumulator -> fp32 partial rows (coalesced); TMA loads two chunks ahead
+//   warps 11-14 epilogue: accumulator -> (peer exchange) -> combined fp32 rows (coalesced)
+//   warp 15     TMA producer: inputs two chunks ahead
 // Measured alternatives (1.3B shapes): a 2-CTA cluster exchanging the dq partials through DSMEM and scaling by
 // e^{b-r} in the walk's epilogue took the dq walk from ~100 us to ~350 us (the exchange and the per-channel
 // strided scan of log alpha each cost ~100 us); one single-buffered accumulator per value half (so the two
 // halves' MMAs never wait for each other) was 9 us slower than the ordered double-buffered one.
 #include <cstdlib>
+#include <type_traits>
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -46,14 +51,17 @@ struct KwCfg {
     static constexpr uint32_t OFF_S = AT, OFF_O = AT + ST, OFF_P = AT + ST + OT;
     static constexpr uint32_t STAGE = AT + ST + OT + PTB;
     static constexpr uint32_t OFF_RED = 2 * STAGE;            // [2][128] fp32 (final-state row sums)
-    static constexpr uint32_t SMEM = OFF_RED + 2 * 128 * 4 + 1024;
+    // NVH = 2: the peer's partial of our 32 tokens, pushed by the peer: [128 k][32 t + 4 pad] fp32 (the pad
+    // keeps the 16-byte row reads of a quarter warp on distinct banks)
+    static constexpr uint32_t PRS = 36, OFF_PR = OFF_RED + 2 * 128 * 4;
+    static constexpr uint32_t SMEM = OFF_PR + 128 * PRS * 4 + 1024;
     static_assert(SMEM <= 232448, "dynamic shared memory");
-    static constexpr int NST = 256, NTHR = NST + 96 + 128;
+    static constexpr int NST = 256, NTHR = NST + 96 + 128 + 32;   // + warp 15: TMA producer
     static constexpr uint32_t COL_SB = 256, COL_ACC = 384;   // TMEM: X [256] | SB [128] | acc x2 [64 each]
 };
 }  // namespace
 
-template <int K, bool REV>
+template <int K, bool REV, int NVH>
 __global__ void __launch_bounds__(KwCfg::NTHR, 1)
 k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmDP,
             const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmO,
@@ -61,7 +69,8 @@ k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             float* __restrict__ out32, float* __restrict__ stdot, const int* __restrict__ flag, int T, int V,
             int dbg) {
     // x0: the state entering the walk (REV 0: h0, REV 1: d_final_state), NULL = 0.  dfinal (REV 0 only): with
-    // stdot, the final-state row sums rowsum(S_T (.) dS_T) of this value half.
+    // stdot, the final-state row sums rowsum(S_T (.) dS_T) of this value half.  out32: [units * T][K] fp32, the
+    // unscaled dq^T / dk^T rows summed over all values.
     // dbg (GLA_KW_DBG, timing experiments only; results are wrong when set): 4 epilogue only drains the
     // accumulator, 8 no output MMAs
     using Cfg = KwCfg;
@@ -70,6 +79,9 @@ k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     uint8_t* sm = smem_align1k(smem_raw);
     float* red = reinterpret_cast<float*>(sm + Cfg::OFF_RED);
     __shared__ uint64_t bar_in[2], bar_free[2], bar_sbh[2], bar_sh[2], bar_da[2], bar_db[2], bar_efree[2];
+    // NVH = 2 peer handshake (one-arrival barriers of the receiving CTA): bar_pr = the peer's partial landed
+    // (armed with its bytes by us, completed by the peer's st.async), bar_pfree = the peer has read our partial
+    __shared__ uint64_t bar_pr, bar_pfree;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int vh = blockIdx.x, k0 = 128 * blockIdx.y, unit = blockIdx.z;
@@ -101,13 +113,17 @@ k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             mbar_init(&bar_db[j], 1);
             mbar_init(&bar_efree[j], 1);
         }
+        mbar_init(&bar_pr, 1);
+        mbar_init(&bar_pfree, 1);
         fence_mbar_init();
+        if (NVH == 2) mbar_expect_tx(&bar_pr, 32 * 128 * 4);   // phase 0 (the peer may push once in sync)
         prefetch_tmap(&tmA); prefetch_tmap(&tmS); prefetch_tmap(&tmO); prefetch_tmap(&tmDP);
         load_inputs(0);
         if (NC > 1) load_inputs(1);
     }
     tc_fence_before();
-    __syncthreads();
+    if (NVH == 2) cluster_sync_all();        // the peer's barriers are initialised before any remote access
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tX = tmem_base, tSB = tmem_base + Cfg::COL_SB, tAcc = tmem_base + Cfg::COL_ACC;
     const int lq = warp & 3;
@@ -248,36 +264,79 @@ k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             mma_commit_w(&bar_free[b]);
             __syncwarp();
         }
+    } else if (warp == 15) {
+        // ------------------------------------------------------------------ TMA producer
+        if (lane == 0)
+            for (int j = 2; j < NC; ++j) {   // inputs of step j into buffer j & 1 once step j-2's MMAs are done
+                mbar_wait(&bar_free[j & 1], ((j - 2) >> 1) & 1);
+                load_inputs(j);
+            }
     } else {
         // ------------------------------------------------------------------ epilogue warps
-        // Each thread drains one channel row of the accumulator (64 tokens, fp32) into the fp32 partial
-        // out32[vh][unit rows][K] (unscaled): for a fixed token the 32 lanes of a warp write 32 consecutive
-        // channels (128 B), so every store instruction is fully coalesced.
+        // Each thread drains one channel row of the accumulator (64 tokens, fp32).  It writes the unscaled rows
+        // out32[unit rows][K] of the tokens this CTA finishes (all 64, or with NVH = 2 the 32 of value half vh,
+        // after adding the peer's partial): for a fixed token the 32 lanes of a warp write 32 consecutive channels
+        // (128 B), so every store instruction is fully coalesced.
         const int et = tid - Cfg::NST - 96;
-        float* outp = out32 + ((size_t)vh * gridDim.z * T + rowb) * K + kg;
-        for (int j = 0; j < NC; ++j) {
-            const int b = j & 1;
-            if (et == 0 && j + 2 < NC) {     // inputs of step j+2 into buffer b once step j's MMAs are done
-                mbar_wait(&bar_free[b], (j >> 1) & 1);
-                load_inputs(j + 2);
-            }
-            mbar_wait(&bar_db[b], (j >> 1) & 1);
-            tc_fence_after();
-            uint32_t a[32], a2[32];
-            tmem_ld32(tAcc + 64 * b + lane_base, a);
-            tmem_ld32(tAcc + 64 * b + 32 + lane_base, a2);
-            tmem_wait_ld();
-            tc_fence_before();
-            named_bar_sync(2, 128);          // accumulator b drained
-            if (et == 0) mbar_arrive(&bar_efree[b]);
-            if (dbg & 4) continue;
-            float* o = outp + (size_t)chunk_of(j) * CH * K;
+        float* outp = out32 + rowb * K + kg;
+        float* prbuf = reinterpret_cast<float*>(sm + Cfg::OFF_PR);
+        const uint32_t peer_pr = NVH == 2 ? mapa_shared(prbuf, vh ^ 1) : 0u;
+        const uint32_t peer_prb = NVH == 2 ? mapa_shared(&bar_pr, vh ^ 1) : 0u;
+        const uint32_t peer_pfree = NVH == 2 ? mapa_shared(&bar_pfree, vh ^ 1) : 0u;
+        auto walk = [&](auto Hc) {           // H: this CTA's value half, compile-time (static register indexing)
+            constexpr int H = decltype(Hc)::value, T0 = NVH == 2 ? 32 * H : 0, PT = 32 * (H ^ 1);
+            for (int j = 0; j < NC; ++j) {
+                const int b = j & 1;
+                mbar_wait(&bar_db[b], (j >> 1) & 1);
+                tc_fence_after();
+                uint32_t a[32], a2[32];
+                tmem_ld32(tAcc + 64 * b + lane_base, a);
+                tmem_ld32(tAcc + 64 * b + 32 + lane_base, a2);
+                tmem_wait_ld();
+                tc_fence_before();
+                named_bar_sync(2, 128);      // accumulator b drained
+                if (et == 0) mbar_arrive(&bar_efree[b]);
+                if (dbg & 4) continue;
+                float acc[64];
 #pragma unroll
-            for (int t = 0; t < 32; ++t) {
-                o[(size_t)t * K] = __uint_as_float(a[t]);
-                o[(size_t)(32 + t) * K] = __uint_as_float(a2[t]);
+                for (int t = 0; t < 32; ++t) {
+                    acc[t] = __uint_as_float(a[t]);
+                    acc[32 + t] = __uint_as_float(a2[t]);
+                }
+                if (NVH == 2) {
+                    // our partial of the peer's 32 tokens -> the peer's buffer (row kk) once the peer has read the
+                    // previous one; then the peer's partial of ours, added in a fixed order (own + peer)
+                    if (j > 0) mbar_wait_cluster(&bar_pfree, (j - 1) & 1);
+                    const uint32_t dst = peer_pr + 4u * (uint32_t)(kk * Cfg::PRS);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        st_async_v4(dst + 16u * q, make_float4(acc[PT + 4 * q], acc[PT + 4 * q + 1], acc[PT + 4 * q + 2],
+                                                               acc[PT + 4 * q + 3]), peer_prb);
+                    mbar_wait_cluster(&bar_pr, j & 1);
+                    const float4* src = reinterpret_cast<const float4*>(prbuf + kk * Cfg::PRS);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 v = src[q];
+                        acc[T0 + 4 * q] += v.x; acc[T0 + 4 * q + 1] += v.y;
+                        acc[T0 + 4 * q + 2] += v.z; acc[T0 + 4 * q + 3] += v.w;
+                    }
+                    named_bar_sync(2, 128);  // buffer read by every thread
+                    if (et == 0) {
+                        if (j + 1 < NC) mbar_expect_tx(&bar_pr, 32 * 128 * 4);   // arm the next phase first
+                        mbar_arrive_remote_relaxed(peer_pfree);
+                    }
+                }
+                float* o = outp + ((size_t)chunk_of(j) * CH + T0) * K;
+#pragma unroll
+                for (int t = 0; t < (NVH == 2 ? 32 : 64); ++t) o[(size_t)t * K] = acc[T0 + t];
             }
-        }
+        };
+        if (NVH == 1 || vh == 0) walk(std::integral_constant<int, 0>{});
+        else walk(std::integral_constant<int, 1>{});
+    }
+    if (NVH == 2) {                          // no CTA leaves while its peer may still write to it
+        tc_fence_before();
+        cluster_sync_all();
     }
     tc_fence_before();
     __syncthreads();
@@ -286,33 +345,54 @@ k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
 bool kwalk_ok(int K, int V) { return (K == 128 || K == 256) && (V == 256 || V == 512) && !getenv("GLA_DQ3"); }
 
-template <int K, bool REV>
+template <int K, bool REV, int NVH>
 static cudaError_t launch_kw(const CUtensorMap& mA, const CUtensorMap& mDP, const CUtensorMap& mS, const CUtensorMap& mO,
                              const float* stats, const float* x0, const float* dfinal, float* out32, float* stdot,
                              const int* flag, int T, int V, int units, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(k_bwd_kwalk<K, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)KwCfg::SMEM);
+    auto kern = k_bwd_kwalk<K, REV, NVH>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KwCfg::SMEM);
     if (e != cudaSuccess) return e;
     static const int dbg = getenv("GLA_KW_DBG") ? atoi(getenv("GLA_KW_DBG")) : 0;
-    k_bwd_kwalk<K, REV><<<dim3(V / 256, K / 128, (unsigned)units), KwCfg::NTHR, KwCfg::SMEM, st>>>(
-        mA, mDP, mS, mO, stats, x0, dfinal, out32, stdot, flag, T, V, dbg);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(NVH, K / 128, (unsigned)units);
+    cfg.blockDim = dim3(KwCfg::NTHR);
+    cfg.dynamicSmemBytes = KwCfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;   // the value halves of a channel group: one cluster
+    attr[0].val.clusterDim.x = NVH;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if ((e = cudaLaunchKernelEx(&cfg, kern, mA, mDP, mS, mO, stats, x0, dfinal, out32, stdot, flag, T, V, dbg)) !=
+        cudaSuccess)
+        return e;
     return cudaGetLastError();
+}
+
+template <bool REV>
+static cudaError_t kw_dispatch(int K, int V, const CUtensorMap& mA, const CUtensorMap& mDP, const CUtensorMap& mS,
+                               const CUtensorMap& mO, const float* stats, const float* x0, const float* dfinal,
+                               float* out32, float* stdot, const int* flag, int T, int units, cudaStream_t st) {
+#define GLA_KW(KK, NV)                                                                                              \
+    if (K == KK && V == 256 * NV)                                                                                   \
+        return launch_kw<KK, REV, NV>(mA, mDP, mS, mO, stats, x0, dfinal, out32, stdot, flag, T, V, units, st);
+    GLA_KW(128, 1) GLA_KW(128, 2) GLA_KW(256, 1) GLA_KW(256, 2)
+#undef GLA_KW
+    return cudaErrorNotSupported;
 }
 
 cudaError_t dq_kwalk(int K, int V, const CUtensorMap& mK, const CUtensorMap& mDP, const CUtensorMap& mV,
                      const CUtensorMap& mD, const float* stats, const float* h0, const float* dfinal, float* dq32,
                      float* stdot, const int* flag, int T, int units, cudaStream_t st) {
-    if (K == 128) return launch_kw<128, false>(mK, mDP, mV, mD, stats, h0, dfinal, dq32, stdot, flag, T, V, units, st);
-    if (K == 256) return launch_kw<256, false>(mK, mDP, mV, mD, stats, h0, dfinal, dq32, stdot, flag, T, V, units, st);
-    return cudaErrorNotSupported;
+    return kw_dispatch<false>(K, V, mK, mDP, mV, mD, stats, h0, dfinal, dq32, stdot, flag, T, units, st);
 }
 
 cudaError_t dk_kwalk(int K, int V, const CUtensorMap& mQ, const CUtensorMap& mDP, const CUtensorMap& mD,
                      const CUtensorMap& mV, const float* stats, const float* dfinal, float* dk32, const int* flag,
                      int T, int units, cudaStream_t st) {
-    if (K == 128) return launch_kw<128, true>(mQ, mDP, mD, mV, stats, dfinal, nullptr, dk32, nullptr, flag, T, V, units, st);
-    if (K == 256) return launch_kw<256, true>(mQ, mDP, mD, mV, stats, dfinal, nullptr, dk32, nullptr, flag, T, V, units, st);
-    return cudaErrorNotSupported;
+    return kw_dispatch<true>(K, V, mQ, mDP, mD, mV, stats, dfinal, nullptr, dk32, nullptr, flag, T, units, st);
 }
 
 }  // namespace tc
