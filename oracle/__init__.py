@@ -9,6 +9,8 @@ What it computes (see ``gla_oracle.c`` for the passage-by-passage citations):
   * ``bwd``  -- reverse-mode of the same recurrence (the paper gives none),
                pinned by central finite differences in tests/test_oracle.py
   * ``step`` -- one recurrence step (decode)
+  * ``fwd_beta`` / ``bwd_beta`` / ``step_beta`` -- the same with the general outer-product gate
+               G_t = alpha_t^T beta_t (``gla_beta_oracle.c``), gradients including d log beta
 
 Parity pins (tests/test_oracle.py, all ``-m "not gpu"``): quadratic parallel / semiring form
 (P:224-231), alpha == 1 -> (QK^T (.) M)V, alpha == gamma -> RetNet D-mask,
@@ -24,6 +26,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gla_oracle.c")
+_SRC_BETA = os.path.join(_HERE, "gla_beta_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
@@ -32,8 +35,9 @@ _dp = ctypes.POINTER(ctypes.c_double)
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (plain C99 + pthreads, -O2, no fast-math)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-o", _LIB, _SRC,
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_SRC_BETA))
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-o", _LIB, _SRC, _SRC_BETA,
                                "-lm", "-lpthread"])
     return _LIB
 
@@ -48,7 +52,12 @@ def _load():
         lib.oracle_bwd.argtypes = [i, i, i, i, i, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
                                    _dp, _dp, _dp, _dp, _dp, i]
         lib.oracle_step.argtypes = [i, i, i, i, _dp, _dp, _dp, _dp, _dp, _dp]
-        for f in (lib.oracle_fwd, lib.oracle_bwd, lib.oracle_step):
+        lib.oracle_fwd_beta.argtypes = [i, i, i, i, i, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, i]
+        lib.oracle_bwd_beta.argtypes = [i, i, i, i, i, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+                                        _dp, _dp, _dp, _dp, _dp, _dp, i]
+        lib.oracle_step_beta.argtypes = [i, i, i, i, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
+        for f in (lib.oracle_fwd, lib.oracle_bwd, lib.oracle_step, lib.oracle_fwd_beta, lib.oracle_bwd_beta,
+                  lib.oracle_step_beta):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -108,4 +117,51 @@ def step(q, k, v, log_alpha, state):
     rc = _load().oracle_step(B, H, K, V, _p(q), _p(k), _p(v), _p(g), _p(st), _p(o))
     if rc:
         raise RuntimeError(f"oracle_step failed ({rc})")
+    return o, st
+
+
+def fwd_beta(q, k, v, log_alpha, log_beta, h0=None, nthreads=0):
+    """General gate G_t = alpha_t^T beta_t: o [B,H,T,V], final_state [B,H,K,V] in fp64.
+    log_beta [B,H,T,V]."""
+    q, k, v, g, gb = _d(q), _d(k), _d(v), _d(log_alpha), _d(log_beta)
+    B, H, T, K = q.shape
+    V = v.shape[-1]
+    h0 = None if h0 is None else _d(h0)
+    o = np.empty((B, H, T, V))
+    fs = np.empty((B, H, K, V))
+    rc = _load().oracle_fwd_beta(B, H, T, K, V, _p(q), _p(k), _p(v), _p(g), _p(gb), _p(h0), _p(o), _p(fs),
+                                 _threads(nthreads))
+    if rc:
+        raise RuntimeError(f"oracle_fwd_beta failed ({rc})")
+    return o, fs
+
+
+def bwd_beta(q, k, v, log_alpha, log_beta, d_out, h0=None, d_final=None, nthreads=0):
+    """(dq, dk, dv, dlog_alpha, dlog_beta, dh0) in fp64 for loss = <o, d_out> + <final_state, d_final>, general
+    gate G_t = alpha_t^T beta_t."""
+    q, k, v, g, gb, do = _d(q), _d(k), _d(v), _d(log_alpha), _d(log_beta), _d(d_out)
+    B, H, T, K = q.shape
+    V = v.shape[-1]
+    h0 = None if h0 is None else _d(h0)
+    d_final = None if d_final is None else _d(d_final)
+    dq, dk, dga = (np.empty((B, H, T, K)) for _ in range(3))
+    dv, dgb = np.empty((B, H, T, V)), np.empty((B, H, T, V))
+    dh0 = np.empty((B, H, K, V))
+    rc = _load().oracle_bwd_beta(B, H, T, K, V, _p(q), _p(k), _p(v), _p(g), _p(gb), _p(h0), _p(do), _p(d_final),
+                                 _p(dq), _p(dk), _p(dv), _p(dga), _p(dgb), _p(dh0), _threads(nthreads))
+    if rc:
+        raise RuntimeError(f"oracle_bwd_beta failed ({rc})")
+    return dq, dk, dv, dga, dgb, dh0
+
+
+def step_beta(q, k, v, log_alpha, log_beta, state):
+    """One decode step with both gates.  q,k,log_alpha [B,H,K]; v, log_beta [B,H,V]; state [B,H,K,V]."""
+    q, k, v, g, gb = _d(q), _d(k), _d(v), _d(log_alpha), _d(log_beta)
+    B, H, K = q.shape
+    V = v.shape[-1]
+    st = _d(state).copy()
+    o = np.empty((B, H, V))
+    rc = _load().oracle_step_beta(B, H, K, V, _p(q), _p(k), _p(v), _p(g), _p(gb), _p(st), _p(o))
+    if rc:
+        raise RuntimeError(f"oracle_step_beta failed ({rc})")
     return o, st
