@@ -143,6 +143,32 @@ int gla_recurrent_step(int B, int H, int K, int V, int dtype, int gate_dtype,
                        float *state, void *out_t, void *stream);
 
 /*
+ * The general outer-product gate:  G_t = alpha_t^T beta_t,
+ *   S_t = G_t (.) S_{t-1} + k_t^T v_t,  o_t = q_t S_t          (P:188-189 without the beta == 1 simplification)
+ * with log_beta [B,H,T,V] (gate_dtype; finite, <= 0) the value-side gate.  Computed chunk-wise with the paper's
+ * V~ = V / B, O = O~ (.) B rescaling (Eq. gla_QKV2) applied per chunk with a mid-chunk normaliser
+ * (simt_beta.cu), on the fp32 CUDA-core kernels: GLA_PATH_TC returns GLA_ERR_UNSUPPORTED, AUTO / SIMT run it.
+ * Range: the half-chunk log decay of beta must stay below ~60 (the paper's gates give ~2 at C = 64).
+ * gla_chunk_fwd_beta / gla_chunk_bwd_beta: as gla_chunk_fwd / gla_chunk_bwd plus log_beta (in) and
+ *   d_log_beta [B,H,T,V] fp32 (out) = sum_{s >= t} (o (.) do - v (.) dv)_s + colsum(S_T (.) dS_T).
+ *   workspace: at least gla_beta_workspace_size(d) bytes (required, also for the forward).
+ * gla_recurrent_step_beta: one decode step  state <- (alpha_t^T beta_t) (.) state + k_t^T v_t, out_t = q_t state
+ *   (log_beta_t [B,H,V]).
+ */
+size_t gla_beta_workspace_size(const gla_desc *d);
+int gla_chunk_fwd_beta(const gla_desc *d, const void *q, const void *k, const void *v, const void *log_alpha,
+                       const void *log_beta, const float *initial_state, void *out, float *final_state,
+                       void *workspace, size_t workspace_bytes, void *stream);
+int gla_chunk_bwd_beta(const gla_desc *d, const void *q, const void *k, const void *v, const void *log_alpha,
+                       const void *log_beta, const float *initial_state, const void *d_out,
+                       const float *d_final_state, void *dq, void *dk, void *dv, float *d_log_alpha,
+                       float *d_log_beta, float *d_initial_state, void *workspace, size_t workspace_bytes,
+                       void *stream);
+int gla_recurrent_step_beta(int B, int H, int K, int V, int dtype, int gate_dtype, const void *q_t,
+                            const void *k_t, const void *v_t, const void *log_alpha_t, const void *log_beta_t,
+                            float *state, void *out_t, void *stream);
+
+/*
  * Segment / sequence-parallel helpers (chunk-level recurrence as a two-stage scan).
  * For a segment of T tokens with zero initial state:
  *   gla_state_summary:  S_loc = sum_t (k_t (.) e^{LA_T - LA_t})^T v_t  [B,H,K,V] fp32,

@@ -58,6 +58,11 @@ def lib():
         L.gla_state_summary.argtypes = [dp, vp, vp, vp, vp, vp, vp, sz, vp]
         L.gla_dstate_summary.argtypes = [dp, vp, vp, vp, vp, vp, sz, vp]
         L.gla_state_combine.argtypes = [ip, ip, ip, vp, vp, vp, vp, vp]
+        L.gla_beta_workspace_size.argtypes = [dp]
+        L.gla_beta_workspace_size.restype = sz
+        L.gla_chunk_fwd_beta.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        L.gla_chunk_bwd_beta.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        L.gla_recurrent_step_beta.argtypes = [ip, ip, ip, ip, ip, ip, vp, vp, vp, vp, vp, vp, vp, vp]
         fl = ctypes.c_float
         L.gla_layer_bwd_workspace_size.argtypes = [ip, ip, ip, ip, ip]
         L.gla_layer_bwd_workspace_size.restype = sz
@@ -77,7 +82,8 @@ def lib():
         L.gla_profile_get.restype = ip
         for f in (L.gla_chunk_fwd, L.gla_chunk_bwd, L.gla_recurrent_step, L.gla_state_summary,
                   L.gla_dstate_summary, L.gla_state_combine, L.gla_last_cuda_error, L.gla_version,
-                  L.gla_resolve_path, L.gla_layer_prep, L.gla_layer_out, L.gla_layer_out_bwd, L.gla_layer_prep_bwd):
+                  L.gla_resolve_path, L.gla_layer_prep, L.gla_layer_out, L.gla_layer_out_bwd, L.gla_layer_prep_bwd,
+                  L.gla_chunk_fwd_beta, L.gla_chunk_bwd_beta, L.gla_recurrent_step_beta):
             f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -87,7 +93,8 @@ EXPORTS = ("gla_fwd_workspace_size", "gla_bwd_workspace_size", "gla_chunk_fwd", 
            "gla_recurrent_step", "gla_state_summary", "gla_dstate_summary", "gla_state_combine",
            "gla_status_string", "gla_last_cuda_error", "gla_resolve_path", "gla_version", "gla_profile_enable",
            "gla_profile_reset", "gla_profile_count", "gla_profile_get", "gla_layer_bwd_workspace_size",
-           "gla_layer_prep", "gla_layer_out", "gla_layer_out_bwd", "gla_layer_prep_bwd")
+           "gla_layer_prep", "gla_layer_out", "gla_layer_out_bwd", "gla_layer_prep_bwd", "gla_beta_workspace_size",
+           "gla_chunk_fwd_beta", "gla_chunk_bwd_beta", "gla_recurrent_step_beta")
 
 
 def _dt(t: torch.Tensor) -> int:
@@ -442,4 +449,84 @@ def profile_read():
     for i in range(min(cnt, cap)):
         nm = names.raw[64 * i: 64 * i + 64].split(b"\0", 1)[0].decode()
         out[nm] = (float(ms[i]), int(n[i]))
+    return out
+
+
+# ---- the general outer-product gate G_t = alpha_t^T beta_t (gla.h "value gate") ----------------------
+def beta_workspace(q, v, log_alpha, chunk=64, subchunk=16, path="auto") -> torch.Tensor:
+    n = lib().gla_beta_workspace_size(ctypes.byref(desc(q, v, log_alpha, chunk, subchunk, path)))
+    return torch.empty(max(n, 16), dtype=torch.uint8, device=q.device)
+
+
+def _check_beta(q, v, log_alpha, log_beta):
+    _check(log_beta, "log_beta")
+    _shape(log_beta, tuple(v.shape), "log_beta")
+    if log_beta.dtype != log_alpha.dtype:
+        raise RuntimeError("log_beta must have log_alpha's dtype")
+    _same_device(q.device, [("log_beta", log_beta)])
+
+
+def chunk_fwd_beta(q, k, v, log_alpha, log_beta, chunk: int = 64, subchunk: int = 16, initial_state=None,
+                   output_final_state: bool = False, path: str = "auto", workspace=None):
+    """o [B,H,T,V] and final_state [B,H,K,V] fp32 (or None) with both gates.  gla_chunk_fwd_beta."""
+    _check(q, "q")
+    _check_problem(q, k, v, log_alpha, initial_state=initial_state)
+    _check_beta(q, v, log_alpha, log_beta)
+    B, H, T, K = q.shape
+    V = v.shape[-1]
+    d = desc(q, v, log_alpha, chunk, subchunk, path)
+    out = torch.empty((B, H, T, V), dtype=q.dtype, device=q.device)
+    fs = torch.empty((B, H, K, V), dtype=torch.float32, device=q.device) if output_final_state else None
+    if workspace is None:
+        workspace = beta_workspace(q, v, log_alpha, chunk, subchunk, path)
+    with torch.cuda.device(q.device):
+        _call(lib().gla_chunk_fwd_beta, "gla_chunk_fwd_beta", ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v),
+              _ptr(log_alpha), _ptr(log_beta), _ptr(initial_state), _ptr(out), _ptr(fs), _ptr(workspace),
+              workspace.numel(), _stream(q.device))
+    return out, fs
+
+
+def chunk_bwd_beta(q, k, v, log_alpha, log_beta, d_out, chunk: int = 64, subchunk: int = 16, initial_state=None,
+                   d_final_state=None, need_d_initial_state: bool = False, path: str = "auto", workspace=None):
+    """(dq, dk, dv, d_log_alpha fp32, d_log_beta fp32, d_initial_state fp32 or None).  gla_chunk_bwd_beta."""
+    _check(q, "q")
+    _check_problem(q, k, v, log_alpha, d_out, initial_state, d_final_state)
+    _check_beta(q, v, log_alpha, log_beta)
+    B, H, T, K = q.shape
+    d = desc(q, v, log_alpha, chunk, subchunk, path)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    dg = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+    dgb = torch.empty(v.shape, dtype=torch.float32, device=q.device)
+    dh0 = torch.empty((B, H, K, v.shape[-1]), dtype=torch.float32, device=q.device) if need_d_initial_state else None
+    if workspace is None:
+        workspace = beta_workspace(q, v, log_alpha, chunk, subchunk, path)
+    with torch.cuda.device(q.device):
+        _call(lib().gla_chunk_bwd_beta, "gla_chunk_bwd_beta", ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v),
+              _ptr(log_alpha), _ptr(log_beta), _ptr(initial_state), _ptr(d_out), _ptr(d_final_state), _ptr(dq),
+              _ptr(dk), _ptr(dv), _ptr(dg), _ptr(dgb), _ptr(dh0), _ptr(workspace), workspace.numel(),
+              _stream(q.device))
+    return dq, dk, dv, dg, dgb, dh0
+
+
+def recurrent_step_beta(q_t, k_t, v_t, log_alpha_t, log_beta_t, state):
+    """One decode step with both gates; ``state`` [B,H,K,V] fp32 updated in place; returns o_t [B,H,V]."""
+    for t, n in ((q_t, "q_t"), (k_t, "k_t"), (v_t, "v_t"), (log_alpha_t, "log_alpha_t"), (log_beta_t, "log_beta_t"),
+                 (state, "state")):
+        _check(t, n)
+    B, H, K = q_t.shape
+    V = v_t.shape[-1]
+    _shape(k_t, (B, H, K), "k_t")
+    _shape(log_alpha_t, (B, H, K), "log_alpha_t")
+    _shape(v_t, (B, H, V), "v_t")
+    _shape(log_beta_t, (B, H, V), "log_beta_t")
+    _shape(state, (B, H, K, V), "state")
+    if state.dtype != torch.float32:
+        raise RuntimeError("state must be fp32")
+    out = torch.empty((B, H, V), dtype=q_t.dtype, device=q_t.device)
+    _same_device(q_t.device, [("k_t", k_t), ("v_t", v_t), ("log_alpha_t", log_alpha_t), ("log_beta_t", log_beta_t),
+                              ("state", state)])
+    with torch.cuda.device(q_t.device):
+        _call(lib().gla_recurrent_step_beta, "gla_recurrent_step_beta", B, H, K, V, _dt(q_t), _dt(log_alpha_t),
+              _ptr(q_t), _ptr(k_t), _ptr(v_t), _ptr(log_alpha_t), _ptr(log_beta_t), _ptr(state), _ptr(out),
+              _stream(q_t.device))
     return out

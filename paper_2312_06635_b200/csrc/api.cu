@@ -210,6 +210,83 @@ int gla_chunk_bwd(const gla_desc* d, const void* q, const void* k, const void* v
                                d_initial_state, workspace, workspace_bytes, nullptr, stream);
 }
 
+// ---- the general outer-product gate G_t = alpha_t^T beta_t: fp32 CUDA-core path (simt_beta.cu) ----
+size_t gla_beta_workspace_size(const gla_desc* d) {
+    if (check_desc(d)) return 0;
+    return gla::simt::beta_ws(d->B, d->H, d->T, d->K, d->V, d->chunk);
+}
+
+namespace {
+gla::BetaProblem make_beta(const gla_desc* d, const void* q, const void* k, const void* v, const void* la,
+                           const void* lb, const float* h0, void* ws) {
+    gla::BetaProblem p{};
+    p.B = d->B; p.H = d->H; p.T = d->T; p.K = d->K; p.V = d->V; p.C = d->chunk; p.c = d->subchunk;
+    p.qkv_dtype = d->qkv_dtype; p.gate_dtype = d->gate_dtype;
+    p.q = q; p.k = k; p.v = v; p.g = la; p.lb = lb; p.h0 = h0; p.ws = ws;
+    return p;
+}
+int check_beta(const gla_desc* d) {
+    int s = check_desc(d);
+    if (s) return s;
+    return d->path == GLA_PATH_TC ? GLA_ERR_UNSUPPORTED : GLA_OK;   // the value gate runs on the SIMT kernels
+}
+}  // namespace
+
+int gla_chunk_fwd_beta(const gla_desc* d, const void* q, const void* k, const void* v, const void* log_alpha,
+                       const void* log_beta, const float* initial_state, void* out, float* final_state,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+    int s = check_beta(d);
+    if (s) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((size_t)d->B * d->H == 0) return GLA_OK;
+    if (d->T == 0) {
+        s = check_ptrs({}, {initial_state, final_state});
+        return s ? s : copy_or_zero(final_state, initial_state, (size_t)d->B * d->H * d->K * d->V, st);
+    }
+    s = check_ptrs({q, k, v, log_alpha, log_beta, out, workspace}, {initial_state, final_state});
+    if (s) return s;
+    if (workspace_bytes < gla_beta_workspace_size(d)) return GLA_ERR_WORKSPACE;
+    gla::BetaProblem p = make_beta(d, q, k, v, log_alpha, log_beta, initial_state, workspace);
+    p.out = out; p.final_state = final_state;
+    return cuda_status(gla::simt::fwd_beta(p, st));
+}
+
+int gla_chunk_bwd_beta(const gla_desc* d, const void* q, const void* k, const void* v, const void* log_alpha,
+                       const void* log_beta, const float* initial_state, const void* d_out,
+                       const float* d_final_state, void* dq, void* dk, void* dv, float* d_log_alpha,
+                       float* d_log_beta, float* d_initial_state, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+    int s = check_beta(d);
+    if (s) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((size_t)d->B * d->H == 0) return GLA_OK;
+    if (d->T == 0) {
+        s = check_ptrs({}, {initial_state, d_final_state, d_initial_state});
+        return s ? s : copy_or_zero(d_initial_state, d_final_state, (size_t)d->B * d->H * d->K * d->V, st);
+    }
+    s = check_ptrs({q, k, v, log_alpha, log_beta, d_out, dq, dk, dv, d_log_alpha, d_log_beta, workspace},
+                   {initial_state, d_final_state, d_initial_state});
+    if (s) return s;
+    if (workspace_bytes < gla_beta_workspace_size(d)) return GLA_ERR_WORKSPACE;
+    gla::BetaBwdProblem p{};
+    p.f = make_beta(d, q, k, v, log_alpha, log_beta, initial_state, workspace);
+    p.dO = d_out; p.dfinal = d_final_state; p.dq = dq; p.dk = dk; p.dv = dv; p.dg = d_log_alpha;
+    p.dlb = d_log_beta; p.dh0 = d_initial_state;
+    return cuda_status(gla::simt::bwd_beta(p, st));
+}
+
+int gla_recurrent_step_beta(int B, int H, int K, int V, int dtype, int gate_dtype, const void* q_t,
+                            const void* k_t, const void* v_t, const void* log_alpha_t, const void* log_beta_t,
+                            float* state, void* out_t, void* stream) {
+    if (B < 0 || H < 0 || K <= 0 || V <= 0) return GLA_ERR_SHAPE;
+    if (!ok_dtype(dtype) || !ok_dtype(gate_dtype)) return GLA_ERR_DTYPE;
+    int s = check_ptrs({q_t, k_t, v_t, log_alpha_t, log_beta_t, state, out_t}, {});
+    if (s) return s;
+    if ((size_t)B * H == 0) return GLA_OK;
+    return cuda_status(gla::simt::step_beta(B * H, K, V, dtype, gate_dtype, q_t, k_t, v_t, log_alpha_t, log_beta_t,
+                                            state, out_t, (cudaStream_t)stream));
+}
+
 int gla_recurrent_step(int B, int H, int K, int V, int dtype, int gate_dtype, const void* q_t, const void* k_t,
                        const void* v_t, const void* log_alpha_t, float* state, void* out_t, void* stream) {
     if (B < 0 || H < 0 || K <= 0 || V <= 0 || K > 1024) return GLA_ERR_SHAPE;   // (K <= 1024: staged in smem)

@@ -141,7 +141,9 @@ __global__ void __launch_bounds__(NT) k_fwd_state(const TQ* __restrict__ q, cons
                                                   const float* __restrict__ Pws, const float* __restrict__ h0,
                                                   TQ* __restrict__ out, float* __restrict__ final_state,
                                                   float* __restrict__ log_decay, int T, int K, int V, int C,
-                                                  int mode) {
+                                                  int mode, const float* __restrict__ colD = nullptr) {
+    // colD (value-gate path, simt_beta.cu; NULL = 1): the state update is followed by a per-value-column decay
+    // colD[bh][chunk][v], i.e. H <- colD (.)_col (e^Gamma H + (K e^{Gamma-b})^T V).
     extern __shared__ float smem[];
     float* qe = smem;                          // [C][K]   q (.) e^{b}
     float* ke = qe + C * K;                    // [C][K]   k (.) e^{Gamma - b}
@@ -195,10 +197,11 @@ __global__ void __launch_bounds__(NT) k_fwd_state(const TQ* __restrict__ q, cons
         // H_{i+1} = e^{Gamma} (.) H_i + (K (.) e^{Gamma - b})^T V
         {
             const int j = tid % VT_FWD;
+            const float cd = (colD && v0 + j < V) ? colD[((size_t)bh * NC + i) * V + v0 + j] : 1.f;
             for (int m = tid / VT_FWD; m < K; m += NT / VT_FWD) {
                 float a = eG[m] * Hs[m * VT_FWD + j];
                 for (int s = 0; s < C; ++s) a += ke[s * K + m] * Vs[s * VT_FWD + j];
-                Hs[m * VT_FWD + j] = a;
+                Hs[m * VT_FWD + j] = colD ? a * cd : a;
             }
         }
     }
@@ -238,7 +241,8 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
                                                const TQ* __restrict__ dO, const float* __restrict__ h0,
                                                const float* __restrict__ dPws, TQ* __restrict__ dq,
                                                float* __restrict__ dq32, float* __restrict__ ST,
-                                               int T, int K, int V, int C, const int* __restrict__ run_if) {
+                                               int T, int K, int V, int C, const int* __restrict__ run_if,
+                                               const float* __restrict__ colD = nullptr) {
     if (run_if && *run_if == 0) return;
     extern __shared__ float smem[];
     float* Hs = smem;                          // [KT][V]
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
                 if (j >= cs) continue;
                 float a = eG[m] * Hs[m * V + c0 + j];
                 for (int s = 0; s < C; ++s) a += ke[s * KT_BWD + m] * sv[s * VS_BWD + j];
-                Hs[m * V + c0 + j] = a;
+                Hs[m * V + c0 + j] = colD ? a * colD[((size_t)bh * NC + i) * V + c0 + j] : a;
             }
         }
         __syncthreads();
@@ -336,7 +340,8 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
                                                const float* __restrict__ dPws, const float* __restrict__ dq32,
                                                const float* __restrict__ ST, TQ* __restrict__ dk,
                                                float* __restrict__ dg, float* __restrict__ dh0,
-                                               int T, int K, int V, int C, const int* __restrict__ run_if) {
+                                               int T, int K, int V, int C, const int* __restrict__ run_if,
+                                               const float* __restrict__ colD = nullptr) {
     if (run_if && *run_if == 0) return;
     extern __shared__ float smem[];
     float* dH = smem;                          // [KT][V]
@@ -367,6 +372,8 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
         const size_t rowK = ((size_t)bh * T + (size_t)i * C) * K;
         const size_t rowV = ((size_t)bh * T + (size_t)i * C) * V;
         __syncthreads();
+        if (colD)   // adjoint of the column decay that followed chunk i's update: dH_{i+1} <- colD_i (.)_col dH_{i+1}
+            for (int e = tid; e < KT_BWD * V; e += NT) dH[e] *= colD[((size_t)bh * NC + i) * V + e % V];
         if (tid < KT_BWD) {
             const int m = tid;
             const bool ok = m0 + m < K;
@@ -449,7 +456,8 @@ __global__ void __launch_bounds__(NT) k_bwd_dv(const TQ* __restrict__ q, const T
                                                const TG* __restrict__ g, const TQ* __restrict__ dO,
                                                const float* __restrict__ dfinal, const float* __restrict__ Pws,
                                                TQ* __restrict__ dv, float* __restrict__ dh0,
-                                               int T, int K, int V, int C, int mode, const int* __restrict__ run_if) {
+                                               int T, int K, int V, int C, int mode, const int* __restrict__ run_if,
+                                               const float* __restrict__ colD = nullptr) {
     if (run_if && *run_if == 0) return;
     extern __shared__ float smem[];
     float* qe = smem;                          // [C][K] q e^{b}
@@ -469,6 +477,9 @@ __global__ void __launch_bounds__(NT) k_bwd_dv(const TQ* __restrict__ q, const T
         const size_t rowK = ((size_t)bh * T + (size_t)i * C) * K;
         const size_t rowV = ((size_t)bh * T + (size_t)i * C) * V;
         __syncthreads();
+        if (colD)   // adjoint of the column decay after chunk i (see k_bwd_dk)
+            for (int e = tid; e < K * VT_FWD; e += NT)
+                if (v0 + e % VT_FWD < V) dH[e] *= colD[((size_t)bh * NC + i) * V + v0 + e % VT_FWD];
         for (int m = tid; m < K; m += NT) {
             float run = 0.f;
             for (int t = 0; t < C; ++t) {
@@ -607,7 +618,7 @@ static cudaError_t fwd_impl(const Problem& p, cudaStream_t st) {
         GLA_PROF("simt::k_fwd_state", st);
         k_fwd_state<TQ, TG><<<dim3(cdiv(p.V, VT_FWD), BH), NT, sm, st>>>(q, k, v, g, Pws, p.h0, (TQ*)p.out,
                                                                         p.final_state, p.log_decay, p.T, p.K,
-                                                                        p.V, p.C, p.mode);
+                                                                        p.V, p.C, p.mode, p.colD);
     }
     return cudaGetLastError();
 }
@@ -682,17 +693,18 @@ static cudaError_t bwd_impl(const BwdProblem& p, cudaStream_t st) {
     {
         GLA_PROF("simt::k_bwd_dq", st);
         k_bwd_dq<TQ, TG><<<dim3(cdiv(p.K, KT_BWD), BH), NT, smk, st>>>(q, k, v, g, dO, p.h0, dPws, (TQ*)p.dq, dq32,
-                                                                      ST, p.T, p.K, p.V, p.C, nullptr);
+                                                                      ST, p.T, p.K, p.V, p.C, nullptr, p.colD);
     }
     {
         GLA_PROF("simt::k_bwd_dk", st);
         k_bwd_dk<TQ, TG><<<dim3(cdiv(p.K, KT_BWD), BH), NT, smk, st>>>(q, k, v, g, dO, p.dfinal, dPws, dq32, ST,
-                                                                      (TQ*)p.dk, p.dg, p.dh0, p.T, p.K, p.V, p.C, nullptr);
+                                                                      (TQ*)p.dk, p.dg, p.dh0, p.T, p.K, p.V, p.C, nullptr,
+                                                                      p.colD);
     }
     {
         GLA_PROF("simt::k_bwd_dv", st);
         k_bwd_dv<TQ, TG><<<dim3(cdiv(p.V, VT_FWD), BH), NT, smv, st>>>(q, k, g, dO, p.dfinal, Pws, (TQ*)p.dv,
-                                                                      nullptr, p.T, p.K, p.V, p.C, 0, nullptr);
+                                                                      nullptr, p.T, p.K, p.V, p.C, 0, nullptr, p.colD);
     }
     return cudaGetLastError();
 }

@@ -122,8 +122,8 @@ k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         if (NC > 1) load_inputs(1);
     }
     tc_fence_before();
+    __syncthreads();
     if (NVH == 2) cluster_sync_all();        // the peer's barriers are initialised before any remote access
-    else __syncthreads();
     tc_fence_after();
     const uint32_t tX = tmem_base, tSB = tmem_base + Cfg::COL_SB, tAcc = tmem_base + Cfg::COL_ACC;
     const int lq = warp & 3;

@@ -1,6 +1,6 @@
 """Small-shape run of every kernel family under compute-sanitizer (memcheck / racecheck / synccheck):
 TC forward + saved backward (K-tiled dq / dk walks, dv walk, reduce), recomputing TC backward, SIMT forward +
-backward, TC segment summaries, decode step.  python tools/sanitize_small.py  (run under compute-sanitizer)."""
+backward, TC segment summaries, decode step, the two-gate (beta) path.  python tools/sanitize_small.py  (run under compute-sanitizer)."""
 import os
 import sys
 
@@ -30,5 +30,10 @@ G.chunk_bwd(p["q"], p["k"], p["v"], p["g"], p["do"], 32, 8, path="simt")
 st = torch.zeros(1, 2, 64, 128, device="cuda")
 G.recurrent_step(p["q"][:, :, 0].contiguous(), p["k"][:, :, 0].contiguous(), p["v"][:, :, 0].contiguous(),
                  p["g"][:, :, 0].contiguous(), st)
+lb = synth.gates("std", 1, 2, 128, 128, seed=5).cuda()
+G.chunk_fwd_beta(p["q"], p["k"], p["v"], p["g"], lb, 32, 8, None, True)
+G.chunk_bwd_beta(p["q"], p["k"], p["v"], p["g"], lb, p["do"], 32, 8)
+G.recurrent_step_beta(p["q"][:, :, 0].contiguous(), p["k"][:, :, 0].contiguous(), p["v"][:, :, 0].contiguous(),
+                      p["g"][:, :, 0].contiguous(), lb[:, :, 0].contiguous(), st)
 torch.cuda.synchronize()
 print("sanitize_small: done")
