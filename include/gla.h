@@ -47,7 +47,7 @@ extern "C" {
 typedef enum {
     GLA_OK = 0,
     GLA_ERR_SHAPE = 1,        /* B,H,T < 0 or K,V <= 0, or K,V above the supported maximum            */
-    GLA_ERR_PLAN = 2,         /* chunk does not divide T, subchunk does not divide chunk, or C/c unsupported ("split into non-overlapping chunks") */
+    GLA_ERR_PLAN = 2,         /* chunk does not divide T, subchunk does not divide chunk, or C/c unsupported (C > 128, or C > 64 beyond the SIMT tiles) ("split into non-overlapping chunks") */
     GLA_ERR_DTYPE = 3,        /* unknown dtype code                                                   */
     GLA_ERR_ALIGN = 4,        /* a pointer is not 16-byte aligned                                     */
     GLA_ERR_NULL = 5,         /* a required pointer is NULL                                           */
@@ -61,8 +61,10 @@ typedef enum { GLA_BF16 = 0, GLA_FP32 = 1 } gla_dtype;
 /* Which implementation runs.
  *   GLA_PATH_AUTO : tensor-core path (tcgen05/TMEM/TMA) when qkv_dtype == BF16 and the shape is supported,
  *                   otherwise the SIMT path.
- *   GLA_PATH_SIMT : fp32-arithmetic CUDA-core kernels (the "fp32 debug build": any C, c with c | C | T,
- *                   K <= 256, V <= 1024; parity 1e-5 vs the fp64 oracle with fp32 inputs).
+ *   GLA_PATH_SIMT : fp32-arithmetic CUDA-core kernels (the "fp32 debug build": any C <= 128, c with c | C | T,
+ *                   K <= 256, V <= 1024; parity 1e-5 vs the fp64 oracle with fp32 inputs).  C > 64 needs the
+ *                   kernels' per-CTA tiles to fit in shared memory (e.g. C = 128 with K, V <= 128), else
+ *                   GLA_ERR_PLAN.
  *   GLA_PATH_TC   : bf16 tensor-core kernels: qkv_dtype BF16, C = 64, c | 64 (ignored, see above),
  *                   K in {64,128,256}, V % 128 == 0.  The TC backward needs K in {128,256} and
  *                   V / 128 in {1,2,4,8}; other TC-forward shapes run the backward on the SIMT kernels. */

@@ -27,9 +27,11 @@ int check_desc(const gla_desc* d) {
     if (d->B < 0 || d->H < 0 || d->T < 0 || d->K <= 0 || d->V <= 0) return GLA_ERR_SHAPE;
     if (d->K > 256 || d->V > 1024) return GLA_ERR_SHAPE;
     if (!ok_dtype(d->qkv_dtype) || !ok_dtype(d->gate_dtype)) return GLA_ERR_DTYPE;
-    if (d->chunk <= 0 || d->subchunk <= 0 || d->chunk > 64) return GLA_ERR_PLAN;
+    if (d->chunk <= 0 || d->subchunk <= 0 || d->chunk > 128) return GLA_ERR_PLAN;
     if (d->T % d->chunk != 0 || d->chunk % d->subchunk != 0) return GLA_ERR_PLAN;
     if (d->path < GLA_PATH_AUTO || d->path > GLA_PATH_TC) return GLA_ERR_UNSUPPORTED;
+    // chunks above 64 exist only on the SIMT kernels, within their shared-memory tiles
+    if (d->chunk > 64 && (d->path == GLA_PATH_TC || !gla::simt::plan_ok(d->chunk, d->K, d->V))) return GLA_ERR_PLAN;
     return GLA_OK;
 }
 

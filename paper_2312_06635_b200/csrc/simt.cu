@@ -25,11 +25,11 @@ namespace gla {
 namespace simt {
 
 constexpr int NT = 256;      // threads per CTA
-constexpr int KS = 32;       // channel slice for the intra kernels
+constexpr int KS = 24;       // channel slice for the intra kernels (3 x [MAXC][KS+1] fp32 static smem < 48 KB)
 constexpr int VT_FWD = 32;   // V tile of k_fwd_state / k_bwd_dv
 constexpr int KT_BWD = 32;   // K tile of k_bwd_dq / k_bwd_dk
 constexpr int VS_BWD = 64;   // V slice staged per step in k_bwd_dq / k_bwd_dk
-constexpr int MAXC = 64;
+constexpr int MAXC = 128;    // largest chunk C (the f4 chunk-size sweep runs C = 8 .. 128)
 
 // ---------------------------------------------------------------------------------------------
 // P[t][s] (s <= t) for one chunk.  grid (T/C, BH).  P written to Pws[bh][chunk][C][C] (fp32).
@@ -748,6 +748,10 @@ cudaError_t combine(int BH, int K, int V, const float* Hin, const float* D, cons
         k_combine<<<blocks, 256, 0, st>>>(Hin, D, S, Hout, BH, K, V);
     }
     return cudaGetLastError();
+}
+
+bool plan_ok(int C, int K, int V) {
+    return C >= 1 && C <= MAXC && fwd_state_smem(C, K) <= 232448 && bwd_k_smem(C, V) <= 232448;
 }
 
 size_t fwd_ws(int B, int H, int T, int K, int V, int C) { return sizeof(float) * (size_t)B * H * T * C; }

@@ -60,6 +60,8 @@ cudaError_t step(int BH, int K, int V, int qkv_dtype, int gate_dtype, const void
 cudaError_t combine(int BH, int K, int V, const float* Hin, const float* D, const float* S, float* Hout,
                     cudaStream_t st);
 size_t fwd_ws(int B, int H, int T, int K, int V, int C);
+// chunk plan the SIMT kernels can run: C <= 128 and their shared-memory tiles fit (227 KB per CTA)
+bool plan_ok(int C, int K, int V);
 size_t bwd_ws(int B, int H, int T, int K, int V, int C);
 }  // namespace simt
 }  // namespace gla

@@ -54,7 +54,8 @@ def fwd(L, d, q=FAKE, out=FAKE, ws=FAKE, wsb=1 << 40):
 
 
 @pytest.mark.parametrize("kw,code", [
-    (dict(T=100), 2), (dict(subchunk=5), 2), (dict(chunk=128, T=256), 2), (dict(chunk=0), 2),
+    (dict(T=100), 2), (dict(subchunk=5), 2), (dict(chunk=256, T=256), 2), (dict(chunk=128, T=256, path=2), 2),
+    (dict(chunk=128, T=256, K=256, V=512), 2), (dict(chunk=0), 2),
     (dict(K=0), 1), (dict(V=-1), 1), (dict(K=512), 1), (dict(B=-1), 1),
     (dict(qkv_dtype=7), 3), (dict(gate_dtype=-1), 3), (dict(path=9), 6),
 ])

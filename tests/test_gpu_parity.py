@@ -197,3 +197,11 @@ def test_autograd_wrapper():
     (o * p["do"]).sum().backward()
     dq, dk, dv, dg, _ = G.chunk_bwd(p["q"], p["k"], p["v"], p["g"], p["do"], 16, 4, path="simt")
     assert torch.equal(q.grad, dq) and torch.equal(g.grad, dg)
+
+
+# ---- chunk sizes beyond the tensor-core path's 64 (the f4 sweep's plans), fp32 SIMT ------------------------
+@pytest.mark.parametrize("C,c", [(128, 16), (128, 128), (128, 32), (8, 2)])
+def test_simt_large_and_small_chunks(C, c):
+    p = problem(1, 2, 256, 64, 128, seed=4, dtype=torch.float32, h0=True, dfinal=True)
+    check_fwd(p, C, c, "simt", F32_TOL)
+    check_bwd(p, C, c, "simt", F32_TOL)
