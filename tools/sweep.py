@@ -62,8 +62,29 @@ for name, (B, H, T, K, V) in [("340M (configs[1])", (8, 4, 2048, 128, 256)), ("1
     del q, k, v, g, do, wf, wb, o, gr
     torch.cuda.empty_cache()
 
+print("\n## Guard cliff: the same 1.3B step with `mixed` gates (half the channels log alpha = -5: every chunk fails "
+      "the factorisation guard, DESIGN.md R9)\n")
+print("| gates | ms / step | M tokens/s |")
+print("|---|---|---|")
+for gate in ("std", "mixed"):
+    B, H, T, K, V = 16, 4, 2048, 256, 512
+    p = synth.problem(B, H, T, K, V, seed=1, gate=gate)
+    q, k, v, g, do = (p[n].cuda() for n in ("q", "k", "v", "g", "do"))
+    wf, wb = G.fwd_workspace(q, v, g), G.bwd_workspace(q, v, g)
+    o = torch.empty(B, H, T, V, dtype=q.dtype, device="cuda")
+    gr = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), torch.empty(q.shape, device="cuda"), None)
+
+    def step():
+        G.chunk_fwd(q, k, v, g, out=o, workspace=wf)
+        G.chunk_bwd(q, k, v, g, do, grads=gr, workspace=wb, fwd_workspace=wf)
+    ms = timeit(step, n=3, warm=1)
+    print(f"| {gate} | {ms:.3f} | {B * T / ms / 1e3:.1f} |")
+    del q, k, v, g, do, wf, wb, o, gr
+    torch.cuda.empty_cache()
+
 print("\n## Decode: gla_recurrent_step (fp32 state read + written once per step), H = 4, K = 256, V = 512; "
-      "20 steps per CUDA graph replay\n")
+      "20 steps per CUDA graph replay, each step on a different state buffer of a >= 512 MB pool (so every "
+      "step's state comes from HBM, not from the 126 MB L2)\n")
 print("| B | us / step | M head-steps/s | state GB/s | % of HBM copy peak |")
 print("|---|---|---|---|---|")
 for B in (1, 16, 64, 256):
@@ -72,19 +93,28 @@ for B in (1, 16, 64, 256):
     kt = torch.randn(B, H, K, device="cuda").bfloat16()
     vt = torch.randn(B, H, V, device="cuda").bfloat16()
     gt = torch.nn.functional.logsigmoid(torch.randn(B, H, K, device="cuda")) / 16
-    st = torch.zeros(B, H, K, V, device="cuda")
+    nst = max(20, -(-512 * 2**20 // (B * H * K * V * 4)))
+    sts = [torch.zeros(B, H, K, V, device="cuda") for _ in range(nst)]
     out = torch.empty(B, H, V, device="cuda", dtype=torch.bfloat16)
     # 20 steps captured in a CUDA graph and replayed: device time per step without host launch overhead
     s_ = torch.cuda.Stream()
     s_.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s_):
-        for _ in range(3):
-            G.recurrent_step(qt, kt, vt, gt, st, out)
+        for i in range(3):
+            G.recurrent_step(qt, kt, vt, gt, sts[i], out)
     torch.cuda.current_stream().wait_stream(s_)
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
-        for _ in range(20):
-            G.recurrent_step(qt, kt, vt, gt, st, out)
-    ms = timeit(graph.replay, n=20, warm=3) / 20
+    graphs = []
+    for r in range(nst // 20):
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for i in range(20):
+                G.recurrent_step(qt, kt, vt, gt, sts[20 * r + i], out)
+        graphs.append(graph)
+    it = [0]
+
+    def replay():
+        graphs[it[0] % len(graphs)].replay()
+        it[0] += 1
+    ms = timeit(replay, n=20, warm=3) / 20
     by = B * H * K * V * 8
     print(f"| {B} | {ms * 1e3:.1f} | {B * H / ms / 1e3:.2f} | {by / ms / 1e6:.0f} | {100 * by / ms / 1e6 / HBM:.1f} |")
