@@ -514,15 +514,20 @@ def report(args, cfg, W, world, ms_step, value, prof, launches, clk, e2e, chain,
         ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary_latest.json")))
     except Exception:
         pass
-    ncu_key = {"tc::fwd_prep": "k_fwd_prep<", "tc::fwd_state": "k_fwd_state<", "tc::bwd_dp": "k_bwd_dp",
-               "tc::bwd_prep": "k_bwd_prep<", "tc::bwd_dq": "k_bwd_dq", "tc::bwd_dkv": "k_bwd_dkv",
-               "tc::bwd_dk": "k_bwd_dk", "tc::bwd_dv": "k_bwd_dv", "tc::bwd_reduce": "k_bwd_reduce"}
+    # which kernel of the capture each traced name is (the K-tiled dq / dk walks are one template, REV = 0 / 1;
+    # the dv walk is k_bwd_dkv3<K, 2>)
+    ncu_keys = {"tc::fwd_prep": [f"k_fwd_prep<{K},"], "tc::fwd_state": [f"k_fwd_state<{K}>"],
+                "tc::bwd_dp": ["k_bwd_dp"], "tc::bwd_prep": [f"k_bwd_prep<{K},"],
+                "tc::bwd_dq": [f"k_bwd_kwalk<{K}, 0,", f"k_bwd_kwalk<{K}, false", f"k_bwd_dq3<{K}>"],
+                "tc::bwd_dk": [f"k_bwd_kwalk<{K}, 1,", f"k_bwd_kwalk<{K}, true"],
+                "tc::bwd_dv": [f"k_bwd_dkv3<{K}, 2>"], "tc::bwd_dkv": [f"k_bwd_dkv3<{K}, 1>"],
+                "tc::bwd_reduce": [f"k_bwd_reduce_tma<{K},"]}
 
     def traffic_of(name):
-        key = ncu_key.get(name)
-        for n, v in ncu.items():
-            if key and key in n.split("::")[-1] and (f"<{K}," in n or f"<{K}>" in n or n.endswith(key)):
-                return v.get("traffic_bytes")
+        for key in ncu_keys.get(name, []):
+            for n, v in ncu.items():
+                if key in n:
+                    return v.get("traffic_bytes")
         return None
 
     kernels = {}
