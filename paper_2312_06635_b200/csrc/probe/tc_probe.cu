@@ -101,6 +101,67 @@ __global__ void __launch_bounds__(128) k_probe(const __nv_bfloat16* __restrict__
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// D[128 x N] = A[128 x K] . B[K x N] in tf32: A (fp32) staged into TMEM one element per column, B (fp32) as a
+// K-major SW128 tile (N rows of 32 fp32 per K block of 32).
+__global__ void __launch_bounds__(128) k_probe_tf32(const float* __restrict__ A, const float* __restrict__ B,
+                                                    float* __restrict__ D, int N, int K) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sB = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t bar_mma;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    if (warp == 0) tmem_alloc(&tbase, 512);
+    if (tid == 0) {
+        mbar_init(&bar_mma, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    tc_fence_after();
+    for (int e = tid; e < N * K; e += 128) {
+        const int k = e / N, n = e % N;
+        const uint32_t off = (k / 32) * (N * 128) + sw128_off(n, 2 * (k % 32));
+        *reinterpret_cast<float*>(sB + off) = B[(size_t)k * N + n];
+    }
+    const uint32_t tA = tbase + 256;
+    for (int c0 = 0; c0 < K; c0 += 32) {
+        uint32_t r[32];
+        const int m = 32 * warp + lane;
+        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(A[(size_t)m * K + c0 + j]);
+        tmem_st32(taddr(tA, 32 * warp, c0), r);
+    }
+    tmem_wait_st();
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+        const uint32_t id = idesc_tf32(128, N, 0);
+        for (int kk = 0; kk < K / 8; ++kk)
+            mma_tf32_ta(tbase, tA + kk * 8, sdesc_sw128(smem_u32(sB) + (kk / 4) * (N * 128) + (kk % 4) * 32, 16, 1024),
+                        id, kk > 0);
+        mma_commit(&bar_mma);
+    }
+    mbar_wait(&bar_mma, 0);
+    tc_fence_after();
+    for (int c0 = 0; c0 < N; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(taddr(tbase, 32 * warp, c0), r);
+        tmem_wait_ld();
+        for (int j = 0; j < 32; ++j) D[(size_t)(32 * warp + lane) * N + c0 + j] = __uint_as_float(r[j]);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tbase, 512);
+}
+
+extern "C" int probe_gemm_tf32(const float* A, const float* B, float* D, int N, int K) {
+    const int smem = 131072 + 1024;
+    cudaFuncSetAttribute(k_probe_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_probe_tf32<<<1, 128, smem>>>(A, B, D, N, K);
+    cudaError_t e = cudaDeviceSynchronize();
+    return e == cudaSuccess ? 0 : 1000 + (int)e;
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);

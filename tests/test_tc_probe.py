@@ -45,3 +45,19 @@ def test_probe_gemm_a_in_tmem(probe, N, K, b_mn):
     ref = A.float() @ B.float()
     err = (D - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-5, err
+
+
+@pytest.mark.parametrize("N,K", [(64, 256), (64, 128), (128, 64)])
+def test_probe_tf32_a_in_tmem(N, K):
+    """kind::tf32 with the fp32 A operand read from TMEM and a K-major SW128 fp32 B tile (the anchored-frame
+    walks' output MMA): equals an fp32 matmul of tf32-truncated operands."""
+    L = ctypes.CDLL(LIB)
+    L.probe_gemm_tf32.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 2
+    torch.manual_seed(2)
+    A = torch.randn(128, K, device="cuda")
+    B = torch.randn(K, N, device="cuda")
+    D = torch.full((128, N), float("nan"), device="cuda")
+    assert L.probe_gemm_tf32(A.data_ptr(), B.data_ptr(), D.data_ptr(), N, K) == 0
+    ref = A.double() @ B.double()
+    err = (D.double() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 2e-3, err
