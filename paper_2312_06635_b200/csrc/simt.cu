@@ -553,16 +553,36 @@ __global__ void __launch_bounds__(CQ * RG) k_step(const TQ* __restrict__ q, cons
     for (int u = 0; u < 4; ++u) vv[u] = (col + u < V) ? to_f(v[(size_t)bh * V + col + u]) : 0.f;
     const bool vec = col + 3 < V && (V % 4) == 0;
     __syncthreads();
+    if (vec) {
+        // NB rows per batch: all loads first, then the updates and stores (the rows of one thread never alias, but
+        // the compiler cannot know that: without the batching every load waited for the previous row's store)
+        constexpr int NB = 8;
+        float* base = state + (size_t)bh * K * V + col;
+        for (int m0 = rg; m0 < K; m0 += RG * NB) {
+            float4 s4[NB];
+#pragma unroll
+            for (int u = 0; u < NB; ++u) {
+                const int m = m0 + u * RG;
+                if (m < K) s4[u] = *reinterpret_cast<const float4*>(base + (size_t)m * V);
+            }
+#pragma unroll
+            for (int u = 0; u < NB; ++u) {
+                const int m = m0 + u * RG;
+                if (m < K) {
+                    const float a = sa[m], km = sk[m], qm = sq[m];
+                    float4 x = s4[u];
+                    x.x = a * x.x + km * vv[0]; x.y = a * x.y + km * vv[1];
+                    x.z = a * x.z + km * vv[2]; x.w = a * x.w + km * vv[3];
+                    *reinterpret_cast<float4*>(base + (size_t)m * V) = x;
+                    o[0] += qm * x.x; o[1] += qm * x.y; o[2] += qm * x.z; o[3] += qm * x.w;
+                }
+            }
+        }
+    } else
     for (int m = rg; m < K; m += RG) {
         const float a = sa[m], km = sk[m], qm = sq[m];
         float* row = state + ((size_t)bh * K + m) * V;
-        if (vec) {
-            float4 s4 = *reinterpret_cast<float4*>(row + col);
-            s4.x = a * s4.x + km * vv[0]; s4.y = a * s4.y + km * vv[1];
-            s4.z = a * s4.z + km * vv[2]; s4.w = a * s4.w + km * vv[3];
-            *reinterpret_cast<float4*>(row + col) = s4;
-            o[0] += qm * s4.x; o[1] += qm * s4.y; o[2] += qm * s4.z; o[3] += qm * s4.w;
-        } else {
+        {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if (col + u < V) {
