@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(NT) k_fwd_state(const TQ* __restrict__ q, cons
 // Backward, K-tiled kernels.  smem: H or dH [KT][V], qe/ke/b for the K-tile [C][KT] x3,
 // dP [C][C], staged dO / V slices [C][VS].
 __host__ __device__ inline size_t bwd_k_smem(int C, int V) {
-    return sizeof(float) * ((size_t)KT_BWD * V + (size_t)4 * C * KT_BWD + (size_t)C * C +
+    return sizeof(float) * ((size_t)KT_BWD * (V + 1) + (size_t)4 * C * KT_BWD + (size_t)C * C +
                             (size_t)2 * C * VS_BWD + KT_BWD);
 }
 
@@ -245,8 +245,9 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
                                                const float* __restrict__ colD = nullptr) {
     if (run_if && *run_if == 0) return;
     extern __shared__ float smem[];
-    float* Hs = smem;                          // [KT][V]
-    float* sb = Hs + KT_BWD * V;               // [C][KT] b
+    const int HV = V + 1;                      // padded row stride: the inter loops read a column per warp
+    float* Hs = smem;                          // [KT][V + 1]
+    float* sb = Hs + KT_BWD * HV;              // [C][KT] b
     float* sk = sb + C * KT_BWD;               // [C][KT] k
     float* ke = sk + C * KT_BWD;               // [C][KT] k e^{Gamma-b}
     float* acc = ke + C * KT_BWD;              // [C][KT] dq accumulator
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
     const int NC = T / C;
     for (int e = tid; e < KT_BWD * V; e += NT) {
         const int m = e / V, j = e % V;
-        Hs[e] = (h0 && m0 + m < K) ? h0[((size_t)bh * K + m0 + m) * V + j] : 0.f;
+        Hs[m * HV + j] = (h0 && m0 + m < K) ? h0[((size_t)bh * K + m0 + m) * V + j] : 0.f;
     }
     for (int i = 0; i < NC; ++i) {
         const size_t rowK = ((size_t)bh * T + (size_t)i * C) * K;
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
             for (int e = tid; e < C * KT_BWD; e += NT) {
                 const int t = e / KT_BWD, m = e % KT_BWD;
                 float a = 0.f;
-                for (int j = 0; j < cs; ++j) a += sd[t * VS_BWD + j] * Hs[m * V + c0 + j];
+                for (int j = 0; j < cs; ++j) a += sd[t * VS_BWD + j] * Hs[m * HV + c0 + j];
                 acc[e] += a * expf(sb[t * KT_BWD + m]);
             }
             __syncthreads();
@@ -310,9 +311,9 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
             for (int e = tid; e < KT_BWD * VS_BWD; e += NT) {
                 const int m = e / VS_BWD, j = e % VS_BWD;
                 if (j >= cs) continue;
-                float a = eG[m] * Hs[m * V + c0 + j];
+                float a = eG[m] * Hs[m * HV + c0 + j];
                 for (int s = 0; s < C; ++s) a += ke[s * KT_BWD + m] * sv[s * VS_BWD + j];
-                Hs[m * V + c0 + j] = colD ? a * colD[((size_t)bh * NC + i) * V + c0 + j] : a;
+                Hs[m * HV + c0 + j] = colD ? a * colD[((size_t)bh * NC + i) * V + c0 + j] : a;
             }
         }
         __syncthreads();
@@ -327,7 +328,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
     __syncthreads();
     for (int e = tid; e < KT_BWD * V; e += NT) {
         const int m = e / V, j = e % V;
-        if (m0 + m < K) ST[((size_t)bh * K + m0 + m) * V + j] = Hs[e];
+        if (m0 + m < K) ST[((size_t)bh * K + m0 + m) * V + j] = Hs[m * HV + j];
     }
 }
 
@@ -344,8 +345,9 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
                                                const float* __restrict__ colD = nullptr) {
     if (run_if && *run_if == 0) return;
     extern __shared__ float smem[];
-    float* dH = smem;                          // [KT][V]
-    float* sb = dH + KT_BWD * V;               // [C][KT] b
+    const int HV = V + 1;                      // padded row stride (see k_bwd_dq)
+    float* dH = smem;                          // [KT][V + 1]
+    float* sb = dH + KT_BWD * HV;              // [C][KT] b
     float* sq = sb + C * KT_BWD;               // [C][KT] q
     float* qe = sq + C * KT_BWD;               // [C][KT] q e^{b}
     float* acc = qe + C * KT_BWD;              // [C][KT] dk accumulator
@@ -358,14 +360,14 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
     const int NC = T / C;
     for (int e = tid; e < KT_BWD * V; e += NT) {
         const int m = e / V, j = e % V;
-        dH[e] = (dfinal && m0 + m < K) ? dfinal[((size_t)bh * K + m0 + m) * V + j] : 0.f;
+        dH[m * HV + j] = (dfinal && m0 + m < K) ? dfinal[((size_t)bh * K + m0 + m) * V + j] : 0.f;
     }
     __syncthreads();
     // carry init: rowsum(S_T (.) dS_T) -- the final-state term of d log alpha (R6)
     if (tid < KT_BWD) {
         float a = 0.f;
         if (m0 + tid < K)
-            for (int j = 0; j < V; ++j) a += ST[((size_t)bh * K + m0 + tid) * V + j] * dH[tid * V + j];
+            for (int j = 0; j < V; ++j) a += ST[((size_t)bh * K + m0 + tid) * V + j] * dH[tid * HV + j];
         carry[tid] = a;
     }
     for (int i = NC - 1; i >= 0; --i) {
@@ -373,7 +375,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
         const size_t rowV = ((size_t)bh * T + (size_t)i * C) * V;
         __syncthreads();
         if (colD)   // adjoint of the column decay that followed chunk i's update: dH_{i+1} <- colD_i (.)_col dH_{i+1}
-            for (int e = tid; e < KT_BWD * V; e += NT) dH[e] *= colD[((size_t)bh * NC + i) * V + e % V];
+            for (int e = tid; e < KT_BWD * V; e += NT) dH[(e / V) * HV + e % V] *= colD[((size_t)bh * NC + i) * V + e % V];
         if (tid < KT_BWD) {
             const int m = tid;
             const bool ok = m0 + m < K;
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
             for (int e = tid; e < C * KT_BWD; e += NT) {
                 const int s = e / KT_BWD, m = e % KT_BWD;
                 float a = 0.f;
-                for (int j = 0; j < cs; ++j) a += sv[s * VS_BWD + j] * dH[m * V + c0 + j];
+                for (int j = 0; j < cs; ++j) a += sv[s * VS_BWD + j] * dH[m * HV + c0 + j];
                 acc[e] += a * expf(sb[(C - 1) * KT_BWD + m] - sb[s * KT_BWD + m]);
             }
             __syncthreads();
@@ -418,9 +420,9 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
             for (int e = tid; e < KT_BWD * VS_BWD; e += NT) {
                 const int m = e / VS_BWD, j = e % VS_BWD;
                 if (j >= cs) continue;
-                float a = expf(sb[(C - 1) * KT_BWD + m]) * dH[m * V + c0 + j];
+                float a = expf(sb[(C - 1) * KT_BWD + m]) * dH[m * HV + c0 + j];
                 for (int t = 0; t < C; ++t) a += qe[t * KT_BWD + m] * sd[t * VS_BWD + j];
-                dH[m * V + c0 + j] = a;
+                dH[m * HV + c0 + j] = a;
             }
         }
         __syncthreads();
@@ -445,7 +447,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
     if (dh0)
         for (int e = tid; e < KT_BWD * V; e += NT) {
             const int m = e / V, j = e % V;
-            if (m0 + m < K) dh0[((size_t)bh * K + m0 + m) * V + j] = dH[e];
+            if (m0 + m < K) dh0[((size_t)bh * K + m0 + m) * V + j] = dH[m * HV + j];
         }
 }
 
