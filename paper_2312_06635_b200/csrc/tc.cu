@@ -32,10 +32,13 @@ int fwd_segments(int BH, int V, int NC) {
     int S = 1;
     if (force == 1) return S;
     if (force > 1) return (NC % force == 0 && NC / force >= 8) ? force : 1;
-    // The summary walks cost ~0.8 of a full walk, so splitting pays only when the unsplit walk would use at most
-    // a quarter of the SMs (measured: S = 2 at 64 CTAs was slower; S = 4 at 32 CTAs 1.5x faster end to end).
+    // The summaries cost a fixed share of a segment, so splitting pays when the unsplit walk would use at most a
+    // quarter of the SMs (S = 4 at 32 CTAs 1.5x faster end to end), or half of them with long segments (below).
     const int nvt = V / 128 > 0 ? V / 128 : 1, ctas = BH * nvt;
-    if ((long)ctas * 4 > num_sms()) return 1;
+    // Long walks that fill at most half of the SMs split in two (T = 8K at 1.3B: 1,040 vs 1,081 us per step); short
+    // ones do not (340M, 32 chunks: S = 2 at 304 vs 253 us): the summaries and the chain are a fixed cost per segment.
+    if ((long)ctas * 4 > num_sms())
+        return ((long)ctas * 2 <= num_sms() && NC % 2 == 0 && NC / 2 >= 32) ? 2 : 1;
     while ((long)ctas * 2 * S <= num_sms() && NC % (2 * S) == 0 && NC / (2 * S) >= 8) S *= 2;
     return S >= 4 ? S : 1;
 }

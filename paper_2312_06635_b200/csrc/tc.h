@@ -27,8 +27,9 @@ struct FwdSaved {
 };
 // Intra-GPU segment split of long sequences: the walks run over B*H*S virtual units of T/S
 // tokens each -- the same [B*H*T, D] rows, since unit (b,h) segment s starts at row (b*H + h)*T + s*T/S.
-// Used only when the unsplit walks fill at most a quarter of the SMs; S doubles while the split walks still fit
-// in one wave and every segment keeps >= 8 chunks (S >= 4, else 1).  GLA_SEGMENTS=1 disables it.
+// Used when the unsplit walks fill at most a quarter of the SMs (S doubles while the split walks still fit in one
+// wave and every segment keeps >= 8 chunks; S >= 4, else 1), or at most half of them with segments of >= 32
+// chunks (S = 2).  GLA_SEGMENTS=1 disables it.
 int fwd_segments(int BH, int V, int NC);
 // Sequential state chains over the segments of every (b,h): forward H_{s+1} = e^{D_s} H_s + S_loc_s
 // (writes H_s for every s; H_0 = h0 or 0), backward dF_{s-1} = e^{D_s} dF_s + dh_loc_s (dF_{S-1} = dfinal or 0).
