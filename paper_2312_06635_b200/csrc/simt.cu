@@ -70,12 +70,12 @@ __global__ void __launch_bounds__(NT) k_intra_P(const TQ* __restrict__ q, const 
             const int x = t / c, y = s / c;
             float a = 0.f;
             if (x == y) {                         // diagonal sub-chunk: exponent b_t - b_s <= 0
-                for (int m = 0; m < ms; ++m) a += sq[t][m] * sk[s][m] * expf(sb[t][m] - sb[s][m]);
+                for (int m = 0; m < ms; ++m) a += sq[t][m] * sk[s][m] * fexp(sb[t][m] - sb[s][m]);
             } else {                              // off-diagonal pair: normaliser e_y = b[(y+1)c - 1]
                 const int ey = (y + 1) * c - 1;
                 for (int m = 0; m < ms; ++m) {
                     const float e = sb[ey][m];
-                    a += (sq[t][m] * expf(sb[t][m] - e)) * (sk[s][m] * expf(e - sb[s][m]));
+                    a += (sq[t][m] * fexp(sb[t][m] - e)) * (sk[s][m] * fexp(e - sb[s][m]));
                 }
             }
             acc[j] += a;
@@ -126,6 +126,39 @@ __global__ void __launch_bounds__(NT) k_intra_dP(const TQ* __restrict__ dO, cons
     }
 }
 
+// Register-tiled loops of the V-tiled kernels (k_fwd_state, k_bwd_dv) for C = 64, K % 32 == 0: lane = value column
+// j of the 32-wide tile; float4 loads along the channels (broadcast within a warp).  Fixed summation order.
+//   rows:   a[r] = sum_m X[t][m] S[m][j]  for the 8 tokens t = warp + 8 r           (X [C][K], S [K][32])
+//   update: S[m][j] = eS[m] S[m][j] + sum_s A[s][m] Y[s][j]  for the channels m = 4 (warp + 8 r) + u
+__device__ __forceinline__ void rows_tile64(float (&a)[8], const float* X, const float* S, int K) {
+    const int j = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int m = 0; m < K; m += 4) {
+        const float s0 = S[m * VT_FWD + j], s1 = S[(m + 1) * VT_FWD + j], s2 = S[(m + 2) * VT_FWD + j],
+                    s3 = S[(m + 3) * VT_FWD + j];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const float4 x = *reinterpret_cast<const float4*>(X + (w + 8 * r) * K + m);
+            a[r] += x.x * s0 + x.y * s1 + x.z * s2 + x.w * s3;
+        }
+    }
+}
+__device__ __forceinline__ void update_vtile64(float* S, const float* eS, const float* A, const float* Y, int K, int C,
+                                               float cd, bool has_cd) {
+    const int j = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int m0 = 4 * w; m0 < K; m0 += 32) {   // 4 consecutive channels per pass
+        float u[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) u[q] = eS[m0 + q] * S[(m0 + q) * VT_FWD + j];
+        for (int s = 0; s < C; ++s) {
+            const float y = Y[s * VT_FWD + j];
+            const float4 a4 = *reinterpret_cast<const float4*>(A + s * K + m0);
+            u[0] += a4.x * y; u[1] += a4.y * y; u[2] += a4.z * y; u[3] += a4.w * y;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) S[(m0 + q) * VT_FWD + j] = has_cd ? u[q] * cd : u[q];
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Shared-memory carve-up for the (bh, V-tile) kernels: qe,ke [C][K], H [K][VT], P [C][C], V [C][VT],
 // expG [K].
@@ -154,6 +187,7 @@ __global__ void __launch_bounds__(NT) k_fwd_state(const TQ* __restrict__ q, cons
     const int vt = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
     const int v0 = vt * VT_FWD;
     const int NC = T / C;
+    const bool tiled = C == 64 && K % 32 == 0;
     for (int e = tid; e < K * VT_FWD; e += NT) {
         const int m = e / VT_FWD, j = e % VT_FWD;
         Hs[e] = (h0 && v0 + j < V) ? h0[((size_t)bh * K + m) * V + v0 + j] : 0.f;
@@ -163,16 +197,18 @@ __global__ void __launch_bounds__(NT) k_fwd_state(const TQ* __restrict__ q, cons
         const size_t rowV = ((size_t)bh * T + (size_t)i * C) * V;
         __syncthreads();
         // (a1) chunk-local inclusive cumsum b, one channel per thread; build qe, ke.
-        for (int m = tid; m < K; m += NT) {
+        for (int m = tid; m < K; m += NT) {   // (unrolled: batches of independent loads, not one per token)
             float run = 0.f;
+#pragma unroll 8
             for (int t = 0; t < C; ++t) {
                 run += to_f(g[rowK + (size_t)t * K + m]);
                 ke[t * K + m] = run;                                   // b_t (temporarily)
-                if (mode == 0) qe[t * K + m] = to_f(q[rowK + (size_t)t * K + m]) * expf(run);
+                if (mode == 0) qe[t * K + m] = to_f(q[rowK + (size_t)t * K + m]) * fexp(run);
             }
+#pragma unroll 8
             for (int t = 0; t < C; ++t)
-                ke[t * K + m] = to_f(k[rowK + (size_t)t * K + m]) * expf(run - ke[t * K + m]);
-            eG[m] = expf(run);
+                ke[t * K + m] = to_f(k[rowK + (size_t)t * K + m]) * fexp(run - ke[t * K + m]);
+            eG[m] = fexp(run);
         }
         for (int e = tid; e < C * VT_FWD; e += NT) {
             const int t = e / VT_FWD, j = e % VT_FWD;
@@ -186,11 +222,26 @@ __global__ void __launch_bounds__(NT) k_fwd_state(const TQ* __restrict__ q, cons
         if (mode == 0) {
             // o_t = (q_t (.) e^{b_t}) H_i + sum_s P_ts v_s
             const int j = tid % VT_FWD;
-            for (int t = tid / VT_FWD; t < C; t += NT / VT_FWD) {
-                float a = 0.f;
-                for (int m = 0; m < K; ++m) a += qe[t * K + m] * Hs[m * VT_FWD + j];
-                for (int s = 0; s <= t; ++s) a += Ps[t * C + s] * Vs[s * VT_FWD + j];
-                if (v0 + j < V) out[rowV + (size_t)t * V + v0 + j] = from_f<TQ>(a);
+            if (tiled) {
+                float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                rows_tile64(a, qe, Hs, K);
+                const int w = tid / VT_FWD;
+                for (int s = 0; s < C; ++s) {
+                    const float vs = Vs[s * VT_FWD + j];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+                        if (s <= w + 8 * r) a[r] += Ps[(w + 8 * r) * C + s] * vs;
+                }
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    if (v0 + j < V) out[rowV + (size_t)(w + 8 * r) * V + v0 + j] = from_f<TQ>(a[r]);
+            } else {
+                for (int t = tid / VT_FWD; t < C; t += NT / VT_FWD) {
+                    float a = 0.f;
+                    for (int m = 0; m < K; ++m) a += qe[t * K + m] * Hs[m * VT_FWD + j];
+                    for (int s = 0; s <= t; ++s) a += Ps[t * C + s] * Vs[s * VT_FWD + j];
+                    if (v0 + j < V) out[rowV + (size_t)t * V + v0 + j] = from_f<TQ>(a);
+                }
             }
             __syncthreads();
         }
@@ -198,10 +249,14 @@ __global__ void __launch_bounds__(NT) k_fwd_state(const TQ* __restrict__ q, cons
         {
             const int j = tid % VT_FWD;
             const float cd = (colD && v0 + j < V) ? colD[((size_t)bh * NC + i) * V + v0 + j] : 1.f;
-            for (int m = tid / VT_FWD; m < K; m += NT / VT_FWD) {
-                float a = eG[m] * Hs[m * VT_FWD + j];
-                for (int s = 0; s < C; ++s) a += ke[s * K + m] * Vs[s * VT_FWD + j];
-                Hs[m * VT_FWD + j] = colD ? a * cd : a;
+            if (tiled) {
+                update_vtile64(Hs, eG, ke, Vs, K, C, cd, colD != nullptr);
+            } else {
+                for (int m = tid / VT_FWD; m < K; m += NT / VT_FWD) {
+                    float a = eG[m] * Hs[m * VT_FWD + j];
+                    for (int s = 0; s < C; ++s) a += ke[s * K + m] * Vs[s * VT_FWD + j];
+                    Hs[m * VT_FWD + j] = colD ? a * cd : a;
+                }
             }
         }
     }
@@ -230,8 +285,52 @@ __global__ void __launch_bounds__(NT) k_fwd_state(const TQ* __restrict__ q, cons
 // Backward, K-tiled kernels.  smem: H or dH [KT][V], qe/ke/b for the K-tile [C][KT] x3,
 // dP [C][C], staged dO / V slices [C][VS].
 __host__ __device__ inline size_t bwd_k_smem(int C, int V) {
-    return sizeof(float) * ((size_t)KT_BWD * (V + 1) + (size_t)4 * C * KT_BWD + (size_t)C * C +
+    return sizeof(float) * ((size_t)KT_BWD * (V + 4) + (size_t)4 * C * KT_BWD + (size_t)C * C +
                             (size_t)2 * C * VS_BWD + KT_BWD);
+}
+
+// Register-tiled inner loops of the K-tiled backward kernels for the common plan C = 64 with V % 4 == 0 (the exact
+// fallback of the tensor-core path always has C = 64): lane = channel m of the tile, the 8 warps split the tokens
+// (inter) or the values (state update); float4 loads along the values.  Same sums as the scalar loops, in a
+// different (still fixed) order.
+//   inter:  acc[t][m] += scale(t, m) * sum_{j < cs} X[t][j] S[m][c0 + j]      (8 tokens t = warp + 8 r per thread)
+//   update: S[m][c0 + j] = eS * S[m][c0 + j] + sum_s A[s][m] Y[s][j]          (8 values j = 8 warp + u per thread)
+template <typename ScaleF>
+__device__ __forceinline__ void inter_tile64(float* acc, const float* X, const float* S, int HV, int c0, int cs,
+                                             ScaleF scale) {
+    const int m = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const float* srow = S + m * HV + c0;
+    for (int j = 0; j < cs; j += 4) {
+        const float4 h = *reinterpret_cast<const float4*>(srow + j);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const float4 x = *reinterpret_cast<const float4*>(X + (w + 8 * r) * VS_BWD + j);
+            a[r] += x.x * h.x + x.y * h.y + x.z * h.z + x.w * h.w;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const int t = w + 8 * r;
+        acc[t * KT_BWD + m] += a[r] * scale(t, m);
+    }
+}
+__device__ __forceinline__ void update_tile64(float* S, const float* A, const float* Y, int HV, int c0, int cs, float eS,
+                                              int C) {
+    const int m = threadIdx.x & 31, j0 = 8 * (threadIdx.x >> 5);
+    if (j0 >= cs) return;
+    float* srow = S + m * HV + c0 + j0;
+    float4 u0 = *reinterpret_cast<float4*>(srow), u1 = *reinterpret_cast<float4*>(srow + 4);
+    u0.x *= eS; u0.y *= eS; u0.z *= eS; u0.w *= eS; u1.x *= eS; u1.y *= eS; u1.z *= eS; u1.w *= eS;
+    for (int s = 0; s < C; ++s) {
+        const float am = A[s * KT_BWD + m];
+        const float4 y0 = *reinterpret_cast<const float4*>(Y + s * VS_BWD + j0);
+        const float4 y1 = *reinterpret_cast<const float4*>(Y + s * VS_BWD + j0 + 4);
+        u0.x += am * y0.x; u0.y += am * y0.y; u0.z += am * y0.z; u0.w += am * y0.w;
+        u1.x += am * y1.x; u1.y += am * y1.y; u1.z += am * y1.z; u1.w += am * y1.w;
+    }
+    *reinterpret_cast<float4*>(srow) = u0;
+    *reinterpret_cast<float4*>(srow + 4) = u1;
 }
 
 // grid (K/KT, BH).  Forward walk: dq_t = e^{b_t} (.) (dO_t H_i^T) + sum_{s<=t} dP_ts k_s e^{b_t - b_s}.
@@ -245,7 +344,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
                                                const float* __restrict__ colD = nullptr) {
     if (run_if && *run_if == 0) return;
     extern __shared__ float smem[];
-    const int HV = V + 1;                      // padded row stride: the inter loops read a column per warp
+    const int HV = V + 4;                      // padded row stride (16-B rows; lanes = channels hit distinct banks)
     float* Hs = smem;                          // [KT][V + 1]
     float* sb = Hs + KT_BWD * HV;              // [C][KT] b
     float* sk = sb + C * KT_BWD;               // [C][KT] k
@@ -258,6 +357,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
     const int kt = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
     const int m0 = kt * KT_BWD;
     const int NC = T / C;
+    const bool tiled = C == 64 && V % 4 == 0;
     for (int e = tid; e < KT_BWD * V; e += NT) {
         const int m = e / V, j = e % V;
         Hs[m * HV + j] = (h0 && m0 + m < K) ? h0[((size_t)bh * K + m0 + m) * V + j] : 0.f;
@@ -266,17 +366,24 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
         const size_t rowK = ((size_t)bh * T + (size_t)i * C) * K;
         const size_t rowV = ((size_t)bh * T + (size_t)i * C) * V;
         __syncthreads();
+        // log alpha and k of this chunk's channel tile staged by all threads (coalesced, independent loads), then
+        // the chunk-local cumsum by one thread per channel from shared memory
+        for (int e = tid; e < C * KT_BWD; e += NT) {
+            const int t = e / KT_BWD, m = e % KT_BWD;
+            const bool ok = m0 + m < K;
+            sb[e] = ok ? to_f(g[rowK + (size_t)t * K + m0 + m]) : 0.f;
+            sk[e] = ok ? to_f(k[rowK + (size_t)t * K + m0 + m]) : 0.f;
+        }
+        __syncthreads();
         if (tid < KT_BWD) {
             const int m = tid;
             float run = 0.f;
             for (int t = 0; t < C; ++t) {
-                const bool ok = m0 + m < K;
-                run += ok ? to_f(g[rowK + (size_t)t * K + m0 + m]) : 0.f;
+                run += sb[t * KT_BWD + m];
                 sb[t * KT_BWD + m] = run;
-                sk[t * KT_BWD + m] = ok ? to_f(k[rowK + (size_t)t * K + m0 + m]) : 0.f;
             }
-            for (int t = 0; t < C; ++t) ke[t * KT_BWD + m] = sk[t * KT_BWD + m] * expf(run - sb[t * KT_BWD + m]);
-            eG[m] = expf(run);
+            for (int t = 0; t < C; ++t) ke[t * KT_BWD + m] = sk[t * KT_BWD + m] * fexp(run - sb[t * KT_BWD + m]);
+            eG[m] = fexp(run);
         }
         const float* dPc = dPws + ((size_t)bh * NC + i) * (size_t)C * C;
         for (int e = tid; e < C * C; e += NT) sdP[e] = dPc[e];
@@ -287,7 +394,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
             const int t = e / KT_BWD, m = e % KT_BWD;
             float a = 0.f;
             const float bt = sb[t * KT_BWD + m];
-            for (int s = 0; s <= t; ++s) a += sdP[t * C + s] * sk[s * KT_BWD + m] * expf(bt - sb[s * KT_BWD + m]);
+            for (int s = 0; s <= t; ++s) a += sdP[t * C + s] * sk[s * KT_BWD + m] * fexp(bt - sb[s * KT_BWD + m]);
             acc[e] = a;
         }
         for (int c0 = 0; c0 < V; c0 += VS_BWD) {
@@ -300,21 +407,27 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
             }
             __syncthreads();
             // inter: e^{b_t} (.) sum_v dO_tv H[m][v]  (H = H_i, before the update below)
-            for (int e = tid; e < C * KT_BWD; e += NT) {
-                const int t = e / KT_BWD, m = e % KT_BWD;
-                float a = 0.f;
-                for (int j = 0; j < cs; ++j) a += sd[t * VS_BWD + j] * Hs[m * HV + c0 + j];
-                acc[e] += a * expf(sb[t * KT_BWD + m]);
-            }
+            if (tiled)
+                inter_tile64(acc, sd, Hs, HV, c0, cs, [&](int t, int m) { return fexp(sb[t * KT_BWD + m]); });
+            else
+                for (int e = tid; e < C * KT_BWD; e += NT) {
+                    const int t = e / KT_BWD, m = e % KT_BWD;
+                    float a = 0.f;
+                    for (int j = 0; j < cs; ++j) a += sd[t * VS_BWD + j] * Hs[m * HV + c0 + j];
+                    acc[e] += a * fexp(sb[t * KT_BWD + m]);
+                }
             __syncthreads();
             // H_{i+1}[m][v] = e^{Gamma_m} H + sum_s ke[s][m] V[s][v]  for this V slice
-            for (int e = tid; e < KT_BWD * VS_BWD; e += NT) {
-                const int m = e / VS_BWD, j = e % VS_BWD;
-                if (j >= cs) continue;
-                float a = eG[m] * Hs[m * HV + c0 + j];
-                for (int s = 0; s < C; ++s) a += ke[s * KT_BWD + m] * sv[s * VS_BWD + j];
-                Hs[m * HV + c0 + j] = colD ? a * colD[((size_t)bh * NC + i) * V + c0 + j] : a;
-            }
+            if (tiled && !colD)
+                update_tile64(Hs, ke, sv, HV, c0, cs, eG[tid & 31], C);
+            else
+                for (int e = tid; e < KT_BWD * VS_BWD; e += NT) {
+                    const int m = e / VS_BWD, j = e % VS_BWD;
+                    if (j >= cs) continue;
+                    float a = eG[m] * Hs[m * HV + c0 + j];
+                    for (int s = 0; s < C; ++s) a += ke[s * KT_BWD + m] * sv[s * VS_BWD + j];
+                    Hs[m * HV + c0 + j] = colD ? a * colD[((size_t)bh * NC + i) * V + c0 + j] : a;
+                }
         }
         __syncthreads();
         for (int e = tid; e < C * KT_BWD; e += NT) {
@@ -345,7 +458,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
                                                const float* __restrict__ colD = nullptr) {
     if (run_if && *run_if == 0) return;
     extern __shared__ float smem[];
-    const int HV = V + 1;                      // padded row stride (see k_bwd_dq)
+    const int HV = V + 4;                      // padded row stride (see k_bwd_dq)
     float* dH = smem;                          // [KT][V + 1]
     float* sb = dH + KT_BWD * HV;              // [C][KT] b
     float* sq = sb + C * KT_BWD;               // [C][KT] q
@@ -358,6 +471,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
     const int kt = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
     const int m0 = kt * KT_BWD;
     const int NC = T / C;
+    const bool tiled = C == 64 && V % 4 == 0;
     for (int e = tid; e < KT_BWD * V; e += NT) {
         const int m = e / V, j = e % V;
         dH[m * HV + j] = (dfinal && m0 + m < K) ? dfinal[((size_t)bh * K + m0 + m) * V + j] : 0.f;
@@ -376,16 +490,20 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
         __syncthreads();
         if (colD)   // adjoint of the column decay that followed chunk i's update: dH_{i+1} <- colD_i (.)_col dH_{i+1}
             for (int e = tid; e < KT_BWD * V; e += NT) dH[(e / V) * HV + e % V] *= colD[((size_t)bh * NC + i) * V + e % V];
+        for (int e = tid; e < C * KT_BWD; e += NT) {   // staged as in k_bwd_dq
+            const int t = e / KT_BWD, m = e % KT_BWD;
+            const bool ok = m0 + m < K;
+            sb[e] = ok ? to_f(g[rowK + (size_t)t * K + m0 + m]) : 0.f;
+            sq[e] = ok ? to_f(q[rowK + (size_t)t * K + m0 + m]) : 0.f;
+        }
+        __syncthreads();
         if (tid < KT_BWD) {
             const int m = tid;
-            const bool ok = m0 + m < K;
             float run = 0.f;
             for (int t = 0; t < C; ++t) {
-                run += ok ? to_f(g[rowK + (size_t)t * K + m0 + m]) : 0.f;
+                run += sb[t * KT_BWD + m];
                 sb[t * KT_BWD + m] = run;
-                const float qv = ok ? to_f(q[rowK + (size_t)t * K + m0 + m]) : 0.f;
-                sq[t * KT_BWD + m] = qv;
-                qe[t * KT_BWD + m] = qv * expf(run);
+                qe[t * KT_BWD + m] = sq[t * KT_BWD + m] * fexp(run);
             }
         }
         const float* dPc = dPws + ((size_t)bh * NC + i) * (size_t)C * C;
@@ -396,7 +514,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
             const int s = e / KT_BWD, m = e % KT_BWD;
             float a = 0.f;
             const float bs = sb[s * KT_BWD + m];
-            for (int t = s; t < C; ++t) a += sdP[t * C + s] * sq[t * KT_BWD + m] * expf(sb[t * KT_BWD + m] - bs);
+            for (int t = s; t < C; ++t) a += sdP[t * C + s] * sq[t * KT_BWD + m] * fexp(sb[t * KT_BWD + m] - bs);
             acc[e] = a;
         }
         for (int c0 = 0; c0 < V; c0 += VS_BWD) {
@@ -409,21 +527,29 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
             }
             __syncthreads();
             // inter: e^{Gamma - b_s} (.) sum_v V_sv dH_{i+1}[m][v]
-            for (int e = tid; e < C * KT_BWD; e += NT) {
-                const int s = e / KT_BWD, m = e % KT_BWD;
-                float a = 0.f;
-                for (int j = 0; j < cs; ++j) a += sv[s * VS_BWD + j] * dH[m * HV + c0 + j];
-                acc[e] += a * expf(sb[(C - 1) * KT_BWD + m] - sb[s * KT_BWD + m]);
-            }
+            if (tiled)
+                inter_tile64(acc, sv, dH, HV, c0, cs, [&](int t, int m) {
+                    return fexp(sb[(C - 1) * KT_BWD + m] - sb[t * KT_BWD + m]);
+                });
+            else
+                for (int e = tid; e < C * KT_BWD; e += NT) {
+                    const int s = e / KT_BWD, m = e % KT_BWD;
+                    float a = 0.f;
+                    for (int j = 0; j < cs; ++j) a += sv[s * VS_BWD + j] * dH[m * HV + c0 + j];
+                    acc[e] += a * fexp(sb[(C - 1) * KT_BWD + m] - sb[s * KT_BWD + m]);
+                }
             __syncthreads();
             // dH_i = e^{Gamma} dH_{i+1} + (q e^b)^T dO   for this V slice
-            for (int e = tid; e < KT_BWD * VS_BWD; e += NT) {
-                const int m = e / VS_BWD, j = e % VS_BWD;
-                if (j >= cs) continue;
-                float a = expf(sb[(C - 1) * KT_BWD + m]) * dH[m * HV + c0 + j];
-                for (int t = 0; t < C; ++t) a += qe[t * KT_BWD + m] * sd[t * VS_BWD + j];
-                dH[m * HV + c0 + j] = a;
-            }
+            if (tiled)
+                update_tile64(dH, qe, sd, HV, c0, cs, fexp(sb[(C - 1) * KT_BWD + (tid & 31)]), C);
+            else
+                for (int e = tid; e < KT_BWD * VS_BWD; e += NT) {
+                    const int m = e / VS_BWD, j = e % VS_BWD;
+                    if (j >= cs) continue;
+                    float a = fexp(sb[(C - 1) * KT_BWD + m]) * dH[m * HV + c0 + j];
+                    for (int t = 0; t < C; ++t) a += qe[t * KT_BWD + m] * sd[t * VS_BWD + j];
+                    dH[m * HV + c0 + j] = a;
+                }
         }
         __syncthreads();
         for (int e = tid; e < C * KT_BWD; e += NT) {
@@ -471,6 +597,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dv(const TQ* __restrict__ q, const T
     const int vt = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
     const int v0 = vt * VT_FWD;
     const int NC = T / C;
+    const bool tiled = C == 64 && K % 32 == 0;
     for (int e = tid; e < K * VT_FWD; e += NT) {
         const int m = e / VT_FWD, j = e % VT_FWD;
         dH[e] = (dfinal && v0 + j < V) ? dfinal[((size_t)bh * K + m) * V + v0 + j] : 0.f;
@@ -482,16 +609,18 @@ __global__ void __launch_bounds__(NT) k_bwd_dv(const TQ* __restrict__ q, const T
         if (colD)   // adjoint of the column decay after chunk i (see k_bwd_dk)
             for (int e = tid; e < K * VT_FWD; e += NT)
                 if (v0 + e % VT_FWD < V) dH[e] *= colD[((size_t)bh * NC + i) * V + v0 + e % VT_FWD];
-        for (int m = tid; m < K; m += NT) {
+        for (int m = tid; m < K; m += NT) {   // (unrolled as in k_fwd_state)
             float run = 0.f;
+#pragma unroll 8
             for (int t = 0; t < C; ++t) {
                 run += to_f(g[rowK + (size_t)t * K + m]);
                 ke[t * K + m] = run;
-                qe[t * K + m] = to_f(q[rowK + (size_t)t * K + m]) * expf(run);
+                qe[t * K + m] = to_f(q[rowK + (size_t)t * K + m]) * fexp(run);
             }
+#pragma unroll 8
             for (int t = 0; t < C; ++t)
-                ke[t * K + m] = to_f(k[rowK + (size_t)t * K + m]) * expf(run - ke[t * K + m]);
-            eG[m] = expf(run);
+                ke[t * K + m] = to_f(k[rowK + (size_t)t * K + m]) * fexp(run - ke[t * K + m]);
+            eG[m] = fexp(run);
         }
         for (int e = tid; e < C * VT_FWD; e += NT) {
             const int t = e / VT_FWD, j = e % VT_FWD;
@@ -504,15 +633,32 @@ __global__ void __launch_bounds__(NT) k_bwd_dv(const TQ* __restrict__ q, const T
         __syncthreads();
         if (mode == 0) {
             const int j = tid % VT_FWD;
-            for (int s = tid / VT_FWD; s < C; s += NT / VT_FWD) {
-                float a = 0.f;
-                for (int t = s; t < C; ++t) a += Ps[t * C + s] * sd[t * VT_FWD + j];
-                for (int m = 0; m < K; ++m) a += ke[s * K + m] * dH[m * VT_FWD + j];
-                if (v0 + j < V) dv[rowV + (size_t)s * V + v0 + j] = from_f<TQ>(a);
+            if (tiled) {
+                float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                const int w = tid / VT_FWD;
+                for (int t = 0; t < C; ++t) {
+                    const float x = sd[t * VT_FWD + j];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+                        if (t >= w + 8 * r) a[r] += Ps[t * C + w + 8 * r] * x;
+                }
+                rows_tile64(a, ke, dH, K);
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    if (v0 + j < V) dv[rowV + (size_t)(w + 8 * r) * V + v0 + j] = from_f<TQ>(a[r]);
+            } else {
+                for (int s = tid / VT_FWD; s < C; s += NT / VT_FWD) {
+                    float a = 0.f;
+                    for (int t = s; t < C; ++t) a += Ps[t * C + s] * sd[t * VT_FWD + j];
+                    for (int m = 0; m < K; ++m) a += ke[s * K + m] * dH[m * VT_FWD + j];
+                    if (v0 + j < V) dv[rowV + (size_t)s * V + v0 + j] = from_f<TQ>(a);
+                }
             }
             __syncthreads();
         }
-        {
+        if (tiled) {
+            update_vtile64(dH, eG, qe, sd, K, C, 1.f, false);
+        } else {
             const int j = tid % VT_FWD;
             for (int m = tid / VT_FWD; m < K; m += NT / VT_FWD) {
                 float a = eG[m] * dH[m * VT_FWD + j];
@@ -545,7 +691,7 @@ __global__ void __launch_bounds__(CQ * RG) k_step(const TQ* __restrict__ q, cons
     const int col = blockIdx.x * 4 * CQ + (tid % CQ) * 4;
     const int rg = tid / CQ;
     for (int m = tid; m < K; m += CQ * RG) {
-        sa[m] = expf(to_f(g[(size_t)bh * K + m]));
+        sa[m] = fexp(to_f(g[(size_t)bh * K + m]));
         sk[m] = to_f(k[(size_t)bh * K + m]);
         sq[m] = to_f(q[(size_t)bh * K + m]);
     }
@@ -610,7 +756,7 @@ __global__ void k_combine(const float* __restrict__ Hin, const float* __restrict
     const size_t n = (size_t)BH * K * V;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
         const size_t row = e / V;   // (bh, m)
-        Hout[e] = expf(D[row]) * Hin[e] + S[e];
+        Hout[e] = fexp(D[row]) * Hin[e] + S[e];
     }
 }
 
