@@ -31,6 +31,10 @@ __device__ __forceinline__ void ld8(const __nv_bfloat16* p, float (&x)[8]) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) { x[2 * i] = tc::bf16lo(w[i]); x[2 * i + 1] = tc::bf16hi(w[i]); }
 }
+__device__ __forceinline__ void ldf8(const float* p, float (&x)[8]) {   // 8 fp32 parameters, two 16-B loads
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p + 4));
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+}
 __device__ __forceinline__ void st8(__nv_bfloat16* p, const float (&x)[8]) {
     *reinterpret_cast<uint4*>(p) = make_uint4(tc::pack_bf16(x[0], x[1]), tc::pack_bf16(x[2], x[3]),
                                               tc::pack_bf16(x[4], x[5]), tc::pack_bf16(x[6], x[7]));
@@ -39,16 +43,17 @@ __device__ __forceinline__ void st8(__nv_bfloat16* p, const float (&x)[8]) {
 
 // ---- forward prep: P, z_alpha -> q, k, v [B,H,T,.] (bf16), log alpha [B,H,T,K] (fp32) ---------------------------
 // One thread per 8 consecutive elements of a row; the vector index space of a row is q | k | v | gate.
+template <typename I>   // index type: 32-bit when the element count allows (cheaper divisions)
 __global__ void k_prep(const __nv_bfloat16* __restrict__ P, int ldP, const __nv_bfloat16* __restrict__ Za,
                        const float* __restrict__ b_alpha, __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ k,
                        __nv_bfloat16* __restrict__ v, float* __restrict__ g, int B, int T, int H, int K, int V,
                        float inv_tau) {
     const int HK = H * K, HV = H * V, nvec = (3 * HK + HV) / 8;
-    const size_t total = (size_t)B * T * nvec;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const size_t row = i / nvec;                     // b * T + t
-        const int c = 8 * (int)(i % nvec);
-        const int b = (int)(row / T), t = (int)(row % T);
+    const I total = (I)B * T * nvec;
+    for (I i = (I)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (I)gridDim.x * blockDim.x) {
+        const I row = i / nvec;                          // b * T + t
+        const int c = 8 * (int)(i - row * nvec);
+        const int b = (int)(row / T), t = (int)(row - (I)b * T);
         float x[8];
         if (c < 2 * HK + HV) {                           // q | k | v: transpose to [B,H,T,D]
             ld8(P + row * ldP + c, x);
@@ -60,9 +65,10 @@ __global__ void k_prep(const __nv_bfloat16* __restrict__ P, int ldP, const __nv_
         } else {                                         // gate: log alpha = logsigmoid(z + b_alpha) / tau
             const int cc = c - 2 * HK - HV, h = cc / K, e = cc % K;
             ld8(Za + row * HK + cc, x);
-            float y[8];
+            float y[8], ba[8];
+            ldf8(b_alpha + cc, ba);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) y[j] = logsigmoid(x[j] + b_alpha[cc + j]) * inv_tau;
+            for (int j = 0; j < 8; ++j) y[j] = logsigmoid(x[j] + ba[j]) * inv_tau;
             float4* o = reinterpret_cast<float4*>(g + (((size_t)b * H + h) * T + t) * K + e);
             o[0] = make_float4(y[0], y[1], y[2], y[3]);
             o[1] = make_float4(y[4], y[5], y[6], y[7]);
@@ -78,18 +84,20 @@ __global__ void k_out(const __nv_bfloat16* __restrict__ O, const __nv_bfloat16* 
                       __nv_bfloat16* __restrict__ Z, float* __restrict__ mean_out, float* __restrict__ rstd_out,
                       int B, int T, int H, int V, float eps) {
     const int lane = threadIdx.x & 31;
-    const size_t nw = (size_t)B * T * H;
-    for (size_t w = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nw; w += ((size_t)gridDim.x * blockDim.x) >> 5) {
-        const size_t row = w / H;
-        const int h = (int)(w % H), b = (int)(row / T), t = (int)(row % T);
+    const int nw = B * T * H;   // (row, head) items; B*T*H < 2^31 (checked by the caller's shapes)
+    for (int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); w < nw; w += (int)((gridDim.x * blockDim.x) >> 5)) {
+        const int row = w / H, h = w - row * H, b = row / T, t = row - b * T;
         const __nv_bfloat16* o = O + (((size_t)b * H + h) * T + t) * V;
-        float x[NCH][8], s = 0.f;
+        float x[NCH][8], rp[NCH][8], s = 0.f;
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) {
+        for (int c = 0; c < NCH; ++c) {   // both rows' loads issued before any use (one memory latency per item)
             ld8(o + 8 * (lane + 32 * c), x[c]);
+            ld8(P + (size_t)row * ldP + r_off + h * V + 8 * (lane + 32 * c), rp[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
 #pragma unroll
             for (int j = 0; j < 8; ++j) s += x[c][j];
-        }
 #pragma unroll
         for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
         const float mu = s / V;
@@ -105,14 +113,16 @@ __global__ void k_out(const __nv_bfloat16* __restrict__ O, const __nv_bfloat16* 
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
             const int e = 8 * (lane + 32 * c), col = h * V + e;
-            float rp[8], z[8];
-            ld8(P + row * ldP + r_off + col, rp);
+            float z[8], br[8], lw[8], lb[8];
+            ldf8(b_r + col, br);
+            ldf8(ln_w + col, lw);
+            ldf8(ln_b + col, lb);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const float r = rp[j] + b_r[col + j];
-                z[j] = ((x[c][j] - mu) * rs * ln_w[col + j] + ln_b[col + j]) * (r * sigmoid(r));
+                const float r = rp[c][j] + br[j];
+                z[j] = ((x[c][j] - mu) * rs * lw[j] + lb[j]) * (r * sigmoid(r));
             }
-            st8(Z + row * (size_t)(H * V) + col, z);
+            st8(Z + (size_t)row * (H * V) + col, z);
         }
     }
 }
@@ -126,35 +136,59 @@ __global__ void k_out_bwd(const __nv_bfloat16* __restrict__ dZ, const __nv_bfloa
                           const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                           __nv_bfloat16* __restrict__ dO, __nv_bfloat16* __restrict__ dP, float* __restrict__ part,
                           int B, int T, int H, int V, int rows_per_cta) {
-    // blockDim = 32 * H: warp h handles head h of each of this CTA's rows
+    // blockDim = 32 * H: warp h handles head h of each of this CTA's rows, the next row's loads in flight while
+    // the current row is computed (the kernel is latency-bound otherwise: one row of loads per warp at a time).
     const int lane = threadIdx.x & 31, h = threadIdx.x >> 5;
     const size_t nrows = (size_t)B * T, HV = (size_t)H * V;
     float aw[NCH][8] = {}, ab[NCH][8] = {}, ar[NCH][8] = {};
     const size_t r0 = (size_t)blockIdx.x * rows_per_cta, r1 = min(nrows, r0 + rows_per_cta);
-    for (size_t row = r0; row < r1; ++row) {
+    uint4 X[NCH], R[NCH], D[NCH];
+    float MU = 0.f, RS = 0.f;
+    auto load = [&](size_t row) {
         const int b = (int)(row / T), t = (int)(row % T);
-        const size_t w = row * H + h;
-        const float mu = mean_in[w], rs = rstd_in[w];
         const __nv_bfloat16* o = O + (((size_t)b * H + h) * T + t) * V;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const int e = 8 * (lane + 32 * c), col = h * V + e;
+            X[c] = *reinterpret_cast<const uint4*>(o + e);
+            R[c] = *reinterpret_cast<const uint4*>(P + row * ldP + r_off + col);
+            D[c] = *reinterpret_cast<const uint4*>(dZ + row * HV + col);
+        }
+        MU = mean_in[row * H + h];
+        RS = rstd_in[row * H + h];
+    };
+    if (r0 < r1) load(r0);
+    for (size_t row = r0; row < r1; ++row) {
+        uint4 Xc[NCH], Rc[NCH], Dc[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) { Xc[c] = X[c]; Rc[c] = R[c]; Dc[c] = D[c]; }
+        const float mu = MU, rs = RS;
+        if (row + 1 < r1) load(row + 1);
+        const int b = (int)(row / T), t = (int)(row % T);
         float n[NCH][8], dn[NCH][8], s1 = 0.f, s2 = 0.f;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
             const int e = 8 * (lane + 32 * c), col = h * V + e;
-            float x[8], rp[8], dz[8], drp[8];
-            ld8(o + e, x);
-            ld8(P + row * ldP + r_off + col, rp);
-            ld8(dZ + row * HV + col, dz);
+            const uint32_t xw[4] = {Xc[c].x, Xc[c].y, Xc[c].z, Xc[c].w}, rw[4] = {Rc[c].x, Rc[c].y, Rc[c].z, Rc[c].w},
+                           dw[4] = {Dc[c].x, Dc[c].y, Dc[c].z, Dc[c].w};
+            float drp[8], br[8], lw[8], lb[8];
+            ldf8(b_r + col, br);
+            ldf8(ln_w + col, lw);
+            ldf8(ln_b + col, lb);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const float r = rp[j] + b_r[col + j], sg = sigmoid(r), sw = r * sg;
-                n[c][j] = (x[j] - mu) * rs;
-                const float a = n[c][j] * ln_w[col + j] + ln_b[col + j];
-                const float da = dz[j] * sw;                          // d(LN output after affine)
-                drp[j] = dz[j] * a * sg * (1.f + r * (1.f - sg));     // Swish'(r) = s (1 + r (1 - s))
+                const float xj = (j & 1) ? tc::bf16hi(xw[j >> 1]) : tc::bf16lo(xw[j >> 1]);
+                const float rj = (j & 1) ? tc::bf16hi(rw[j >> 1]) : tc::bf16lo(rw[j >> 1]);
+                const float dzj = (j & 1) ? tc::bf16hi(dw[j >> 1]) : tc::bf16lo(dw[j >> 1]);
+                const float r = rj + br[j], sg = sigmoid(r), sw = r * sg;
+                n[c][j] = (xj - mu) * rs;
+                const float a = n[c][j] * lw[j] + lb[j];
+                const float da = dzj * sw;                            // d(LN output after affine)
+                drp[j] = dzj * a * sg * (1.f + r * (1.f - sg));       // Swish'(r) = s (1 + r (1 - s))
                 aw[c][j] += da * n[c][j];
                 ab[c][j] += da;
                 ar[c][j] += drp[j];
-                dn[c][j] = da * ln_w[col + j];
+                dn[c][j] = da * lw[j];
                 s1 += dn[c][j];
                 s2 += dn[c][j] * n[c][j];
             }
@@ -189,17 +223,18 @@ __global__ void k_out_bwd(const __nv_bfloat16* __restrict__ dZ, const __nv_bfloa
 }
 
 // ---- backward of the prep: dq, dk, dv, d log alpha -> dP's q | k | v blocks, d z_alpha, d b_alpha partials -------
+template <typename I>
 __global__ void k_prep_bwd(const __nv_bfloat16* __restrict__ dq, const __nv_bfloat16* __restrict__ dk,
                            const __nv_bfloat16* __restrict__ dv, const float* __restrict__ dg,
                            const __nv_bfloat16* __restrict__ Za, const float* __restrict__ b_alpha,
                            __nv_bfloat16* __restrict__ dP, int ldP, __nv_bfloat16* __restrict__ dZa,
                            int B, int T, int H, int K, int V, float inv_tau) {
     const int HK = H * K, HV = H * V, nvec = (3 * HK + HV) / 8;
-    const size_t total = (size_t)B * T * nvec;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const size_t row = i / nvec;
-        const int c = 8 * (int)(i % nvec);
-        const int b = (int)(row / T), t = (int)(row % T);
+    const I total = (I)B * T * nvec;
+    for (I i = (I)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (I)gridDim.x * blockDim.x) {
+        const I row = i / nvec;
+        const int c = 8 * (int)(i - row * nvec);
+        const int b = (int)(row / T), t = (int)(row - (I)b * T);
         float x[8];
         if (c < 2 * HK + HV) {
             const bool isv = c >= 2 * HK;
@@ -214,9 +249,10 @@ __global__ void k_prep_bwd(const __nv_bfloat16* __restrict__ dq, const __nv_bflo
             const float4* gi = reinterpret_cast<const float4*>(dg + (((size_t)b * H + h) * T + t) * K + e);
             const float4 g0 = gi[0], g1 = gi[1];
             const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-            float y[8];
+            float y[8], ba[8];
+            ldf8(b_alpha + cc, ba);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) y[j] = gg[j] * sigmoid(-(x[j] + b_alpha[cc + j])) * inv_tau;
+            for (int j = 0; j < 8; ++j) y[j] = gg[j] * sigmoid(-(x[j] + ba[j])) * inv_tau;
             st8(dZa + row * HK + cc, y);
         }
     }
@@ -285,9 +321,14 @@ int gla_layer_prep(int B, int T, int H, int K, int V, float tau, const void* P, 
     if ((size_t)B * T == 0) return GLA_OK;
     const size_t work = (size_t)B * T * (3 * H * K + H * V) / 8;
     GLA_PROF("layer::prep", (cudaStream_t)stream);
-    gla::layer::k_prep<<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(
-        (const __nv_bfloat16*)P, ldP, (const __nv_bfloat16*)z_alpha, b_alpha, (__nv_bfloat16*)q, (__nv_bfloat16*)k,
-        (__nv_bfloat16*)v, log_alpha, B, T, H, K, V, 1.f / tau);
+    if (work < (1u << 31))
+        gla::layer::k_prep<unsigned><<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(
+            (const __nv_bfloat16*)P, ldP, (const __nv_bfloat16*)z_alpha, b_alpha, (__nv_bfloat16*)q, (__nv_bfloat16*)k,
+            (__nv_bfloat16*)v, log_alpha, B, T, H, K, V, 1.f / tau);
+    else
+        gla::layer::k_prep<size_t><<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(
+            (const __nv_bfloat16*)P, ldP, (const __nv_bfloat16*)z_alpha, b_alpha, (__nv_bfloat16*)q, (__nv_bfloat16*)k,
+            (__nv_bfloat16*)v, log_alpha, B, T, H, K, V, 1.f / tau);
     return lstatus(cudaGetLastError());
 }
 
@@ -387,10 +428,16 @@ int gla_layer_prep_bwd(int B, int T, int H, int K, int V, float tau, const void*
     const size_t work = rows * (3 * H * K + H * V) / 8;
     {
         GLA_PROF("layer::prep_bwd", st);
-        gla::layer::k_prep_bwd<<<grid_for(work, 256), 256, 0, st>>>(
-            (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, d_log_alpha,
-            (const __nv_bfloat16*)z_alpha, b_alpha, (__nv_bfloat16*)dP, ldP, (__nv_bfloat16*)d_z_alpha, B, T, H, K, V,
-            1.f / tau);
+        if (work < (1u << 31))
+            gla::layer::k_prep_bwd<unsigned><<<grid_for(work, 256), 256, 0, st>>>(
+                (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, d_log_alpha,
+                (const __nv_bfloat16*)z_alpha, b_alpha, (__nv_bfloat16*)dP, ldP, (__nv_bfloat16*)d_z_alpha, B, T, H, K,
+                V, 1.f / tau);
+        else
+            gla::layer::k_prep_bwd<size_t><<<grid_for(work, 256), 256, 0, st>>>(
+                (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, d_log_alpha,
+                (const __nv_bfloat16*)z_alpha, b_alpha, (__nv_bfloat16*)dP, ldP, (__nv_bfloat16*)d_z_alpha, B, T, H, K,
+                V, 1.f / tau);
     }
     const int nb2 = (int)(rows < 148 ? rows : 148);
     const int rpc = (int)((rows + nb2 - 1) / nb2);

@@ -16,6 +16,7 @@
 //   k_combine      : H_out = e^{D} (.) H_in + S_loc.
 // Layout [B,H,T,D] row-major; one (b,h) unit = "bh".  No atomics: fixed reduction order.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "prof.h"
@@ -29,7 +30,12 @@ constexpr int KS = 24;       // channel slice for the intra kernels (3 x [MAXC][
 constexpr int VT_FWD = 32;   // V tile of k_fwd_state / k_bwd_dv
 constexpr int KT_BWD = 32;   // K tile of k_bwd_dq / k_bwd_dk
 constexpr int VS_BWD = 64;   // V slice staged per step in k_bwd_dq / k_bwd_dk
-constexpr int MAXC = 128;    // largest chunk C (the f4 chunk-size sweep runs C = 8 .. 128)
+constexpr int MAXC = 128;
+// GLA_SIMT_NOTILE=1: every SIMT kernel runs its scalar loops (the chunk-size sweep compares plans on equal code)
+static int simt_tiles() {
+    static const int v = getenv("GLA_SIMT_NOTILE") ? 0 : 1;
+    return v;
+}    // largest chunk C (the f4 chunk-size sweep runs C = 8 .. 128)
 
 // ---------------------------------------------------------------------------------------------
 // P[t][s] (s <= t) for one chunk.  grid (T/C, BH).  P written to Pws[bh][chunk][C][C] (fp32).
@@ -174,7 +180,7 @@ __global__ void __launch_bounds__(NT) k_fwd_state(const TQ* __restrict__ q, cons
                                                   const float* __restrict__ Pws, const float* __restrict__ h0,
                                                   TQ* __restrict__ out, float* __restrict__ final_state,
                                                   float* __restrict__ log_decay, int T, int K, int V, int C,
-                                                  int mode, const float* __restrict__ colD = nullptr) {
+                                                  int mode, const float* __restrict__ colD = nullptr, int tile_ok = 1) {
     // colD (value-gate path, simt_beta.cu; NULL = 1): the state update is followed by a per-value-column decay
     // colD[bh][chunk][v], i.e. H <- colD (.)_col (e^Gamma H + (K e^{Gamma-b})^T V).
     extern __shared__ float smem[];
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(NT) k_fwd_state(const TQ* __restrict__ q, cons
     const int vt = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
     const int v0 = vt * VT_FWD;
     const int NC = T / C;
-    const bool tiled = C == 64 && K % 32 == 0;
+    const bool tiled = tile_ok && C == 64 && K % 32 == 0;
     for (int e = tid; e < K * VT_FWD; e += NT) {
         const int m = e / VT_FWD, j = e % VT_FWD;
         Hs[e] = (h0 && v0 + j < V) ? h0[((size_t)bh * K + m) * V + v0 + j] : 0.f;
@@ -341,7 +347,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
                                                const float* __restrict__ dPws, TQ* __restrict__ dq,
                                                float* __restrict__ dq32, float* __restrict__ ST,
                                                int T, int K, int V, int C, const int* __restrict__ run_if,
-                                               const float* __restrict__ colD = nullptr) {
+                                               const float* __restrict__ colD = nullptr, int tile_ok = 1) {
     if (run_if && *run_if == 0) return;
     extern __shared__ float smem[];
     const int HV = V + 4;                      // padded row stride (16-B rows; lanes = channels hit distinct banks)
@@ -357,7 +363,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dq(const TQ* __restrict__ q, const T
     const int kt = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
     const int m0 = kt * KT_BWD;
     const int NC = T / C;
-    const bool tiled = C == 64 && V % 4 == 0;
+    const bool tiled = tile_ok && C == 64 && V % 4 == 0;
     for (int e = tid; e < KT_BWD * V; e += NT) {
         const int m = e / V, j = e % V;
         Hs[m * HV + j] = (h0 && m0 + m < K) ? h0[((size_t)bh * K + m0 + m) * V + j] : 0.f;
@@ -455,7 +461,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
                                                const float* __restrict__ ST, TQ* __restrict__ dk,
                                                float* __restrict__ dg, float* __restrict__ dh0,
                                                int T, int K, int V, int C, const int* __restrict__ run_if,
-                                               const float* __restrict__ colD = nullptr) {
+                                               const float* __restrict__ colD = nullptr, int tile_ok = 1) {
     if (run_if && *run_if == 0) return;
     extern __shared__ float smem[];
     const int HV = V + 4;                      // padded row stride (see k_bwd_dq)
@@ -471,7 +477,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dk(const TQ* __restrict__ q, const T
     const int kt = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
     const int m0 = kt * KT_BWD;
     const int NC = T / C;
-    const bool tiled = C == 64 && V % 4 == 0;
+    const bool tiled = tile_ok && C == 64 && V % 4 == 0;
     for (int e = tid; e < KT_BWD * V; e += NT) {
         const int m = e / V, j = e % V;
         dH[m * HV + j] = (dfinal && m0 + m < K) ? dfinal[((size_t)bh * K + m0 + m) * V + j] : 0.f;
@@ -585,7 +591,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dv(const TQ* __restrict__ q, const T
                                                const float* __restrict__ dfinal, const float* __restrict__ Pws,
                                                TQ* __restrict__ dv, float* __restrict__ dh0,
                                                int T, int K, int V, int C, int mode, const int* __restrict__ run_if,
-                                               const float* __restrict__ colD = nullptr) {
+                                               const float* __restrict__ colD = nullptr, int tile_ok = 1) {
     if (run_if && *run_if == 0) return;
     extern __shared__ float smem[];
     float* qe = smem;                          // [C][K] q e^{b}
@@ -597,7 +603,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dv(const TQ* __restrict__ q, const T
     const int vt = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
     const int v0 = vt * VT_FWD;
     const int NC = T / C;
-    const bool tiled = C == 64 && K % 32 == 0;
+    const bool tiled = tile_ok && C == 64 && K % 32 == 0;
     for (int e = tid; e < K * VT_FWD; e += NT) {
         const int m = e / VT_FWD, j = e % VT_FWD;
         dH[e] = (dfinal && v0 + j < V) ? dfinal[((size_t)bh * K + m) * V + v0 + j] : 0.f;
@@ -786,7 +792,7 @@ static cudaError_t fwd_impl(const Problem& p, cudaStream_t st) {
         GLA_PROF("simt::k_fwd_state", st);
         k_fwd_state<TQ, TG><<<dim3(cdiv(p.V, VT_FWD), BH), NT, sm, st>>>(q, k, v, g, Pws, p.h0, (TQ*)p.out,
                                                                         p.final_state, p.log_decay, p.T, p.K,
-                                                                        p.V, p.C, p.mode, p.colD);
+                                                                        p.V, p.C, p.mode, p.colD, simt_tiles());
     }
     return cudaGetLastError();
 }
@@ -861,18 +867,20 @@ static cudaError_t bwd_impl(const BwdProblem& p, cudaStream_t st) {
     {
         GLA_PROF("simt::k_bwd_dq", st);
         k_bwd_dq<TQ, TG><<<dim3(cdiv(p.K, KT_BWD), BH), NT, smk, st>>>(q, k, v, g, dO, p.h0, dPws, (TQ*)p.dq, dq32,
-                                                                      ST, p.T, p.K, p.V, p.C, nullptr, p.colD);
+                                                                      ST, p.T, p.K, p.V, p.C, nullptr, p.colD,
+                                                                      simt_tiles());
     }
     {
         GLA_PROF("simt::k_bwd_dk", st);
         k_bwd_dk<TQ, TG><<<dim3(cdiv(p.K, KT_BWD), BH), NT, smk, st>>>(q, k, v, g, dO, p.dfinal, dPws, dq32, ST,
                                                                       (TQ*)p.dk, p.dg, p.dh0, p.T, p.K, p.V, p.C, nullptr,
-                                                                      p.colD);
+                                                                      p.colD, simt_tiles());
     }
     {
         GLA_PROF("simt::k_bwd_dv", st);
         k_bwd_dv<TQ, TG><<<dim3(cdiv(p.V, VT_FWD), BH), NT, smv, st>>>(q, k, g, dO, p.dfinal, Pws, (TQ*)p.dv,
-                                                                      nullptr, p.T, p.K, p.V, p.C, 0, nullptr, p.colD);
+                                                                      nullptr, p.T, p.K, p.V, p.C, 0, nullptr, p.colD,
+                                                                      simt_tiles());
     }
     return cudaGetLastError();
 }

@@ -10,6 +10,9 @@ import argparse
 import os
 import sys
 
+# the SIMT kernels' register-tiled loops exist only for C = 64: compare the plans on the same (scalar) code
+os.environ.setdefault("GLA_SIMT_NOTILE", "1")
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
@@ -67,7 +70,9 @@ lines = [f"# Chunk-size sweep (f4; P:471-490 Fig. 2 right) -- B={B}, H={H}, T={T
          "`intra scores` = the intra-chunk score blocks P (k_intra_P; on the TC row the prep kernel, which also "
          "forms Q~, K~); `state passing` = the inter-chunk recurrence alone (gla_state_summary, no outputs); "
          "`forward walk` = state passing + cross-chunk output + P V.  The SIMT backward is the fp32 debug "
-         "path (one CTA per (b,h) and 32-channel tile): its totals show the trend, not a tuned kernel.", "",
+         "path (one CTA per (b,h) and 32-channel tile): its totals show the trend, not a tuned kernel.  "
+         "The SIMT rows run the scalar loops for every C (GLA_SIMT_NOTILE=1; the register-tiled loops exist "
+         "only for C = 64).", "",
          "| path / plan | intra scores | state passing | forward walk | forward total | backward total |",
          "|---|---|---|---|---|---|"]
 for r in rows:
