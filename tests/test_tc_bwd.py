@@ -92,8 +92,8 @@ def test_tc_bwd_long_sequence_dlog_alpha(T):
 
 
 @pytest.mark.parametrize("gate", ["std", "strong", "extreme", "mixed"])
-@pytest.mark.parametrize("K,V", [(256, 512), (128, 256)])
-def test_tc_bwd_saved_forward_operands(gate, K, V):
+@pytest.mark.parametrize("K,V", [(256, 512), (128, 256), (128, 512), (256, 256)])   # every K-tiled walk variant:
+def test_tc_bwd_saved_forward_operands(gate, K, V):                                 # 1 or 2 channel groups x 1 or 2 value halves
     """gla_chunk_bwd_saved (reuses the forward's Q~, K~, P, (r, Gamma), exact-path flags and anchor states, forms
     only dP, runs the K-tiled dq walk) against the fp64 oracle for every gradient, and against the recomputing
     backward: dv, dh0 bitwise (same kernels), dq, dk, d log alpha within the bf16 bar (different dq walks)."""
