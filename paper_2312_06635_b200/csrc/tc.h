@@ -49,8 +49,10 @@ cudaError_t dq_kwalk(int K, int V, const CUtensorMap& mK, const CUtensorMap& mDP
 cudaError_t dk_kwalk(int K, int V, const CUtensorMap& mQ, const CUtensorMap& mDP, const CUtensorMap& mD,
                      const CUtensorMap& mV, const float* stats, const float* dfinal, float* dk32, const int* flag,
                      int T, int units, cudaStream_t st);
+// skip_edge (segment split only): the last segment's summary (adj = false) / the first one's (adj = true) is not
+// computed -- the chains never read it.
 cudaError_t seg_summary(const CUtensorMap& mB, const CUtensorMap& mA, const float* stats, const int* flags, float* out,
-                        int K, int V, int Tv, int S, int units, bool adj, cudaStream_t st);
+                        int K, int V, int Tv, int S, int units, bool adj, cudaStream_t st, bool skip_edge = false);
 cudaError_t seg_chain_fwd(const float* stats, const float* h0, const float* S_loc, float* Hv, int BH, int S, int NC,
                           int K, int V, cudaStream_t st);
 cudaError_t seg_chain_bwd(const float* stats, const float* dfinal, const float* dh_loc, float* dFv, int BH, int S,

@@ -1303,7 +1303,8 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         // gives every segment's true d_final_state (the segment-entry states h0v come from the forward)
         if (seg_summary_ok(K, p.V)) {   // one tensor-core contraction per segment (A = Q~hi e^{r + carry}, B = dO)
             GLA_PROF("tc::bwd_dstate_summary", st);
-            if ((e = seg_summary(mD, mQ, stats, fflags, dhv, K, p.V, Tv, S, BHv, true, st)) != cudaSuccess) return e;
+            if ((e = seg_summary(mD, mQ, stats, fflags, dhv, K, p.V, Tv, S, BHv, true, st, true)) != cudaSuccess)
+                return e;
         } else {
             GLA_PROF("tc::bwd_dstate_summary", st);
             k_bwd_dkv3<K, 0><<<grid, Dkv3Cfg<K>::NTHR, Dkv3Cfg<K>::SMEM, st>>>(

@@ -615,7 +615,11 @@ template <int ADJ>
 __global__ void __launch_bounds__(288, 1)
 k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK,
               const float* __restrict__ stats, const int* __restrict__ flags, float* __restrict__ S_loc, int K, int V,
-              int Tv, int S) {
+              int Tv, int S, int skip) {
+    // skip = 1 (segment split): the summary nobody reads is not computed -- the last segment's end state (the
+    // forward chain stops before it; the full walk writes the final state) / the first segment's adjoint (the
+    // backward chain stops after segment 1; the dv walk writes d_initial_state).  blockIdx.z then enumerates the
+    // (b,h) x (S - 1) remaining segments.
     // ADJ = 0: A = K~hi (.) e^{Gamma - r + carry}: the prep kernel's K~hi = k e^{r - b} (exact-path chunks:
     // k e^{Gamma - b}) times a per-channel factor <= 1, so A_t = k_t e^{sum_{u > t} log alpha_u} (suffix to the
     // segment's end); the carry (sum of Gamma over the later chunks) comes from the per-chunk statistics.
@@ -630,8 +634,9 @@ k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ C
     __shared__ float fac[2][128];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int k0 = 128 * blockIdx.x, v0 = 256 * blockIdx.y;
-    const size_t unit = blockIdx.z, rowb = unit * (size_t)Tv;
-    const int nb = Tv / CH, bh = (int)(unit / S), seg = (int)(unit % S), NC = nb * S;
+    const int nseg = S - skip, bh = (int)(blockIdx.z / nseg), seg = (int)(blockIdx.z % nseg) + (ADJ ? skip : 0);
+    const size_t unit = (size_t)bh * S + seg, rowb = unit * (size_t)Tv;
+    const int nb = Tv / CH, NC = nb * S;
     if (warp == 0) tmem_alloc(&tmem_base, 256);
     if (tid == 0) {
         for (int j = 0; j < NS; ++j) { mbar_init(&bar_v[j], 1); mbar_init(&bar_free[j], 1); mbar_init(&bar_a[j], 256); }
@@ -741,19 +746,20 @@ k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ C
 bool seg_summary_ok(int K, int V) { return K % 128 == 0 && V % 256 == 0 && !getenv("GLA_SUMMARY_WALK"); }
 
 cudaError_t seg_summary(const CUtensorMap& mB, const CUtensorMap& mA, const float* stats, const int* flags, float* out,
-                        int K, int V, int Tv, int S, int units, bool adj, cudaStream_t st) {
+                        int K, int V, int Tv, int S, int units, bool adj, cudaStream_t st, bool skip_edge) {
     cudaError_t e;
-    const dim3 grid(K / 128, V / 256, (unsigned)units);
+    const int skip = (skip_edge && S > 1) ? 1 : 0;
+    const dim3 grid(K / 128, V / 256, (unsigned)(units / S * (S - skip)));
     if (adj) {
         if ((e = cudaFuncSetAttribute(k_seg_summary<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)SumCfg::SMEM)))
             return e;
-        k_seg_summary<1><<<grid, 288, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S);
+        k_seg_summary<1><<<grid, 288, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S, skip);
     } else {
         if ((e = cudaFuncSetAttribute(k_seg_summary<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)SumCfg::SMEM)))
             return e;
-        k_seg_summary<0><<<grid, 288, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S);
+        k_seg_summary<0><<<grid, 288, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S, skip);
     }
     return cudaGetLastError();
 }
@@ -838,7 +844,7 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     if (seg_summary_ok(K, p.V)) {
         // chunk-parallel summaries: one tensor-core contraction per (channel tile, value tile, segment)
         GLA_PROF("tc::fwd_state_summary", st);
-        if ((e = seg_summary(mV, mK, stats, flags, slv, K, p.V, Tv, S, (int)(BH * S), false, st)) != cudaSuccess)
+        if ((e = seg_summary(mV, mK, stats, flags, slv, K, p.V, Tv, S, (int)(BH * S), false, st, true)) != cudaSuccess)
             return e;
     } else {
         GLA_PROF("tc::fwd_state_summary", st);
