@@ -43,6 +43,25 @@ int fwd_segments(int BH, int V, int NC) {
     return S >= 4 ? S : 1;
 }
 
+int seg_parts(int BH, int K, int V, int NC, int S) {
+    if (S <= 1) return 1;
+    static int force = -1;   // GLA_SEG_PARTS=P (a power of two <= 8) where it divides the segment's blocks
+    if (force < 0) {
+        const char* e = getenv("GLA_SEG_PARTS");
+        force = e ? atoi(e) : 0;
+    }
+    if (force > 0) return ((NC / S) % force == 0 && NC / S / force >= 4 && force <= 8) ? force : 1;
+    // The split summaries run one CTA per (128 channels, 256 values, segment, part).  One CTA streams a block in
+    // ~0.86 us (latency-bound) and all CTAs together ~110 blocks/us (the L2 -> SM load rate), so parts pay only
+    // while they stay within one wave (T = 8K at 1.3B: 64 -> 128 CTAs, 55 -> 41 us; two waves were slower at
+    // every measured shape, profiles/r2_seg_parts.md).
+    const long ctas = (long)(K / 128) * (V / 256) * BH * (S - 1);
+    const int nb = NC / S;
+    int P = 1;
+    while (P < 8 && ctas * 2 * P <= num_sms() && nb % (2 * P) == 0 && nb / (2 * P) >= 4) P *= 2;
+    return P;
+}
+
 bool supported(int B, int H, int T, int K, int V, int C, int c, int qkv_dtype, int gate_dtype) {
     (void)B; (void)H; (void)T; (void)gate_dtype;
     return qkv_dtype == 0 && (K == 64 || K == 128 || K == 256) && V % 128 == 0 && C == 64 && c > 0 && 64 % c == 0;

@@ -31,6 +31,9 @@ struct FwdSaved {
 // wave and every segment keeps >= 8 chunks; S >= 4, else 1), or at most half of them with segments of >= 32
 // chunks (S = 2).  GLA_SEGMENTS=1 disables it.
 int fwd_segments(int BH, int V, int NC);
+// With S > 1 segments, each segment's summary contraction is split over seg_parts() token ranges (partial sums
+// added in a fixed order by the chains), so the summary kernels fill the SMs (1 when S == 1).
+int seg_parts(int BH, int K, int V, int NC, int S);
 // Sequential state chains over the segments of every (b,h): forward H_{s+1} = e^{D_s} H_s + S_loc_s
 // (writes H_s for every s; H_0 = h0 or 0), backward dF_{s-1} = e^{D_s} dF_s + dh_loc_s (dF_{S-1} = dfinal or 0).
 // D_s = sum of the chunk totals Gamma over segment s, read from the prep statistics.
@@ -52,11 +55,12 @@ cudaError_t dk_kwalk(int K, int V, const CUtensorMap& mQ, const CUtensorMap& mDP
 // skip_edge (segment split only): the last segment's summary (adj = false) / the first one's (adj = true) is not
 // computed -- the chains never read it.
 cudaError_t seg_summary(const CUtensorMap& mB, const CUtensorMap& mA, const float* stats, const int* flags, float* out,
-                        int K, int V, int Tv, int S, int units, bool adj, cudaStream_t st, bool skip_edge = false);
+                        int K, int V, int Tv, int S, int units, bool adj, cudaStream_t st, bool skip_edge = false,
+                        int parts = 1, float* dec = nullptr);
 cudaError_t seg_chain_fwd(const float* stats, const float* h0, const float* S_loc, float* Hv, int BH, int S, int NC,
-                          int K, int V, cudaStream_t st);
+                          int K, int V, cudaStream_t st, int parts = 1, const float* dec = nullptr);
 cudaError_t seg_chain_bwd(const float* stats, const float* dfinal, const float* dh_loc, float* dFv, int BH, int S,
-                          int NC, int K, int V, cudaStream_t st);
+                          int NC, int K, int V, cudaStream_t st, int parts = 1, const float* dec = nullptr);
 // TC segment summaries of a whole [B,H,T] call (gla_state_summary / gla_dstate_summary): p.q, p.k, p.g as in the
 // forward (adj: p.k may alias p.q), B_op = v (adj = false) or d_out (adj = true); workspace p.ws of fwd_ws size.
 bool summary_tc_ok(int K, int V);

@@ -1177,7 +1177,9 @@ size_t bwd_tc_ws(int B, int H, int T, int K, int V, int C) {
     bytes += NA * BH * V * K * sizeof(__nv_bfloat16);           // state anchors (bf16)
     bytes += NA * NVT * BH * K * sizeof(float);                 // anchor row-sum partials
     bytes = (bytes + 255) & ~size_t(255);
-    if (Smax > 1) bytes += 2 * BH * Smax * K * V * sizeof(float);   // per-segment d_final / d_initial states
+    if (Smax > 1)   // per-segment d_final states; d_initial states (the split summaries' partials before the chain)
+        bytes += (1 + seg_parts((int)BH, K, V, T / CH, Smax)) * BH * Smax * K * V * sizeof(float) +
+                 BH * Smax * K * sizeof(float);   // per-segment log decays
     return bytes + simt::bwd_ws(B, H, T, K, V, C);              // exact-path fallback scratch
 }
 
@@ -1259,8 +1261,11 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     used += NA * BH * p.V * K * 2 + NA * NVT * BH * K * 4;
     used = (used + 255) & ~size_t(255);
     float* dFv = (float*)(ws + used);                       // per-segment d_final_state (S > 1)
-    float* dhv = dFv + (Smax > 1 ? (size_t)BH * Smax * K * p.V : 0);   // per-segment dh0 / dh_loc
-    if (Smax > 1) used += 2 * (size_t)BH * Smax * K * p.V * 4;
+    float* dhv = dFv + (Smax > 1 ? (size_t)BH * Smax * K * p.V : 0);   // per-segment dh0 / dh_loc (partials)
+    const int SP = (Smax > 1 && seg_summary_ok(K, p.V)) ? seg_parts(BH, K, p.V, NC, Smax) : 1;
+    if (Smax > 1) used += (size_t)(1 + seg_parts(BH, K, p.V, NC, Smax)) * BH * Smax * K * p.V * 4;
+    float* dec = (Smax > 1 && seg_summary_ok(K, p.V)) ? (float*)(ws + used) : nullptr;   // per-segment log decays
+    if (Smax > 1) used += (size_t)BH * Smax * K * 4;
     cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
     CUtensorMap mQ, mK, mP, mDP, mV, mD;
@@ -1303,7 +1308,7 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         // gives every segment's true d_final_state (the segment-entry states h0v come from the forward)
         if (seg_summary_ok(K, p.V)) {   // one tensor-core contraction per segment (A = Q~hi e^{r + carry}, B = dO)
             GLA_PROF("tc::bwd_dstate_summary", st);
-            if ((e = seg_summary(mD, mQ, stats, fflags, dhv, K, p.V, Tv, S, BHv, true, st, true)) != cudaSuccess)
+            if ((e = seg_summary(mD, mQ, stats, fflags, dhv, K, p.V, Tv, S, BHv, true, st, true, SP, dec)) != cudaSuccess)
                 return e;
         } else {
             GLA_PROF("tc::bwd_dstate_summary", st);
@@ -1312,7 +1317,8 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
                 p.V);
         }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        if ((e = seg_chain_bwd(stats, p.dfinal, dhv, dFv, BH, S, NC, K, p.V, st)) != cudaSuccess) return e;
+        if ((e = seg_chain_bwd(stats, p.dfinal, dhv, dFv, BH, S, NC, K, p.V, st, SP,
+                               seg_summary_ok(K, p.V) ? dec : nullptr)) != cudaSuccess) return e;
         dfin = dFv;
         dh0w = p.dh0 ? dhv : nullptr;
     }

@@ -615,7 +615,7 @@ template <int ADJ>
 __global__ void __launch_bounds__(288, 1)
 k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK,
               const float* __restrict__ stats, const int* __restrict__ flags, float* __restrict__ S_loc, int K, int V,
-              int Tv, int S, int skip) {
+              int Tv, int S, int skip, int P, float* __restrict__ dec) {
     // skip = 1 (segment split): the summary nobody reads is not computed -- the last segment's end state (the
     // forward chain stops before it; the full walk writes the final state) / the first segment's adjoint (the
     // backward chain stops after segment 1; the dv walk writes d_initial_state).  blockIdx.z then enumerates the
@@ -631,12 +631,15 @@ k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ C
     constexpr int NS = SumCfg::NS;
     __shared__ uint64_t bar_v[NS], bar_free[NS], bar_a[NS];
     __shared__ uint32_t tmem_base;
-    __shared__ float fac[2][128];
+    __shared__ __align__(16) float fac[2][128];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int k0 = 128 * blockIdx.x, v0 = 256 * blockIdx.y;
-    const int nseg = S - skip, bh = (int)(blockIdx.z / nseg), seg = (int)(blockIdx.z % nseg) + (ADJ ? skip : 0);
+    // P > 1: blockIdx.z also enumerates P token ranges of the segment (walk steps [part nbp, (part+1) nbp)); the
+    // partial sums go to S_loc[(unit P + part)] and the chains add them in part order.
+    const int nseg = S - skip, part = (int)(blockIdx.z % P), zz = (int)(blockIdx.z / P);
+    const int bh = zz / nseg, seg = zz % nseg + (ADJ ? skip : 0);
     const size_t unit = (size_t)bh * S + seg, rowb = unit * (size_t)Tv;
-    const int nb = Tv / CH, NC = nb * S;
+    const int nbs = Tv / CH, NC = nbs * S, nb = nbs / P, j0 = part * nb;   // this CTA's walk steps: j0 + [0, nb)
     if (warp == 0) tmem_alloc(&tmem_base, 256);
     if (tid == 0) {
         for (int j = 0; j < NS; ++j) { mbar_init(&bar_v[j], 1); mbar_init(&bar_free[j], 1); mbar_init(&bar_a[j], 256); }
@@ -654,7 +657,7 @@ k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ C
             auto load_blk = [&](int j) {                       // K~hi and V of block j -> stage j % NS
                 uint8_t* sA = sm + (j % NS) * SumCfg::STAGE;
                 uint64_t* bar = &bar_v[j % NS];
-                const int r0 = (int)(rowb + (size_t)(ADJ ? j : nb - 1 - j) * CH);
+                const int r0 = (int)(rowb + (size_t)(ADJ ? j0 + j : nbs - 1 - (j0 + j)) * CH);
                 mbar_expect_tx(bar, SumCfg::STAGE);
                 tma_load_2d(sA, &tmK, bar, k0, r0);
                 tma_load_2d(sA + 8192, &tmK, bar, k0 + 64, r0);
@@ -685,13 +688,19 @@ k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ C
         float carry = 0.f;                             // channel tid (< 128): sum of Gamma over the passed chunks
         float nr = 0.f, nG = 0.f;                      // (r, Gamma, flag) of the next block, loaded one ahead
         int nf = 0;
+        auto chunk_idx = [&](int j) {                  // walk step j of the segment -> chunk index
+            return (size_t)bh * NC + (size_t)seg * nbs + (ADJ ? j : nbs - 1 - j);
+        };
         auto load_st = [&](int j) {
-            const size_t ci = (size_t)bh * NC + (size_t)seg * nb + (ADJ ? j : nb - 1 - j);
+            const size_t ci = chunk_idx(j0 + j);
             nr = stats[ci * 2 * K + k0 + tid];
             nG = stats[ci * 2 * K + K + k0 + tid];
             nf = flags[ci];
         };
-        if (tid < 128) load_st(0);
+        if (tid < 128) {
+            for (int j = 0; j < j0; ++j) carry += stats[chunk_idx(j) * 2 * K + K + k0 + tid];   // earlier parts' chunks
+            load_st(0);
+        }
         for (int j = 0; j < nb; ++j) {
             const int bs = j % NS;
             uint8_t* sA = sm + bs * SumCfg::STAGE;
@@ -703,28 +712,35 @@ k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ C
                 if (j + 1 < nb) load_st(j + 1);
             }
             named_bar_sync(1, 256);                    // fac[j & 1] written (its readers of block j-2 are done)
+            // thread tid scales channels 8 (tid % 16) + [0, 8) of rows tid / 16 + 16 e: its 8 factors are read once
+            // (two 16-byte loads), and each quarter-warp touches the 8 positions of one 128-byte row (no conflicts)
+            const int c8 = tid & 15, blk = c8 >> 3;
+            const float4 f0 = *reinterpret_cast<const float4*>(fj + 8 * c8);
+            const float4 f1 = *reinterpret_cast<const float4*>(fj + 8 * c8 + 4);
+            const float fv[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
             mbar_wait(&bar_v[bs], (j / NS) & 1);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {              // 1024 16-byte chunks of the two SW128 blocks
-                const int id = tid + 256 * e, blk = id >> 9, row = (id >> 3) & 63, pos = id & 7;
-                const int cb = 64 * blk + 8 * (pos ^ (row & 7));
+                const int row = (tid >> 4) + 16 * e, pos = (c8 & 7) ^ (row & 7);
                 uint4* pch = reinterpret_cast<uint4*>(sA + blk * 8192 + row * 128 + pos * 16);
                 uint4 w = *pch;
                 uint32_t* u = reinterpret_cast<uint32_t*>(&w);
 #pragma unroll
                 for (int m = 0; m < 4; ++m)
-                    u[m] = pack_bf16(bf16lo(u[m]) * fj[cb + 2 * m], bf16hi(u[m]) * fj[cb + 2 * m + 1]);
+                    u[m] = pack_bf16(bf16lo(u[m]) * fv[2 * m], bf16hi(u[m]) * fv[2 * m + 1]);
                 *pch = w;
             }
             fence_async_smem();
             mbar_arrive(&bar_a[bs]);
         }
+        // the segment's total log decay (sum of Gamma over all its chunks) for the chains, if asked for
+        if (dec && tid < 128 && blockIdx.y == 0 && part == P - 1) dec[unit * K + k0 + tid] = carry;
     }
     mbar_wait(&bar_free[(nb - 1) % NS], ((nb - 1) / NS) & 1);
     tc_fence_after();
     if (warp < 8) {   // epilogue: warp w reads lanes 32 (w % 4) + [0, 32) (channels), columns 128 (w / 4) + [0, 128)
         const int kr = 32 * (warp & 3) + lane, cb = 128 * (warp >> 2);
-        float* out = S_loc + (unit * K + k0 + kr) * (size_t)V + v0 + cb;
+        float* out = S_loc + ((unit * P + part) * K + k0 + kr) * (size_t)V + v0 + cb;
         const uint32_t lb = (uint32_t)(32 * (warp & 3)) << 16;
 #pragma unroll 1
         for (int q = 0; q < 4; ++q) {
@@ -746,20 +762,21 @@ k_seg_summary(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ C
 bool seg_summary_ok(int K, int V) { return K % 128 == 0 && V % 256 == 0 && !getenv("GLA_SUMMARY_WALK"); }
 
 cudaError_t seg_summary(const CUtensorMap& mB, const CUtensorMap& mA, const float* stats, const int* flags, float* out,
-                        int K, int V, int Tv, int S, int units, bool adj, cudaStream_t st, bool skip_edge) {
+                        int K, int V, int Tv, int S, int units, bool adj, cudaStream_t st, bool skip_edge, int parts,
+                        float* dec) {
     cudaError_t e;
     const int skip = (skip_edge && S > 1) ? 1 : 0;
-    const dim3 grid(K / 128, V / 256, (unsigned)(units / S * (S - skip)));
+    const dim3 grid(K / 128, V / 256, (unsigned)(units / S * (S - skip) * parts));
     if (adj) {
         if ((e = cudaFuncSetAttribute(k_seg_summary<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)SumCfg::SMEM)))
             return e;
-        k_seg_summary<1><<<grid, 288, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S, skip);
+        k_seg_summary<1><<<grid, 288, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S, skip, parts, dec);
     } else {
         if ((e = cudaFuncSetAttribute(k_seg_summary<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)SumCfg::SMEM)))
             return e;
-        k_seg_summary<0><<<grid, 288, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S, skip);
+        k_seg_summary<0><<<grid, 288, SumCfg::SMEM, st>>>(mB, mA, stats, flags, out, K, V, Tv, S, skip, parts, dec);
     }
     return cudaGetLastError();
 }
@@ -772,7 +789,9 @@ size_t fwd2_ws(int B, int H, int T, int K, int V) {
     const size_t BH = (size_t)B * H, NC = T / CH;
     const int S = fwd_segments((int)BH, V, (int)NC);
     return al(BH * T * K * 2) * 2 + al(BH * T * 64 * 2) + al(BH * NC * 2 * K * 4) + al(BH * NC * 4) +
-           al(BH * T * K * 4) + al(n_anch(T) * BH * V * K * 2) + (S > 1 ? 2 * al(BH * S * K * V * 4) : 0);
+           al(BH * T * K * 4) + al(n_anch(T) * BH * V * K * 2) +
+           (S > 1 ? al(BH * S * K * V * 4) + al(BH * S * K * V * 4 * seg_parts((int)BH, K, V, (int)NC, S)) +
+                        al(BH * S * K * 4) : 0);
 }
 
 FwdSaved fwd2_saved(const void* ws, int B, int H, int T, int K, int V) {
@@ -805,6 +824,9 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     const int S = fwd_segments((int)BH, p.V, (int)NC);
     float* h0v = (float*)w; w += S > 1 ? al(BH * S * K * p.V * 4) : 0;   // segment-entry states (saved for bwd)
     float* slv = (float*)w;                                              // segment summaries / final states
+    const int SP = S > 1 && seg_summary_ok(K, p.V) ? seg_parts((int)BH, K, p.V, (int)NC, S) : 1;
+    w += S > 1 ? al(BH * S * K * p.V * 4 * seg_parts((int)BH, K, p.V, (int)NC, S)) : 0;
+    float* dec = S > 1 && seg_summary_ok(K, p.V) ? (float*)w : nullptr;  // per-segment log decays (summaries)
     CUtensorMap mQ, mK, mP, mV, mO, mA;
     cudaError_t e;
     if ((e = make_map_2d(&mQ, Qt, rows, K, true)) != cudaSuccess) return e;
@@ -844,7 +866,8 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     if (seg_summary_ok(K, p.V)) {
         // chunk-parallel summaries: one tensor-core contraction per (channel tile, value tile, segment)
         GLA_PROF("tc::fwd_state_summary", st);
-        if ((e = seg_summary(mV, mK, stats, flags, slv, K, p.V, Tv, S, (int)(BH * S), false, st, true)) != cudaSuccess)
+        if ((e = seg_summary(mV, mK, stats, flags, slv, K, p.V, Tv, S, (int)(BH * S), false, st, true, SP, dec)) !=
+            cudaSuccess)
             return e;
     } else {
         GLA_PROF("tc::fwd_state_summary", st);
@@ -852,7 +875,7 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
                                                                          slv, nullptr, Tv, p.V, 0);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if ((e = seg_chain_fwd(stats, p.h0, slv, h0v, (int)BH, S, (int)NC, K, p.V, st)) != cudaSuccess) return e;
+    if ((e = seg_chain_fwd(stats, p.h0, slv, h0v, (int)BH, S, (int)NC, K, p.V, st, SP, dec)) != cudaSuccess) return e;
     {
         GLA_PROF("tc::fwd_state", st);
         k_fwd_state<K><<<gv, StateCfg<K>::NTHR, StateCfg<K>::SMEM, st>>>(mQ, mK, mP, mV, mO, mA, stats, flags, h0v,
@@ -968,7 +991,7 @@ __device__ __forceinline__ float seg_decay(const float* stats, int bh, int s, in
 }
 __global__ void k_seg_chain_fwd(const float* __restrict__ stats, const float* __restrict__ h0,
                                 const float* __restrict__ S_loc, float* __restrict__ Hv, int BH, int S, int NC, int K,
-                                int V) {
+                                int V, int P, const float* __restrict__ dec) {
     const size_t n = (size_t)BH * K * (V / 4);
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n) return;
@@ -978,18 +1001,35 @@ __global__ void k_seg_chain_fwd(const float* __restrict__ stats, const float* __
     const size_t KV = (size_t)K * V, off = (size_t)k * V + v;
     float4 H = h0 ? *reinterpret_cast<const float4*>(h0 + bh * KV + off) : make_float4(0.f, 0.f, 0.f, 0.f);
     const int NCs = NC / S;
-    for (int s = 0; s < S; ++s) {
-        *reinterpret_cast<float4*>(Hv + ((size_t)bh * S + s) * KV + off) = H;
-        if (s + 1 < S) {
-            const float a = __expf(seg_decay(stats, bh, s, NCs, NC, K, k));
-            const float4 l = *reinterpret_cast<const float4*>(S_loc + ((size_t)bh * S + s) * KV + off);
-            H = make_float4(a * H.x + l.x, a * H.y + l.y, a * H.z + l.z, a * H.w + l.w);
+    // groups of 4 segments: the group's summaries and decays are loaded first (independent loads in flight), then
+    // the chain steps through them
+    for (int s0 = 0; s0 < S; s0 += 4) {
+        float4 L[4];
+        float A[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int s = s0 + u;
+            if (s + 1 < S) {
+                A[u] = __expf(dec ? dec[((size_t)bh * S + s) * K + k] : seg_decay(stats, bh, s, NCs, NC, K, k));
+                L[u] = *reinterpret_cast<const float4*>(S_loc + ((size_t)bh * S + s) * P * KV + off);
+                for (int pp = 1; pp < P; ++pp) {   // the summary's token-range partials, in part order
+                    const float4 m = *reinterpret_cast<const float4*>(S_loc + (((size_t)bh * S + s) * P + pp) * KV + off);
+                    L[u] = make_float4(L[u].x + m.x, L[u].y + m.y, L[u].z + m.z, L[u].w + m.w);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int s = s0 + u;
+            if (s < S) *reinterpret_cast<float4*>(Hv + ((size_t)bh * S + s) * KV + off) = H;
+            if (s + 1 < S)
+                H = make_float4(A[u] * H.x + L[u].x, A[u] * H.y + L[u].y, A[u] * H.z + L[u].z, A[u] * H.w + L[u].w);
         }
     }
 }
 __global__ void k_seg_chain_bwd(const float* __restrict__ stats, const float* __restrict__ dfinal,
                                 const float* __restrict__ dh_loc, float* __restrict__ dFv, int BH, int S, int NC, int K,
-                                int V) {
+                                int V, int P, const float* __restrict__ dec) {
     const size_t n = (size_t)BH * K * (V / 4);
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n) return;
@@ -999,29 +1039,45 @@ __global__ void k_seg_chain_bwd(const float* __restrict__ stats, const float* __
     const size_t KV = (size_t)K * V, off = (size_t)k * V + v;
     float4 F = dfinal ? *reinterpret_cast<const float4*>(dfinal + bh * KV + off) : make_float4(0.f, 0.f, 0.f, 0.f);
     const int NCs = NC / S;
-    for (int s = S - 1; s >= 0; --s) {
-        *reinterpret_cast<float4*>(dFv + ((size_t)bh * S + s) * KV + off) = F;
-        if (s > 0) {
-            const float a = __expf(seg_decay(stats, bh, s, NCs, NC, K, k));
-            const float4 l = *reinterpret_cast<const float4*>(dh_loc + ((size_t)bh * S + s) * KV + off);
-            F = make_float4(a * F.x + l.x, a * F.y + l.y, a * F.z + l.z, a * F.w + l.w);
+    for (int s0 = S - 1; s0 >= 0; s0 -= 4) {   // groups of 4 segments, loads first (see k_seg_chain_fwd)
+        float4 L[4];
+        float A[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int s = s0 - u;
+            if (s > 0) {
+                A[u] = __expf(dec ? dec[((size_t)bh * S + s) * K + k] : seg_decay(stats, bh, s, NCs, NC, K, k));
+                L[u] = *reinterpret_cast<const float4*>(dh_loc + ((size_t)bh * S + s) * P * KV + off);
+                for (int pp = 1; pp < P; ++pp) {
+                    const float4 m = *reinterpret_cast<const float4*>(dh_loc + (((size_t)bh * S + s) * P + pp) * KV + off);
+                    L[u] = make_float4(L[u].x + m.x, L[u].y + m.y, L[u].z + m.z, L[u].w + m.w);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int s = s0 - u;
+            if (s >= 0) *reinterpret_cast<float4*>(dFv + ((size_t)bh * S + s) * KV + off) = F;
+            if (s > 0)
+                F = make_float4(A[u] * F.x + L[u].x, A[u] * F.y + L[u].y, A[u] * F.z + L[u].z, A[u] * F.w + L[u].w);
         }
     }
 }
 }  // namespace
 
 cudaError_t seg_chain_fwd(const float* stats, const float* h0, const float* S_loc, float* Hv, int BH, int S, int NC,
-                          int K, int V, cudaStream_t st) {
+                          int K, int V, cudaStream_t st, int parts, const float* dec) {
     const size_t n = (size_t)BH * K * (V / 4);
     GLA_PROF("tc::seg_chain", st);
-    k_seg_chain_fwd<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stats, h0, S_loc, Hv, BH, S, NC, K, V);
+    k_seg_chain_fwd<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stats, h0, S_loc, Hv, BH, S, NC, K, V, parts, dec);
     return cudaGetLastError();
 }
 cudaError_t seg_chain_bwd(const float* stats, const float* dfinal, const float* dh_loc, float* dFv, int BH, int S,
-                          int NC, int K, int V, cudaStream_t st) {
+                          int NC, int K, int V, cudaStream_t st, int parts, const float* dec) {
     const size_t n = (size_t)BH * K * (V / 4);
     GLA_PROF("tc::seg_chain", st);
-    k_seg_chain_bwd<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stats, dfinal, dh_loc, dFv, BH, S, NC, K, V);
+    k_seg_chain_bwd<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stats, dfinal, dh_loc, dFv, BH, S, NC, K, V, parts,
+                                                                 dec);
     return cudaGetLastError();
 }
 }  // namespace tc
