@@ -48,10 +48,10 @@ bool seg_summary_ok(int K, int V);
 bool kwalk_ok(int K, int V);
 cudaError_t dq_kwalk(int K, int V, const CUtensorMap& mK, const CUtensorMap& mDP, const CUtensorMap& mV,
                      const CUtensorMap& mD, const float* stats, const float* h0, const float* dfinal, float* dq32,
-                     float* stdot, const int* flag, int T, int units, cudaStream_t st);
+                     float* stdot, const int* flag, const int* cflags, int T, int units, cudaStream_t st);
 cudaError_t dk_kwalk(int K, int V, const CUtensorMap& mQ, const CUtensorMap& mDP, const CUtensorMap& mD,
                      const CUtensorMap& mV, const float* stats, const float* dfinal, float* dk32, const int* flag,
-                     int T, int units, cudaStream_t st);
+                     const int* cflags, int T, int units, cudaStream_t st);
 // skip_edge (segment split only): the last segment's summary (adj = false) / the first one's (adj = true) is not
 // computed -- the chains never read it.
 cudaError_t seg_summary(const CUtensorMap& mB, const CUtensorMap& mA, const float* stats, const int* flags, float* out,

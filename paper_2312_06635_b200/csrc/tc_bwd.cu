@@ -84,9 +84,104 @@ struct RedCfg {
     static constexpr uint32_t OFF_Q = 2 * NQ * QT;
     static constexpr uint32_t GT = 64 * 64 * sizeof(TG);                 // log alpha tile bytes
     static constexpr uint32_t STAGE = OFF_Q + 2 * TILE + GT;
-    static constexpr int NS = 2 * STAGE + 64 * 65 * 4 + 1024 <= 232448 ? 2 : 1;
-    static constexpr uint32_t SMEM = NS * STAGE + 1024;
+    static constexpr uint32_t EX = NQ32 ? 3 * 64 * 68 * 4 : 0;   // exact chunks: alpha, dP, dP^T ([64][68] fp32 each)
+    static constexpr int NS = 2 * STAGE + EX + 64 * 65 * 4 + 1024 <= 232448 ? 2 : 1;
+    static constexpr uint32_t OFF_EX = NS * STAGE;
+    static constexpr uint32_t SMEM = NS * STAGE + EX + 1024;
 };
+
+// The exact intra-chunk terms of k_bwd_reduce_tma for one flagged chunk (see there), by the reduce's 256 compute
+// threads: thread (rows 4 (tid / 16) + [0, 4), channels 4 (tid % 16) + [0, 4)) runs both sums for its 4 x 4 block,
+// so each step's shared loads (alpha and k or q of one row: 4 channels each; dP of 4 rows: one float4) feed 16
+// terms.  In: the staged q / k tiles (SW128 bf16 [64][64]), al = alpha, dp = dP, dpT = dP^T (fp32 [64][68]).
+// Out (after a barrier, so every read of al / dp is done): al <- the dq terms, dp <- the dk terms, [t][channel].
+// Not inlined: its registers stay out of the reduce's common path.
+__device__ __noinline__ void exact_intra(const uint8_t* qt, const uint8_t* kt, float (*al)[68], float (*dp)[68],
+                                         const float (*dpT)[68]) {
+    const int tid = threadIdx.x, t0 = 4 * (tid >> 4), c0 = 4 * (tid & 15);
+    auto ld4 = [&](const uint8_t* tile, int u) {   // 4 bf16 channels [c0, c0 + 4) of row u of a SW128 tile
+        const uint2 x = *reinterpret_cast<const uint2*>(tile + u * 128 + ((((c0 >> 3) ^ (u & 7))) << 4) + (c0 & 7) * 2);
+        return make_float4(bf16lo(x.x), bf16hi(x.x), bf16lo(x.y), bf16hi(x.y));
+    };
+    auto ld_al = [&](int u) { return *reinterpret_cast<const float4*>(&al[u][c0]); };
+    float2 w[4][2], aq[4][2], ak[4][2];   // [row][channel pair]
+    auto step = [&](float4 xv, float4 d4, float4 a4, bool upd, float2 (&acc)[4][2]) {   // all 4 rows active
+        const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (upd) { w[r][0] = mul2(w[r][0], make_float2(a4.x, a4.y)); w[r][1] = mul2(w[r][1], make_float2(a4.z, a4.w)); }
+            const float2 p2 = make_float2(dv[r], dv[r]);
+            acc[r][0] = fma2(mul2(p2, make_float2(xv.x, xv.y)), w[r][0], acc[r][0]);
+            acc[r][1] = fma2(mul2(p2, make_float2(xv.z, xv.w)), w[r][1], acc[r][1]);
+        }
+    };
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) { w[r][h] = make_float2(1.f, 1.f); aq[r][h] = make_float2(0.f, 0.f); }
+    // dq_t = sum_{s <= t} dP[t][s] k_s e^{b_t - b_s}: s from t0 + 3 down; row t joins at s = t with w = 1, and
+    // w_t <- w_t alpha_{s+1} for s < t.  The ragged head (s >= t0: rows joining) first, then the rest.
+#pragma unroll
+    for (int j = 3; j >= 0; --j) {
+        const int s2 = t0 + j;
+        const float4 kv = ld4(kt, s2), d4 = *reinterpret_cast<const float4*>(&dpT[s2][t0]);
+        const float4 a4 = j < 3 ? ld_al(s2 + 1) : make_float4(1.f, 1.f, 1.f, 1.f);
+        const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (r < j) continue;
+            if (r > j) { w[r][0] = mul2(w[r][0], make_float2(a4.x, a4.y)); w[r][1] = mul2(w[r][1], make_float2(a4.z, a4.w)); }
+            const float2 p2 = make_float2(dv[r], dv[r]);
+            aq[r][0] = fma2(mul2(p2, make_float2(kv.x, kv.y)), w[r][0], aq[r][0]);
+            aq[r][1] = fma2(mul2(p2, make_float2(kv.z, kv.w)), w[r][1], aq[r][1]);
+        }
+    }
+#pragma unroll 1
+    for (int s2 = t0 - 1; s2 >= 0; --s2)
+        step(ld4(kt, s2), *reinterpret_cast<const float4*>(&dpT[s2][t0]), ld_al(s2 + 1), true, aq);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) { w[r][h] = make_float2(1.f, 1.f); ak[r][h] = make_float2(0.f, 0.f); }
+    // dk_t = sum_{u >= t} dP[u][t] q_u e^{b_u - b_t}: u from t0 up; row t joins at u = t, w_t <- w_t alpha_u for u > t
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const int u2 = t0 + j;
+        const float4 qv = ld4(qt, u2), d4 = *reinterpret_cast<const float4*>(&dp[u2][t0]);
+        const float4 a4 = j > 0 ? ld_al(u2) : make_float4(1.f, 1.f, 1.f, 1.f);
+        const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (r > j) continue;
+            if (r < j) { w[r][0] = mul2(w[r][0], make_float2(a4.x, a4.y)); w[r][1] = mul2(w[r][1], make_float2(a4.z, a4.w)); }
+            const float2 p2 = make_float2(dv[r], dv[r]);
+            ak[r][0] = fma2(mul2(p2, make_float2(qv.x, qv.y)), w[r][0], ak[r][0]);
+            ak[r][1] = fma2(mul2(p2, make_float2(qv.z, qv.w)), w[r][1], ak[r][1]);
+        }
+    }
+    {   // u = t0 + 3: row t0 + 3 joins (w = 1), the others decay
+        const int u2 = t0 + 3;
+        const float4 qv = ld4(qt, u2), d4 = *reinterpret_cast<const float4*>(&dp[u2][t0]), a4 = ld_al(u2);
+        const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (r < 3) { w[r][0] = mul2(w[r][0], make_float2(a4.x, a4.y)); w[r][1] = mul2(w[r][1], make_float2(a4.z, a4.w)); }
+            const float2 p2 = make_float2(dv[r], dv[r]);
+            ak[r][0] = fma2(mul2(p2, make_float2(qv.x, qv.y)), w[r][0], ak[r][0]);
+            ak[r][1] = fma2(mul2(p2, make_float2(qv.z, qv.w)), w[r][1], ak[r][1]);
+        }
+    }
+#pragma unroll 1
+    for (int u2 = t0 + 4; u2 < 64; ++u2)
+        step(ld4(qt, u2), *reinterpret_cast<const float4*>(&dp[u2][t0]), ld_al(u2), true, ak);
+    named_bar_sync(1, 256);   // every read of al / dp done
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        *reinterpret_cast<float4*>(&al[t0 + r][c0]) = make_float4(aq[r][0].x, aq[r][0].y, aq[r][1].x, aq[r][1].y);
+        *reinterpret_cast<float4*>(&dp[t0 + r][c0]) = make_float4(ak[r][0].x, ak[r][0].y, ak[r][1].x, ak[r][1].y);
+    }
+    named_bar_sync(1, 256);
+}
 
 template <int K, int NVT, typename TG, int NQ32>
 __global__ void __launch_bounds__(288, 1)
@@ -94,7 +189,14 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                  const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmDQP,
                  const __grid_constant__ CUtensorMap tmDKP, const float* __restrict__ stdot, int n_stdot,
                  __nv_bfloat16* __restrict__ dq, __nv_bfloat16* __restrict__ dk, float* __restrict__ dg,
-                 const float* __restrict__ cpart, const int* __restrict__ flag, int T, int BH) {
+                 const float* __restrict__ cpart, const int* __restrict__ flag, int T, int BH,
+                 const int* __restrict__ cflags, const __nv_bfloat16* __restrict__ dPm) {
+    // cflags / dPm (NQ32 only, else NULL): the forward's per-chunk exact-path flags and dP = (dO V^T) (.) M.  On a
+    // flagged chunk the walks delivered the inter terms in the r = 0 frame (dq = e^{b} (.) X_q, dk = e^{Gamma - b}
+    // (.) X_k) and no intra term; the intra terms are formed here in fp32 with decay factors <= 1 built as running
+    // products of alpha (no exponent of a difference of cumsums, no overflow whatever the gates):
+    //     dq_t += sum_{s <= t} dP[t][s] k_s e^{b_t - b_s},   dk_t += sum_{u >= t} dP[u][t] q_u e^{b_u - b_t}.
+    // Thread (row t, 16 channels) runs both sums (t + 1 and 64 - t terms: every thread 65 steps).
     using RC = RedCfg<NVT, TG, NQ32>;
     constexpr int NQ = RC::NQ;
     constexpr uint32_t ODK = RC::OFF_DK, OQ = RC::OFF_Q;
@@ -103,6 +205,9 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     uint8_t* sm = smem_align1k(smem_raw);
     __shared__ float sb[64][65];      // g -> b (chunk-local cumsum), then x -> suffix sums
     __shared__ float carry_s[64];
+    float (*al)[68] = reinterpret_cast<float (*)[68]>(sm + RC::OFF_EX);                    // exact chunks: alpha
+    float (*sdp)[68] = reinterpret_cast<float (*)[68]>(sm + RC::OFF_EX + 64 * 68 * 4);     // exact chunks: dP
+    float (*sdpT)[68] = reinterpret_cast<float (*)[68]>(sm + RC::OFF_EX + 2 * 64 * 68 * 4);   // and dP^T
     __shared__ uint64_t bar[2], empty[2];
     const int tid = threadIdx.x, t = tid >> 2, cg = tid & 3;
     const int m0 = blockIdx.x * 64, bh = blockIdx.y;
@@ -165,7 +270,14 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         }
         carry_s[tid] = c0;
     }
+    __shared__ int slow_s[ANCH];      // exact-path flags of this segment's chunks (read alongside the carries)
+    if (NQ32 && tid >= 64 && tid < 64 + ANCH)
+        slow_s[tid - 64] = (cflags && i_lo + tid - 64 <= i_hi) ? cflags[(size_t)bh * NC + i_lo + tid - 64] : 0;
     named_bar_sync(1, 256);
+    uint32_t slow_bits = 0u;
+    if (NQ32)
+#pragma unroll
+        for (int c = 0; c < ANCH; ++c) slow_bits |= (slow_s[c] ? 1u : 0u) << c;
     uint32_t uses[2] = {0u, 0u};
     // byte offset of 8 consecutive bf16 channels [c, c+8) of row t in a SW128 [64][64] bf16 tile
     auto bf_off = [&](int c) { return (uint32_t)(t * 128 + ((((c >> 3) ^ (t & 7))) << 4)); };
@@ -179,6 +291,7 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             carry_s[tid] = c0;
         }
         mbar_wait(&bar[sidx], (uses[sidx]++) & 1);
+        const bool slow = NQ32 && ((slow_bits >> (i - i_lo)) & 1u);
         // (a1) chunk-local cumsum: stage g, one thread per channel scans the 64 rows
         {
             const uint8_t* gt = st + OQ + 2 * RC::TILE;
@@ -204,6 +317,23 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             }
 #pragma unroll
             for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = gv[u];
+            if (NQ32 && slow) {
+#pragma unroll
+                for (int u = 0; u < 16; u += 4)
+                    *reinterpret_cast<float4*>(&al[t][16 * cg + u]) =
+                        make_float4(ex2f(gv[u] * L2E), ex2f(gv[u + 1] * L2E), ex2f(gv[u + 2] * L2E), ex2f(gv[u + 3] * L2E));
+                const uint4* dr = reinterpret_cast<const uint4*>(dPm + (head_row + (size_t)i * CH + t) * 64 + 16 * cg);
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const uint4 x = __ldg(dr + c);
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const int cc = 16 * cg + 8 * c + 2 * w;
+                        sdp[t][cc] = sdpT[cc][t] = bf16lo(word(x, w));
+                        sdp[t][cc + 1] = sdpT[cc + 1][t] = bf16hi(word(x, w));
+                    }
+                }
+            }
         }
         named_bar_sync(1, 256);
         if (tid < 64) {
@@ -211,7 +341,19 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             for (int r = 0; r < CH; ++r) { run += sb[r][tid]; sb[r][tid] = run; }
         }
         named_bar_sync(1, 256);
-        float x[16], dqv[16], dkv[16];
+        float x[16], dqv[16], dkv[16], iqr[16], ikr[16];   // exact-path intra terms (zero on guarded chunks)
+#pragma unroll
+        for (int u = 0; u < 16; ++u) { iqr[u] = 0.f; ikr[u] = 0.f; }
+        if (NQ32 && slow) {   // (all 256 threads: the call synchronises them)
+            exact_intra(st + OQ, st + OQ + RC::TILE, al, sdp, sdpT);
+#pragma unroll
+            for (int u = 0; u < 16; u += 4) {
+                const float4 a = *reinterpret_cast<const float4*>(&al[t][16 * cg + u]);
+                const float4 b = *reinterpret_cast<const float4*>(&sdp[t][16 * cg + u]);
+                iqr[u] = a.x; iqr[u + 1] = a.y; iqr[u + 2] = a.z; iqr[u + 3] = a.w;
+                ikr[u] = b.x; ikr[u + 1] = b.y; ikr[u + 2] = b.z; ikr[u + 3] = b.w;
+            }
+        }
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             const uint32_t o = bf_off(16 * cg + 8 * c);
@@ -252,8 +394,10 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             for (int w = 0; w < 8; ++w) {
                 const int u = 8 * c + w;
                 const float b = sb[t][16 * cg + u], r = sb[CH / 2 - 1][16 * cg + u];
-                dqv[u] = sq[w] * ex2f((b - r) * L2E);
-                dkv[u] = sk[w] * ex2f((r - b) * L2E);
+                // exact-path chunk: the r = 0 frame for dq, r = Gamma for dk, plus the exact intra terms
+                const float rq = (NQ32 && slow) ? 0.f : r, rk = (NQ32 && slow) ? sb[CH - 1][16 * cg + u] : r;
+                dqv[u] = fmaf(sq[w], ex2f((b - rq) * L2E), iqr[u]);
+                dkv[u] = fmaf(sk[w], ex2f((rk - b) * L2E), ikr[u]);
                 const float qf = (w & 1) ? bf16hi(word(qv, w >> 1)) : bf16lo(word(qv, w >> 1));
                 const float kf = (w & 1) ? bf16hi(word(kv, w >> 1)) : bf16lo(word(kv, w >> 1));
                 x[u] = qf * dqv[u] - kf * dkv[u];
@@ -492,7 +636,8 @@ k_bwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
 // k_bwd_dp: dP = (dO V^T) (.) M per chunk over the full V, for the backward that reuses a forward's saved
 // Q~, K~, P (gla_chunk_bwd_saved).  Persistent; warp 0 streams 64-column dO / V boxes through a 4-stage TMA
 // ring, warp 1 issues the M=64 N=64 MMAs, warps 2-5 drain the accumulator (causal mask, bf16, TMA store).
-// It also ORs the forward's per-chunk exact-path flags into the backward's flag (R9).
+// It also ORs the forward's per-chunk exact-path flags into the backward's flag (R9) when given them (the
+// V-tiled walks have no exact path; the K-tiled ones and the reduce do, so the K-tiled backward passes NULL).
 constexpr int DP_NSTG = 4;
 __global__ void __launch_bounds__(192, 1)
 k_bwd_dp(const __grid_constant__ CUtensorMap tmDP, const __grid_constant__ CUtensorMap tmV,
@@ -523,7 +668,7 @@ k_bwd_dp(const __grid_constant__ CUtensorMap tmDP, const __grid_constant__ CUten
             uint32_t cnt = 0;
             for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
                 const int row = (int)((size_t)(item / NC) * T + (size_t)(item % NC) * CH);
-                any |= fflags[item];
+                if (fflags) any |= fflags[item];
                 for (int kb = 0; kb < NKB; ++kb, ++cnt) {
                     const uint32_t s2 = cnt % DP_NSTG, use = cnt / DP_NSTG;
                     if (use > 0) mbar_wait(&empty[s2], (use - 1) & 1);
@@ -858,8 +1003,11 @@ k_bwd_dkv3(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmD,
            const float* __restrict__ stats, const float* __restrict__ dfinal, __nv_bfloat16* __restrict__ dv_out,
            __nv_bfloat16* __restrict__ dkp, float* __restrict__ dh0, const __nv_bfloat16* __restrict__ anch,
-           float* __restrict__ cpart, const int* __restrict__ flag, int T, int V) {
+           float* __restrict__ cpart, const int* __restrict__ flag, int T, int V, const int* __restrict__ cflags) {
     constexpr int emit = EMIT;   // compile-time: the unused roles' code is removed
+    // cflags (emit == 2 only, else NULL): the forward's per-chunk exact-path flags; a flagged chunk's pass takes the
+    // r = 0 frame of its exact operands (Q~ = q e^{b}, K~ = k e^{Gamma - b}): dSB = bf16(dH_{i+1}) (factor
+    // e^{pend}), Z <- dH_{i+1} e^{Gamma} before the update, pending 0 (see k_bwd_kwalk).
     // emit == 0: adjoint-only walk (segment summaries dh_loc): only the Z updates run and only dh0 is written.
     // emit == 2: dv, the anchor carries and dh0 but no dk (dk comes from the K-tiled dk walk, tc_kwalk.cu).
     // (Keeping dSB in TMEM, in the then free dk^T columns, as the A operand of TS-mode dv MMAs measured slower:
@@ -953,22 +1101,32 @@ k_bwd_dkv3(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         }
         tmem_wait_st();
         float st_r = 0.f, st_G = 0.f;          // per-chunk statistics, one chunk ahead
+        int st_slow = 0;
         if (tid < K) {
             st_r = stats[((size_t)bh * NC + NC - 1) * 2 * K + tid];
             st_G = stats[((size_t)bh * NC + NC - 1) * 2 * K + K + tid];
+            st_slow = cflags ? cflags[(size_t)bh * NC + NC - 1] : 0;
         }
         named_bar_sync(1, DC::NST);
         for (int i = NC - 1; i >= 0; --i) {
             const int j = NC - 1 - i;
             if (tid < K) {   // dSB = bf16(dH_{i+1} e^{Gamma - r}); Z <- same; next pending = r
                 const float r_ = st_r, G_ = st_G;
+                const bool slow = st_slow != 0;
                 if (i > 0) {
                     st_r = stats[((size_t)bh * NC + i - 1) * 2 * K + tid];
                     st_G = stats[((size_t)bh * NC + i - 1) * 2 * K + K + tid];
+                    st_slow = cflags ? cflags[(size_t)bh * NC + i - 1] : 0;
                 }
-                fsb[tid] = ex2f((pend[tid] + G_ - r_) * L2E);
-                fy[tid] = fsb[tid];
-                pend[tid] = r_;
+                if (!slow) {
+                    fsb[tid] = ex2f((pend[tid] + G_ - r_) * L2E);
+                    fy[tid] = fsb[tid];
+                    pend[tid] = r_;
+                } else {     // exact-path chunk: dSB = bf16(dH_{i+1}), Z <- dH_{i+1} e^{Gamma}, pending 0
+                    fsb[tid] = ex2f(pend[tid] * L2E);
+                    fy[tid] = ex2f((pend[tid] + G_) * L2E);
+                    pend[tid] = 0.f;
+                }
             }
             named_bar_sync(1, DC::NST);        // fsb / fy visible
             const int bd = i + 1;              // exact d log alpha carry at boundary bd over this V tile
@@ -1285,6 +1443,9 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         return e;
     if ((e = cudaFuncSetAttribute(k_bwd_dkv3<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Dkv3Cfg<K>::SMEM)))
         return e;
+    // With the forward's anchors the walks are the K-tiled ones (tc_kwalk.cu): dq and dk leave them complete (no
+    // V-tile partials), and they and the reduce follow the forward's exact path on flagged chunks.
+    const bool kw = saved_anch && kwalk_ok(K, p.V);
     if (saved) {
         GLA_PROF("tc::bwd_dp", st);
         const int nitems = NC * BH;
@@ -1292,7 +1453,8 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         if ((e = cudaFuncSetAttribute(k_bwd_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess)
             return e;
         const int grid_dp = nitems < 2 * num_sms() ? nitems : 2 * num_sms();
-        k_bwd_dp<<<(unsigned)grid_dp, 192, smem, st>>>(mDP, mV, mD, fflags, flag, p.T, p.V, NC, nitems);
+        k_bwd_dp<<<(unsigned)grid_dp, 192, smem, st>>>(mDP, mV, mD, kw ? nullptr : fflags, flag, p.T, p.V, NC,
+                                                        nitems);
     } else {
         GLA_PROF("tc::bwd_prep", st);
         const int nitems = NC * BH;
@@ -1314,7 +1476,7 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
             GLA_PROF("tc::bwd_dstate_summary", st);
             k_bwd_dkv3<K, 0><<<grid, Dkv3Cfg<K>::NTHR, Dkv3Cfg<K>::SMEM, st>>>(
                 mQ, mK, mP, mDP, mV, mD, stats, nullptr, (__nv_bfloat16*)p.dv, dkp, dhv, nullptr, cpart, flag, Tv,
-                p.V);
+                p.V, nullptr);
         }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if ((e = seg_chain_bwd(stats, p.dfinal, dhv, dFv, BH, S, NC, K, p.V, st, SP,
@@ -1335,16 +1497,13 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         if ((e = cudaEventRecord(ev_in, st)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(sq, ev_in, 0)) != cudaSuccess) return e;
     }
-    // With the forward's anchors the dq walk is the K-tiled one (tc_kwalk.cu): dq leaves it complete (no V-tile
-    // partials); the reduce then only sums the dk partials and forms d log alpha.
-    const bool kw = saved_anch && kwalk_ok(K, p.V);
     float* dq32 = reinterpret_cast<float*>(dqp);   // (V/256) fp32 partials: the same bytes as NVT bf16 ones
     float* dk32 = reinterpret_cast<float*>(dkp);
     {
         GLA_PROF("tc::bwd_dq", sq);
         if (kw) {
-            if ((e = dq_kwalk(K, p.V, mK, mDP, mV, mD, stats, h0w, dfin, dq32, dfin ? stdot : nullptr, flag, Tv,
-                              BHv, sq)) != cudaSuccess)
+            if ((e = dq_kwalk(K, p.V, mK, mDP, mV, mD, stats, h0w, dfin, dq32, dfin ? stdot : nullptr, flag, fflags,
+                              Tv, BHv, sq)) != cudaSuccess)
                 return e;
         } else {
             k_bwd_dq3<K><<<grid, Dq3Cfg<K>::NTHR, Dq3Cfg<K>::SMEM, sq>>>(mK, mDP, mV, mD, stats, h0w, dfin, dqp,
@@ -1354,7 +1513,8 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
     }
     if (kw) {
         GLA_PROF("tc::bwd_dk", st);
-        if ((e = dk_kwalk(K, p.V, mQ, mDP, mD, mV, stats, dfin, dk32, flag, Tv, BHv, st)) != cudaSuccess) return e;
+        if ((e = dk_kwalk(K, p.V, mQ, mDP, mD, mV, stats, dfin, dk32, flag, fflags, Tv, BHv, st)) != cudaSuccess)
+            return e;
     }
     // K-tiled walks: the dv walk runs on a second side stream, concurrently with the dq and dk walks (three
     // independent 1-CTA-per-SM kernels of ~256 CTAs each fill the 148 SMs better together than one by one).
@@ -1371,11 +1531,11 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         if (kw)
             k_bwd_dkv3<K, 2><<<grid, Dkv3Cfg<K>::NTHR, Dkv3Cfg<K>::SMEM, sv>>>(
                 mQ, mK, mP, mDP, mV, mD, stats, dfin, (__nv_bfloat16*)p.dv, dkp, dh0w, saved_anch ? saved_anch : anch,
-                cpart, flag, Tv, p.V);
+                cpart, flag, Tv, p.V, fflags);
         else
             k_bwd_dkv3<K, 1><<<grid, Dkv3Cfg<K>::NTHR, Dkv3Cfg<K>::SMEM, sv>>>(
                 mQ, mK, mP, mDP, mV, mD, stats, dfin, (__nv_bfloat16*)p.dv, dkp, dh0w, saved_anch ? saved_anch : anch,
-                cpart, flag, Tv, p.V);
+                cpart, flag, Tv, p.V, nullptr);
     }
     if (sv != st) {
         if ((e = cudaEventRecord(ev_dv, sv)) != cudaSuccess) return e;
@@ -1425,7 +1585,8 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
                                       (int)RedCfg<N, TG, NQ32>::SMEM)) != cudaSuccess)                              \
             return e;                                                                                               \
         k_bwd_reduce_tma<K, N, TG, NQ32><<<rg, 288, RedCfg<N, TG, NQ32>::SMEM, st>>>(                               \
-            mQr, mKr, mGr, mDQP, mDKP, sd, NQ32 ? p.V / 256 : NVT, dq_, dk_, p.dg, cpart, flag, Tv, BHv);            \
+            mQr, mKr, mGr, mDQP, mDKP, sd, NQ32 ? p.V / 256 : NVT, dq_, dk_, p.dg, cpart, flag, Tv, BHv,             \
+            NQ32 ? fflags : nullptr, NQ32 ? dPm : nullptr);                                                         \
         break;
         if (kw) {   // one combined fp32 dq and dk per element (the walks sum the value halves)
             switch (NVT) {

@@ -13,8 +13,10 @@
 // Compared with one fused kernel per (b,h) x V tile (the first design, in git history), the operand
 // construction and P run once per chunk instead of once per V tile (4x at d_v' = 512), at the price of writing /
 // re-reading Q~hi, K~hi and P (2.1 KB per token-head at K = 256).  Exact path for chunks failing the
-// factorisation guard: prep computes P in fp32 log space with factors <= 1 and Q~ = q e^{b}, K~ = k e^{Gamma-b};
-// the state kernel applies the decay before the update.
+// factorisation guard: Q~ = q e^{b}, K~ = k e^{Gamma-b} (every factor <= 1; the state kernel applies the decay
+// before the update) and P from the paper's per-sub-chunk-pair normalisers taken down to single
+// tokens: six levels of sub-chunk pairs, each one stacked hi/lo tensor-core product whose two factors are <= 1
+// (see k_fwd_prep).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cstdio>
@@ -44,9 +46,167 @@ struct PrepCfg {
     static constexpr uint32_t OP = KB * 16384;          // [KB][128 rows: hi | lo][128 B]
     static constexpr uint32_t OFF_Q = 0, OFF_K = OP, OFF_P = 2 * OP;       // P [64 t][128 B]
     static constexpr uint32_t OFF_X = OFF_P + 8192;     // exchange [64][64] fp32 and gtot
-    static constexpr uint32_t SMEM = OFF_X + 16384 + 1024;
+    static constexpr uint32_t OFF_B = OFF_X + 16384;    // exact path: b at each row group's last row [RG][K], diag [64]
+    static constexpr uint32_t SMEM = OFF_B + Tl::RG * K * 4 + 256 + 1024;
     static_assert(Tl::RG * K * 4 <= 16384, "gtot fits the exchange buffer");
 };
+
+// The exact-path P of k_fwd_prep, for each of the calling CTA's items whose chunk failed the factorisation guard
+// (R9).  P[t][s] = sum_k q_tk k_sk e^{b_tk - b_sk}, s <= t, with the paper's per-pair normalisers
+// on a binary hierarchy of sub-chunks taken down to single tokens: at level h (half size 32, 16, ..., 1) the
+// chunk splits into groups of 2h rows, an earlier half E and a later half F with normaliser c = the last row of E,
+// and for t in F, s in E of the same group
+//     P[t][s] = sum_k (q_tk e^{b_tk - b_ck}) (k_sk e^{b_ck - b_sk}),
+// both factors <= 1 whatever the gates.  Every pair s < t lies in exactly one level's F x E block of one group
+// (the level where t and s first separate); the diagonal P[t][t] = q_t . k_t needs no factor.  A level is the
+// product of Q_h (rows in F scaled, rows in E zero) and K_h (rows in E scaled, rows in F zero); two levels share
+// one 128 x 128 x K tensor-core MMA (level A on operand rows 0-63, level B on rows 64-127; the diagonal blocks of
+// the product are the two levels), so the six levels take three MMA rounds.  Operands are bf16 (no hi/lo split:
+// every factor is <= 1, and P is stored in bf16).  Returns the bar parity.
+template <int K, typename TG>
+__device__ __noinline__ uint32_t exact_P_phase(const CUtensorMap* tmP, const __nv_bfloat16* __restrict__ q,
+                                               const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g,
+                                               const int* __restrict__ flags, int T, int NC, int nitems, uint8_t* sm,
+                                               uint32_t tP, uint64_t* barp, uint32_t phase) {
+    using Cfg = PrepCfg<K>;
+    using Tl = typename Cfg::Tl;
+    uint8_t* sQ = sm + Cfg::OFF_Q;
+    uint8_t* sK = sm + Cfg::OFF_K;
+    uint8_t* sP = sm + Cfg::OFF_P;
+    float* gtot = reinterpret_cast<float*>(sm + Cfg::OFF_X);
+    float* bnd = reinterpret_cast<float*>(sm + Cfg::OFF_B);
+    float* diag = bnd + Tl::RG * K;
+    uint64_t& bar = *barp;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int oc = tid % Tl::NOCT, rg = tid / Tl::NOCT;
+    const int ch0 = 8 * oc, row0 = rg * Tl::RPG;
+    const int blk = ch0 >> 6, col = ch0 & 63;
+    uint8_t* qb = sQ + blk * 16384;
+    uint8_t* kb = sK + blk * 16384;
+    const int lq = warp & 3, half = warp >> 2;
+    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
+    const int vrow = 32 * lq + lane;
+    ChunkRegs<K> R;
+    for (int it2 = blockIdx.x; it2 < nitems; it2 += gridDim.x) {
+        if (!flags[it2]) continue;   // (written by this CTA in the main loop; ordered by its barriers)
+        const int chunk = it2 % NC, bh = it2 / NC;
+        const size_t crow = (size_t)bh * T + (size_t)chunk * CH;
+        load_chunk<K, TG, true, true>(R, q, k, g, crow, row0, ch0);
+        if (tid == 0) tma_store_wait_read();    // earlier stores have read sQ / sK / sP
+        float2 off[4], rr[4], Gm[4];
+        chunk_cumsum<K>(R, gtot, rg, ch0, off, rr, Gm);
+#pragma unroll
+        for (int r = 0; r < Tl::RPG; ++r)       // R.g <- b (chunk-local cumsum)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) R.g[r][p] = add2(R.g[r][p], off[p]);
+        {   // b at this thread's last row (the normaliser rows of the coarse levels) and the diagonal
+            float4* bb = reinterpret_cast<float4*>(bnd + rg * K + ch0);
+            const int rl = Tl::RPG - 1;
+            bb[0] = make_float4(R.g[rl][0].x, R.g[rl][0].y, R.g[rl][1].x, R.g[rl][1].y);
+            bb[1] = make_float4(R.g[rl][2].x, R.g[rl][2].y, R.g[rl][3].x, R.g[rl][3].y);
+#pragma unroll
+            for (int r = 0; r < Tl::RPG; ++r) {
+                float d = 0.f;
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const float2 qv = unpack2(word(R.q[r], p)), kv = unpack2(word(R.k[r], p));
+                    d = fmaf(qv.x, kv.x, fmaf(qv.y, kv.y, d));
+                }
+#pragma unroll
+                for (int o = Tl::NOCT / 2; o >= 1; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                if (oc == 0) diag[row0 + r] = d;
+            }
+        }
+        __syncthreads();   // bnd, diag visible
+        if (lq < 2) {      // P rows t, columns [32 half, +32): zeros above the diagonal, the diagonal
+            const int t = vrow;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                *reinterpret_cast<uint4*>(sP + sw128_off(t, 32 * half + 8 * u)) = make_uint4(0u, 0u, 0u, 0u);
+            if ((t >> 5) == half)
+                *reinterpret_cast<__nv_bfloat16*>(sP + sw128_off(t, t)) = __float2bfloat16_rn(diag[t]);
+        }
+        // (P entries are written by the epilogue threads of later rounds: each owns disjoint (t, s))
+#pragma unroll   // (unrolled: every level's normaliser rows are compile-time, own-row ones static registers)
+        for (int hA = 32; hA >= 2; hA >>= 2) {   // rounds: levels (32, 16), (8, 4), (2, 1)
+#pragma unroll
+            for (int lv = 0; lv < 2; ++lv) {
+                const int h = lv ? hA >> 1 : hA, ro = 64 * lv;   // operand rows ro + t
+#pragma unroll
+                for (int r = 0; r < Tl::RPG; ++r) {
+                    const int t = row0 + r, c = (t / (2 * h)) * 2 * h + h - 1;
+                    float2 bc[4];
+                    if (h >= Tl::RPG) {   // c is the last row of row group (c + 1) / RPG - 1
+                        const float4* bb = reinterpret_cast<const float4*>(bnd + ((c + 1) / Tl::RPG - 1) * K + ch0);
+                        const float4 x0 = bb[0], x1 = bb[1];
+                        bc[0] = make_float2(x0.x, x0.y); bc[1] = make_float2(x0.z, x0.w);
+                        bc[2] = make_float2(x1.x, x1.y); bc[3] = make_float2(x1.z, x1.w);
+                    } else {              // c is one of this thread's rows: row0 + (r / 2h) 2h + h - 1
+                        const int rc = (r / (2 * h)) * 2 * h + h - 1;
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) bc[p] = R.g[rc][p];
+                    }
+                    uint8_t* qh = qb + sw128_off(ro + t, col);
+                    uint8_t* kh = kb + sw128_off(ro + t, col);
+                    float2 ref[4];
+                    if (t > c) {          // F: Q row q e^{b_t - b_c}, K row zero
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) ref[p] = make_float2(-L2E * bc[p].x, -L2E * bc[p].y);
+                        scaled_row(R.q[r], R.g[r], ref, 1.f, qh, nullptr);
+                        *reinterpret_cast<uint4*>(kh) = make_uint4(0u, 0u, 0u, 0u);
+                    } else {              // E: K row k e^{b_c - b_t}, Q row zero
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) ref[p] = make_float2(L2E * bc[p].x, L2E * bc[p].y);
+                        scaled_row(R.k[r], R.g[r], ref, -1.f, kh, nullptr);
+                        *reinterpret_cast<uint4*>(qh) = make_uint4(0u, 0u, 0u, 0u);
+                    }
+                }
+            }
+            fence_async_smem();
+            tc_fence_before();
+            __syncthreads();
+            if (tid == 0) {
+                tc_fence_after();
+                const uint32_t idP = idesc_bf16(128, 128, 0, 0);
+                const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK);
+#pragma unroll
+                for (int kk = 0; kk < K / 16; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    mma_bf16(tP, sdesc_sw128(aQ + o, 16, 1024), sdesc_sw128(aK + o, 16, 1024), idP, kk > 0);
+                }
+                mma_commit(&bar);
+            }
+            mbar_wait(&bar, phase);
+            phase ^= 1;
+            tc_fence_after();
+            {   // lanes 0-63: level A's rows (columns 0-63), lanes 64-127: level B's rows (columns 64-127)
+                const int lv = lq >> 1, h = lv ? hA >> 1 : hA, t = vrow - 64 * lv;
+                uint32_t a[32];
+                tmem_ld32(tP + lane_base + 64 * lv + 32 * half, a);
+                tmem_wait_ld();
+                const int g0 = (t / (2 * h)) * 2 * h;
+                if (t >= g0 + h) {    // t in F: keep the E columns of its own group
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int s = 32 * half + j;
+                        if (s >= g0 && s < g0 + h)
+                            *reinterpret_cast<__nv_bfloat16*>(sP + sw128_off(t, s)) =
+                                __float2bfloat16_rn(__uint_as_float(a[j]));
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncthreads();   // the TMEM accumulator free, sQ / sK writable again
+        }
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tma_store_2d(tmP, sP, 0, (int)crow);
+            tma_store_commit();
+        }
+    }
+    return phase;
+}
 
 // Persistent: CTA c processes work items (b,h, chunk) c, c + gridDim.x, ...  The next item's q / k / log alpha
 // are loaded into the (then dead) operand registers right after the current item's operand build, so their
@@ -57,7 +217,7 @@ __global__ void __launch_bounds__(NTH, 1)
 k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmP, const __nv_bfloat16* __restrict__ q,
            const __nv_bfloat16* __restrict__ k, const TG* __restrict__ g, float* __restrict__ stats,
-           int* __restrict__ flags, float* __restrict__ bws, int T, int NC, int nitems) {
+           int* __restrict__ flags, int T, int NC, int nitems) {
     using Cfg = PrepCfg<K>;
     using Tl = typename Cfg::Tl;
     extern __shared__ uint8_t smem_raw[];
@@ -87,8 +247,8 @@ k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     __syncthreads();
     tc_fence_after();
     const uint32_t tP = tmem_base;
-    uint32_t phase = 0;
-    for (; item < nitems; item += gridDim.x, phase ^= 1) {
+    uint32_t phase = 0;                         // parity of the next wait on bar (one commit per MMA round)
+    for (; item < nitems; item += gridDim.x) {
         const int chunk = item % NC, bh = item / NC;
         const size_t crow = (size_t)bh * T + (size_t)chunk * CH;
         if (tid == 0) tma_store_wait_read();    // the previous item's Q~ / K~ / P stores have read their smem
@@ -126,11 +286,6 @@ k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
             for (int p = 0; p < 4; ++p) b[p] = add2(R.g[r][p], off[p]);
             scaled_row(R.q[r], b, refq, 1.f, qb + sw128_off(t, col), qb + sw128_off(64 + t, col));
             scaled_row(R.k[r], b, refk, -1.f, kb + sw128_off(t, col), kb + sw128_off(64 + t, col));
-            if (slow) {
-                float4* wb = reinterpret_cast<float4*>(bws + (crow + t) * K + ch0);
-                wb[0] = make_float4(b[0].x, b[0].y, b[1].x, b[1].y);
-                wb[1] = make_float4(b[2].x, b[2].y, b[3].x, b[3].y);
-            }
         }
         {   // the operand registers are dead: start loading the next item (overlaps MMA, epilogue, stores)
             const int nx = item + gridDim.x;
@@ -163,6 +318,7 @@ k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
         const int vrow = 32 * lq + lane;
         mbar_wait(&bar, phase);   // the P MMA (if any) has completed
+        phase ^= 1;
         tc_fence_after();
         if (!slow) {
             if (lq >= 2) {   // lo rows: lh + ll
@@ -195,31 +351,24 @@ k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
                     *reinterpret_cast<uint4*>(sP + sw128_off(t, 32 * half + 8 * u)) =
                         make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
             }
-        } else {
-            // exact path: P[t][s] = sum_m q_tm k_sm e^{b_tm - b_sm}, s <= t, every exponent <= 0
-            __syncthreads();
-            for (int e = tid; e < CH * CH; e += NTH) {
-                const int t = e >> 6, s_ = e & 63;
-                float acc = 0.f;
-                if (s_ <= t) {
-                    const __nv_bfloat16* qt = q + (crow + t) * K;
-                    const __nv_bfloat16* ks = k + (crow + s_) * K;
-                    const float* bt = bws + (crow + t) * K;
-                    const float* bs = bws + (crow + s_) * K;
-                    for (int m = 0; m < K; ++m)
-                        acc += __bfloat162float(qt[m]) * __bfloat162float(ks[m]) * ex2f((bt[m] - bs[m]) * L2E);
-                }
-                *reinterpret_cast<__nv_bfloat16*>(sP + sw128_off(t, s_)) = __float2bfloat16_rn(acc);
-            }
         }
         fence_async_smem();
         tc_fence_before();
         __syncthreads();                         // P staged; TMEM P drained; exch free
-        if (tid == 0) {
+        if (tid == 0 && !slow) {                 // (the exact path's P is written by the second phase below)
             tma_store_2d(&tmP, sP, 0, (int)crow);
             tma_store_commit();
         }
     }
+    // Second phase: P of this CTA's chunks that failed the guard.  In the common case none did: one parallel read of
+    // the CTA's flags (written above by this CTA, ordered by its barriers) skips it.  A separate, non-inlined
+    // function so that its registers never compete with the prefetched operands above.
+    bool any_exact = false;
+    for (int b0 = 0; (size_t)blockIdx.x + (size_t)b0 * gridDim.x < (size_t)nitems; b0 += NTH) {
+        const size_t it2 = blockIdx.x + (size_t)(b0 + tid) * gridDim.x;
+        any_exact |= __syncthreads_or(it2 < (size_t)nitems && flags[it2] != 0) != 0;
+    }
+    if (any_exact) phase = exact_P_phase<K, TG>(&tmP, q, k, g, flags, T, NC, nitems, sm, tP, &bar, phase);
     if (tid == 0) tma_store_wait_all();
     tc_fence_before();
     __syncthreads();
@@ -789,7 +938,7 @@ size_t fwd2_ws(int B, int H, int T, int K, int V) {
     const size_t BH = (size_t)B * H, NC = T / CH;
     const int S = fwd_segments((int)BH, V, (int)NC);
     return al(BH * T * K * 2) * 2 + al(BH * T * 64 * 2) + al(BH * NC * 2 * K * 4) + al(BH * NC * 4) +
-           al(BH * T * K * 4) + al(n_anch(T) * BH * V * K * 2) +
+           al(n_anch(T) * BH * V * K * 2) +
            (S > 1 ? al(BH * S * K * V * 4) + al(BH * S * K * V * 4 * seg_parts((int)BH, K, V, (int)NC, S)) +
                         al(BH * S * K * 4) : 0);
 }
@@ -803,7 +952,6 @@ FwdSaved fwd2_saved(const void* ws, int B, int H, int T, int K, int V) {
     f.Pm = w; w += al(rows * 64 * 2);
     f.stats = (const float*)w; w += al(BH * NC * 2 * K * 4);
     f.flags = (const int*)w; w += al(BH * NC * 4);
-    w += al(rows * K * 4);                // bws (exact-path cumsums)
     f.anch = w; w += al(n_anch(T) * BH * V * K * 2);
     f.S = fwd_segments((int)BH, V, (int)NC);
     f.h0v = f.S > 1 ? (const float*)w : nullptr;
@@ -819,7 +967,6 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
     __nv_bfloat16* Pm = (__nv_bfloat16*)w; w += al(rows * 64 * 2);
     float* stats = (float*)w; w += al(BH * NC * 2 * K * 4);
     int* flags = (int*)w; w += al(BH * NC * 4);
-    float* bws = (float*)w; w += al(rows * K * 4);
     __nv_bfloat16* anch = (__nv_bfloat16*)w; w += al(n_anch(p.T) * BH * p.V * K * 2);
     const int S = fwd_segments((int)BH, p.V, (int)NC);
     float* h0v = (float*)w; w += S > 1 ? al(BH * S * K * p.V * 4) : 0;   // segment-entry states (saved for bwd)
@@ -848,7 +995,7 @@ static cudaError_t launch_fwd2(const Problem& p, cudaStream_t st) {
         GLA_PROF("tc::fwd_prep", st);
         const int nitems = (int)(NC * BH);
         k_fwd_prep<K, TG><<<(unsigned)(nitems < num_sms() ? nitems : num_sms()), NTH, PrepCfg<K>::SMEM, st>>>(
-            mQ, mK, mP, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k, (const TG*)p.g, stats, flags, bws, p.T,
+            mQ, mK, mP, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k, (const TG*)p.g, stats, flags, p.T,
             (int)NC, nitems);
     }
     __nv_bfloat16* an = saved_anchors() ? anch : nullptr;
@@ -915,8 +1062,7 @@ static cudaError_t launch_summary(const Problem& p, const void* B_op, float* out
     __nv_bfloat16* Kt = (__nv_bfloat16*)w; w += al(rows * K * 2);
     __nv_bfloat16* Pm = (__nv_bfloat16*)w; w += al(rows * 64 * 2);
     float* stats = (float*)w; w += al(BH * NC * 2 * K * 4);
-    int* flags = (int*)w; w += al(BH * NC * 4);
-    float* bws = (float*)w;
+    int* flags = (int*)w;
     CUtensorMap mQ, mK, mP, mB;
     cudaError_t e;
     if ((e = make_map_2d(&mQ, Qt, rows, K, true)) != cudaSuccess) return e;
@@ -930,7 +1076,7 @@ static cudaError_t launch_summary(const Problem& p, const void* B_op, float* out
         GLA_PROF("tc::fwd_prep", st);
         const int nitems = (int)(NC * BH);
         k_fwd_prep<K, TG><<<(unsigned)(nitems < num_sms() ? nitems : num_sms()), NTH, PrepCfg<K>::SMEM, st>>>(
-            mQ, mK, mP, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k, (const TG*)p.g, stats, flags, bws, p.T,
+            mQ, mK, mP, (const __nv_bfloat16*)p.q, (const __nv_bfloat16*)p.k, (const TG*)p.g, stats, flags, p.T,
             (int)NC, nitems);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -66,11 +66,16 @@ __global__ void __launch_bounds__(KwCfg::NTHR, 1)
 k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmDP,
             const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmO,
             const float* __restrict__ stats, const float* __restrict__ x0, const float* __restrict__ dfinal,
-            float* __restrict__ out32, float* __restrict__ stdot, const int* __restrict__ flag, int T, int V,
-            int dbg) {
+            float* __restrict__ out32, float* __restrict__ stdot, const int* __restrict__ flag,
+            const int* __restrict__ cflags, int T, int V, int dbg) {
     // x0: the state entering the walk (REV 0: h0, REV 1: d_final_state), NULL = 0.  dfinal (REV 0 only): with
     // stdot, the final-state row sums rowsum(S_T (.) dS_T) of this value half.  out32: [units * T][K] fp32, the
     // unscaled dq^T / dk^T rows summed over all values.
+    // cflags: the forward's per-chunk exact-path flags [units][NC] (R9), or NULL.  A flagged chunk's saved
+    // operands are the exact forms (K~ = k e^{Gamma - b}, Q~ = q e^{b}), so its state pass takes the r = 0 frame:
+    // X <- X e^{pend + Gamma} (the decay before the update), SB <- bf16(X e^{pend}) (the state at the chunk's
+    // start), pending 0 -- the forward walk's exact path -- and its intra term is left to the reduce (the
+    // factorised product would overflow there).
     // dbg (GLA_KW_DBG, timing experiments only; results are wrong when set): 4 epilogue only drains the
     // accumulator, 8 no output MMAs
     using Cfg = KwCfg;
@@ -149,18 +154,24 @@ k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
         tmem_wait_st();
         const float* st_ch = stats + (size_t)unit * NC * 2 * K + kg;   // (r, Gamma) of chunk i at [i * 2K], [i * 2K + K]
+        const int* cf = cflags ? cflags + (size_t)unit * NC : nullptr;
         float pend = 0.f, n_r = st_ch[(size_t)chunk_of(0) * 2 * K], n_G = st_ch[(size_t)chunk_of(0) * 2 * K + K];
+        int n_slow = cf ? cf[chunk_of(0)] : 0;
         named_bar_sync(1, Cfg::NST);
         for (int j = 0; j < NC; ++j) {
             const float r_ = n_r, G_ = n_G;
+            const bool slow = n_slow != 0;
             if (j + 1 < NC) {
                 const size_t c1 = (size_t)chunk_of(j + 1) * 2 * K;
                 n_r = st_ch[c1];
                 n_G = st_ch[c1 + K];
+                n_slow = cf ? cf[chunk_of(j + 1)] : 0;
             }
             // REV 0: X <- H_i e^{r} (SB = bf16(X)), pending Gamma - r.  REV 1: X <- dH_{i+1} e^{Gamma - r}, pending r.
-            const float f = REV ? ex2f((pend + G_ - r_) * L2E) : ex2f((pend + r_) * L2E);
-            pend = REV ? r_ : G_ - r_;
+            // Exact-path chunk: X <- X e^{pend + Gamma}, SB = bf16(X e^{pend}), pending 0.
+            const float f = slow ? ex2f((pend + G_) * L2E) : REV ? ex2f((pend + G_ - r_) * L2E) : ex2f((pend + r_) * L2E);
+            const float fsb = slow ? ex2f(pend * L2E) : f;
+            pend = slow ? 0.f : REV ? r_ : G_ - r_;
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
                 if (j > 0) {                 // half h of the previous step: state MMA done, SB half h read
@@ -174,13 +185,24 @@ k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     uint32_t r[32], pk[16];
                     tmem_ld32(tX + lane_base + c, r);
                     tmem_wait_ld();
+                    if (!slow) {
 #pragma unroll
-                    for (int q = 0; q < 32; q += 2) {
-                        const float2 y = mul2(make_float2(__uint_as_float(r[q]), __uint_as_float(r[q + 1])),
-                                              make_float2(f, f));
-                        r[q] = __float_as_uint(y.x);
-                        r[q + 1] = __float_as_uint(y.y);
-                        pk[q / 2] = pack2(y);
+                        for (int q = 0; q < 32; q += 2) {
+                            const float2 y = mul2(make_float2(__uint_as_float(r[q]), __uint_as_float(r[q + 1])),
+                                                  make_float2(f, f));
+                            r[q] = __float_as_uint(y.x);
+                            r[q + 1] = __float_as_uint(y.y);
+                            pk[q / 2] = pack2(y);
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 32; q += 2) {
+                            const float2 x = make_float2(__uint_as_float(r[q]), __uint_as_float(r[q + 1]));
+                            const float2 y = mul2(x, make_float2(f, f));
+                            r[q] = __float_as_uint(y.x);
+                            r[q + 1] = __float_as_uint(y.y);
+                            pk[q / 2] = pack2(mul2(x, make_float2(fsb, fsb)));
+                        }
                     }
                     tmem_st32(tX + lane_base + c, r);
                     tmem_st16(tSB + lane_base + c / 2, pk);
@@ -239,7 +261,11 @@ k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         const int h = warp - 9;
         const uint32_t idO = idesc_bf16(128, 64, 0, 0);            // out^T[k][t] += SB[k][v] B[t][v]: A in TMEM
         const uint32_t idIN = idesc_bf16(128, 64, 1, REV ? 1 : 0); // += A^T[k][s] dP^T (dq) / dP (dk)
+        const int* cf = (h == 0 && intra && cflags) ? cflags + (size_t)unit * NC : nullptr;
+        int n_exact = cf ? cf[chunk_of(0)] : 0;   // exact-path flag of chunk j, loaded one step ahead
         for (int j = 0; j < NC; ++j) {
+            const bool exact = n_exact != 0;
+            if (cf && j + 1 < NC) n_exact = cf[chunk_of(j + 1)];
             const int b = j & 1;
             const uint32_t aA = smem_u32(sm + b * Cfg::STAGE), aO = aA + Cfg::OFF_O, adP = aA + Cfg::OFF_P;
             const uint32_t acc = tAcc + 64 * b;
@@ -254,7 +280,7 @@ k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     mma_bf16_ta_w(acc, tSB + 64 * h + 8 * s,
                                   sdesc_sw128(aO + (2 * h + (s >> 2)) * 8192 + (s & 3) * 32, 16, 1024), idO,
                                   (h == 1 || s > 0) ? 1u : 0u);
-            if (h == 0 && intra)
+            if (h == 0 && intra && !exact)   // (exact-path chunks: the intra term is formed in the reduce)
 #pragma unroll
                 for (int s = 0; s < CH / 16; ++s)   // dq: B = dP[t][s] K-major; dk: B = dP[t][s] MN-major (N = s)
                     mma_bf16_w(acc, sdesc_sw128(aA + s * 2048, 8192, 1024),
@@ -348,7 +374,7 @@ bool kwalk_ok(int K, int V) { return (K == 128 || K == 256) && (V == 256 || V ==
 template <int K, bool REV, int NVH>
 static cudaError_t launch_kw(const CUtensorMap& mA, const CUtensorMap& mDP, const CUtensorMap& mS, const CUtensorMap& mO,
                              const float* stats, const float* x0, const float* dfinal, float* out32, float* stdot,
-                             const int* flag, int T, int V, int units, cudaStream_t st) {
+                             const int* flag, const int* cflags, int T, int V, int units, cudaStream_t st) {
     auto kern = k_bwd_kwalk<K, REV, NVH>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KwCfg::SMEM);
     if (e != cudaSuccess) return e;
@@ -365,7 +391,7 @@ static cudaError_t launch_kw(const CUtensorMap& mA, const CUtensorMap& mDP, cons
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if ((e = cudaLaunchKernelEx(&cfg, kern, mA, mDP, mS, mO, stats, x0, dfinal, out32, stdot, flag, T, V, dbg)) !=
+    if ((e = cudaLaunchKernelEx(&cfg, kern, mA, mDP, mS, mO, stats, x0, dfinal, out32, stdot, flag, cflags, T, V, dbg)) !=
         cudaSuccess)
         return e;
     return cudaGetLastError();
@@ -374,10 +400,11 @@ static cudaError_t launch_kw(const CUtensorMap& mA, const CUtensorMap& mDP, cons
 template <bool REV>
 static cudaError_t kw_dispatch(int K, int V, const CUtensorMap& mA, const CUtensorMap& mDP, const CUtensorMap& mS,
                                const CUtensorMap& mO, const float* stats, const float* x0, const float* dfinal,
-                               float* out32, float* stdot, const int* flag, int T, int units, cudaStream_t st) {
+                               float* out32, float* stdot, const int* flag, const int* cflags, int T, int units,
+                               cudaStream_t st) {
 #define GLA_KW(KK, NV)                                                                                              \
     if (K == KK && V == 256 * NV)                                                                                   \
-        return launch_kw<KK, REV, NV>(mA, mDP, mS, mO, stats, x0, dfinal, out32, stdot, flag, T, V, units, st);
+        return launch_kw<KK, REV, NV>(mA, mDP, mS, mO, stats, x0, dfinal, out32, stdot, flag, cflags, T, V, units, st);
     GLA_KW(128, 1) GLA_KW(128, 2) GLA_KW(256, 1) GLA_KW(256, 2)
 #undef GLA_KW
     return cudaErrorNotSupported;
@@ -385,14 +412,14 @@ static cudaError_t kw_dispatch(int K, int V, const CUtensorMap& mA, const CUtens
 
 cudaError_t dq_kwalk(int K, int V, const CUtensorMap& mK, const CUtensorMap& mDP, const CUtensorMap& mV,
                      const CUtensorMap& mD, const float* stats, const float* h0, const float* dfinal, float* dq32,
-                     float* stdot, const int* flag, int T, int units, cudaStream_t st) {
-    return kw_dispatch<false>(K, V, mK, mDP, mV, mD, stats, h0, dfinal, dq32, stdot, flag, T, units, st);
+                     float* stdot, const int* flag, const int* cflags, int T, int units, cudaStream_t st) {
+    return kw_dispatch<false>(K, V, mK, mDP, mV, mD, stats, h0, dfinal, dq32, stdot, flag, cflags, T, units, st);
 }
 
 cudaError_t dk_kwalk(int K, int V, const CUtensorMap& mQ, const CUtensorMap& mDP, const CUtensorMap& mD,
                      const CUtensorMap& mV, const float* stats, const float* dfinal, float* dk32, const int* flag,
-                     int T, int units, cudaStream_t st) {
-    return kw_dispatch<true>(K, V, mQ, mDP, mD, mV, stats, dfinal, nullptr, dk32, nullptr, flag, T, units, st);
+                     const int* cflags, int T, int units, cudaStream_t st) {
+    return kw_dispatch<true>(K, V, mQ, mDP, mD, mV, stats, dfinal, nullptr, dk32, nullptr, flag, cflags, T, units, st);
 }
 
 }  // namespace tc

@@ -95,8 +95,11 @@ def test_tc_bwd_long_sequence_dlog_alpha(T):
 @pytest.mark.parametrize("K,V", [(256, 512), (128, 256), (128, 512), (256, 256)])   # every K-tiled walk variant:
 def test_tc_bwd_saved_forward_operands(gate, K, V):                                 # 1 or 2 channel groups x 1 or 2 value halves
     """gla_chunk_bwd_saved (reuses the forward's Q~, K~, P, (r, Gamma), exact-path flags and anchor states, forms
-    only dP, runs the K-tiled dq walk) against the fp64 oracle for every gradient, and against the recomputing
-    backward: dv, dh0 bitwise (same kernels), dq, dk, d log alpha within the bf16 bar (different dq walks)."""
+    only dP, runs the K-tiled walks) against the fp64 oracle for every gradient, and against the recomputing
+    backward: dv, dh0 bitwise (same kernels), dq, dk, d log alpha within the bf16 bar (different dq walks).
+    `mixed` and `extreme` fail the factorisation guard on every chunk: the saved backward then runs the tensor-core
+    exact path (r = 0 frames in the walks, exact intra terms in the reduce), the recomputing one the fp32
+    CUDA-core kernels, so every gradient is compared within the bar."""
     p = problem(2, 2, 320, K, V, seed=31, gate=gate, h0=True, dfinal=True)
     p["gate_kind"] = gate
     pc = cuda(p)
@@ -106,8 +109,9 @@ def test_tc_bwd_saved_forward_operands(gate, K, V):                             
     b = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, pc["h0"], pc["dfinal"], True, "tc",
                     fwd_workspace=wf)
     torch.cuda.synchronize()
+    exact = gate in ("mixed", "extreme")
     for x, y, n in zip(a, b, ("dq", "dk", "dv", "dlog_alpha", "dh0")):
-        if n in ("dv", "dh0") or gate == "mixed":   # (mixed: the guard sends both to the same exact kernels)
+        if n in ("dv", "dh0") and not exact:
             assert torch.equal(x, y), n
         else:
             d = (x.float() - y.float()).abs().max().item() / max(y.float().abs().max().item(), 1e-30)
@@ -192,3 +196,39 @@ def test_odd_shapes_fwd_and_saved_bwd(B, H, T, K, V):
     for name, x, y in zip(("dq", "dk", "dv", "dlog_alpha", "dh0"), got, ref):
         e = nerr_slices(x.float().cpu().numpy(), y)
         assert e < TOL, (name, e)
+
+
+def _sprinkle_exact_chunks(p, marks):
+    """Make the listed (b, h, chunk) failing the factorisation guard: half the channels at log alpha = -5 there
+    (half-chunk decay 160 > 60), std gates elsewhere -- frame changes between guarded and exact chunks."""
+    g = p["g"].clone()
+    K = g.shape[-1]
+    for b, h, c in marks:
+        g[b, h, 64 * c:64 * (c + 1), :K // 2] = -5.0
+    p["g"] = g
+    return p
+
+
+@pytest.mark.parametrize("B,H,T,K,V,marks", [
+    (1, 2, 640, 256, 512, [(0, 0, 1), (0, 0, 4), (0, 0, 5), (0, 0, 9), (0, 1, 0)]),   # one unit, several segments' worth
+    (2, 1, 576, 128, 256, [(0, 0, 8), (1, 0, 3)]),                                   # last chunk / a middle one
+    (1, 1, 4096, 128, 256, [(0, 0, 5), (0, 0, 16), (0, 0, 17), (0, 0, 40), (0, 0, 63)]),   # segment split S = 4
+])
+def test_tc_exact_path_on_some_chunks(B, H, T, K, V, marks):
+    """The tensor-core exact path (R9; DESIGN.md §8 guard cliff) on a few chunks among guarded ones: forward
+    (exact P from the per-sub-chunk-pair normalisers; r = 0 state frame) and the saved backward (r = 0
+    frames in the K-tiled and dv walks, exact intra terms in the reduce) against the fp64 oracle, every output
+    including the strict d log alpha (R12 applies only to `extreme`)."""
+    p = _sprinkle_exact_chunks(problem(B, H, T, K, V, seed=61, h0=True, dfinal=True), marks)
+    pc = cuda(p)
+    wf = G.fwd_workspace(pc["q"], pc["v"], pc["g"], 64, 16, "tc")
+    o, fs = G.chunk_fwd(pc["q"], pc["k"], pc["v"], pc["g"], 64, 16, pc["h0"], True, "tc", workspace=wf)
+    got = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, pc["h0"], pc["dfinal"], True, "tc",
+                      fwd_workspace=wf)
+    torch.cuda.synchronize()
+    ro, rfs = oracle_fwd(p)
+    errs = {"o": nerr_slices(o.float().cpu().numpy(), ro), "final_state": nerr_slices(fs.cpu().numpy(), rfs)}
+    for name, x, y in zip(("dq", "dk", "dv", "dlog_alpha", "dh0"), got, oracle_bwd(p)):
+        errs[name] = nerr_slices(x.float().cpu().numpy(), y)
+    print("exact chunks", B, H, T, K, V, " ".join(f"{n}={e:.2e}" for n, e in errs.items()))
+    assert all(e < TOL for e in errs.values()), errs

@@ -1,2 +1,5 @@
-for e in "GLA_DV_LAST=1" "X=1"; do echo "== $e"; for r in 1 2; do env $e timeout 120 python tools/kbench.py 1p3b 2>&1 | grep 'step'; done; done
-timeout 600 python -m pytest tests/test_tc_bwd.py -m gpu -x -q 2>&1 | tail -2
+# A/B of the current build against ab/libgla_old.so on the same box: alternating kbench runs
+for i in 1 2; do
+  echo "old: $(GLA_LIB=$PWD/ab/libgla_old.so timeout 200 python tools/kbench.py ${1:-1p3b} 2>&1 | grep -E 'step \(wall|us/launch' | tr -s ' ' | tr '\n' ';')"
+  echo "new: $(timeout 200 python tools/kbench.py ${1:-1p3b} 2>&1 | grep -E 'step \(wall|us/launch' | tr -s ' ' | tr '\n' ';')"
+done

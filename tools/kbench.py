@@ -8,6 +8,9 @@ import torch
 import synth
 from paper_2312_06635_b200 import binding as G
 
+if os.environ.get("GLA_LIB"):   # A/B timing against another build of the library
+    G.LIB_PATH = os.environ["GLA_LIB"]
+
 CFG = {"1p3b": (16, 4, 2048, 256, 512), "340m": (8, 4, 2048, 128, 256), "long16k": (2, 4, 16384, 256, 512), "t4k": (8, 4, 4096, 256, 512),
        "t8k": (4, 4, 8192, 256, 512), "long32k": (1, 4, 32768, 256, 512)}
 name = sys.argv[1] if len(sys.argv) > 1 else "1p3b"
