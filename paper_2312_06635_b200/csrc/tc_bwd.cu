@@ -38,6 +38,9 @@ namespace tc {
 
 namespace {
 constexpr int CH = 64;
+#ifndef GLA_RED_PF
+#define GLA_RED_PF 1
+#endif
 constexpr int VT = 128;
 constexpr int NTH = 256;
 constexpr float L2E = 1.4426950408889634f;
@@ -85,7 +88,7 @@ struct RedCfg {
     static constexpr uint32_t GT = 64 * 64 * sizeof(TG);                 // log alpha tile bytes
     static constexpr uint32_t STAGE = OFF_Q + 2 * TILE + GT;
     static constexpr uint32_t EX = NQ32 ? 3 * 64 * 68 * 4 : 0;   // exact chunks: alpha, dP, dP^T ([64][68] fp32 each)
-    static constexpr int NS = 2 * STAGE + EX + 64 * 65 * 4 + 1024 <= 232448 ? 2 : 1;
+    static constexpr int NS = 2 * STAGE + EX + 2 * 4 * 64 * 4 + 1024 <= 232448 ? 2 : 1;
     static constexpr uint32_t OFF_EX = NS * STAGE;
     static constexpr uint32_t SMEM = NS * STAGE + EX + 1024;
 };
@@ -196,22 +199,19 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     // (.) X_k) and no intra term; the intra terms are formed here in fp32 with decay factors <= 1 built as running
     // products of alpha (no exponent of a difference of cumsums, no overflow whatever the gates):
     //     dq_t += sum_{s <= t} dP[t][s] k_s e^{b_t - b_s},   dk_t += sum_{u >= t} dP[u][t] q_u e^{b_u - b_t}.
-    // Thread (row t, 16 channels) runs both sums (t + 1 and 64 - t terms: every thread 65 steps).
     using RC = RedCfg<NVT, TG, NQ32>;
     constexpr int NQ = RC::NQ;
     constexpr uint32_t ODK = RC::OFF_DK, OQ = RC::OFF_Q;
     if (*flag) return;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_align1k(smem_raw);
-    __shared__ float sb[64][65];      // g -> b (chunk-local cumsum), then x -> suffix sums
-    __shared__ float carry_s[64];
+    __shared__ float gt_s[4][64], xt_s[4][64];   // per row group: totals of g and of q (.) dq - k (.) dk
     float (*al)[68] = reinterpret_cast<float (*)[68]>(sm + RC::OFF_EX);                    // exact chunks: alpha
     float (*sdp)[68] = reinterpret_cast<float (*)[68]>(sm + RC::OFF_EX + 64 * 68 * 4);     // exact chunks: dP
     float (*sdpT)[68] = reinterpret_cast<float (*)[68]>(sm + RC::OFF_EX + 2 * 64 * 68 * 4);   // and dP^T
     __shared__ uint64_t bar[2], empty[2];
-    const int tid = threadIdx.x, t = tid >> 2, cg = tid & 3;
+    const int tid = threadIdx.x;
     const int m0 = blockIdx.x * 64, bh = blockIdx.y;
-    const int mc = m0 + 16 * cg;      // this thread's 16 channels [mc, mc+16)
     const int NC = T / CH;
     // Segment blockIdx.z: chunks [i_lo, i_hi].  The exact carries at every ANCH-th chunk boundary (cpart) make the
     // segments independent, so they run as separate CTAs (more, shorter CTAs: better wave balance).
@@ -239,6 +239,18 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             tma_load_2d(st + OQ + 2 * RC::TILE, &tmG, b, m0, row);
         }
     };
+    auto l2pf = [&](int i) {          // the same boxes as issue(i), prefetched into L2 only
+        const int row = (int)(head_row + (size_t)i * CH);
+        for (int j = 0; j < NQ; ++j) {
+            tma_prefetch_2d(&tmDQP, m0, row + j * BH * T);
+            tma_prefetch_2d(&tmDKP, m0, row + j * BH * T);
+            if (NQ32) { tma_prefetch_2d(&tmDQP, m0 + 32, row + j * BH * T); tma_prefetch_2d(&tmDKP, m0 + 32, row + j * BH * T); }
+        }
+        tma_prefetch_2d(&tmQ, m0, row);
+        tma_prefetch_2d(&tmK, m0, row);
+        tma_prefetch_2d(&tmG, m0, row);
+        if (sizeof(TG) == 4) tma_prefetch_2d(&tmG, m0 + 32, row);
+    };
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -255,180 +267,115 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 const int slot = c % RC::NS;
                 if (n >= (uint32_t)RC::NS) mbar_wait(&empty[slot], ((n / RC::NS) - 1) & 1);
                 issue(c);
+                if (GLA_RED_PF && c - RC::NS >= i_lo) l2pf(c - RC::NS);   // HBM busy while the ring is full
             }
         }
         return;
     }
-    if (tid < 64) {   // carry entering the segment from above: the final-state term, or the exact anchor
-        float c0 = 0.f;
-        if (i_hi == NC - 1) {
-            if (stdot)
-                for (int j = 0; j < n_stdot; ++j) c0 += stdot[((size_t)j * BH + bh) * K + m0 + tid];
-        } else {
-            const size_t a2 = (i_hi + 1) / ANCH - 1;
-            for (int j = 0; j < NVT; ++j) c0 += cpart[((a2 * NVT + j) * BH + bh) * K + m0 + tid];
-        }
-        carry_s[tid] = c0;
+    // Thread layout of the scans: channel ch = tid % 64 of the CTA's 64, rows [16 rg, 16 rg + 16) of the chunk with
+    // rg = tid / 64.  Both scans (the chunk-local cumsum b, the reverse cumsum of q (.) dq - k (.) dk) run in
+    // registers over the thread's 16 rows; the four row groups of a channel combine their totals through shared
+    // memory (one barrier per scan).  The carry of later chunks lives in every thread's registers.
+    const int ch = tid & 63, rg = tid >> 6, t0 = 16 * rg;
+    float carry = 0.f;    // d log alpha carry entering the current chunk from above, channel m0 + ch
+    if (i_hi == NC - 1) {
+        if (stdot)
+            for (int j = 0; j < n_stdot; ++j) carry += stdot[((size_t)j * BH + bh) * K + m0 + ch];
+    } else {
+        const size_t a2 = (i_hi + 1) / ANCH - 1;
+        for (int j = 0; j < NVT; ++j) carry += cpart[((a2 * NVT + j) * BH + bh) * K + m0 + ch];
     }
-    __shared__ int slow_s[ANCH];      // exact-path flags of this segment's chunks (read alongside the carries)
-    if (NQ32 && tid >= 64 && tid < 64 + ANCH)
-        slow_s[tid - 64] = (cflags && i_lo + tid - 64 <= i_hi) ? cflags[(size_t)bh * NC + i_lo + tid - 64] : 0;
+    __shared__ int slow_s[ANCH];      // exact-path flags of this segment's chunks
+    if (NQ32 && tid < ANCH)
+        slow_s[tid] = (cflags && i_lo + tid <= i_hi) ? cflags[(size_t)bh * NC + i_lo + tid] : 0;
     named_bar_sync(1, 256);
     uint32_t slow_bits = 0u;
     if (NQ32)
 #pragma unroll
         for (int c = 0; c < ANCH; ++c) slow_bits |= (slow_s[c] ? 1u : 0u) << c;
     uint32_t uses[2] = {0u, 0u};
-    // byte offset of 8 consecutive bf16 channels [c, c+8) of row t in a SW128 [64][64] bf16 tile
-    auto bf_off = [&](int c) { return (uint32_t)(t * 128 + ((((c >> 3) ^ (t & 7))) << 4)); };
+    // byte offset of element (row u, channel ch) in a SW128 [64][64] bf16 tile / in a pair of [64][32] fp32 boxes
+    auto bf_at = [&](int u) { return (uint32_t)(u * 128 + ((((ch >> 3) ^ (u & 7))) << 4) + (ch & 7) * 2); };
+    auto f32_at = [&](int u) {
+        return (uint32_t)((ch >> 5) * RC::TILE + u * 128 + (((((ch & 31) >> 2) ^ (u & 7))) << 4) + (ch & 3) * 4);
+    };
+    auto ldbf = [](const uint8_t* p) { return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(p)); };
     for (int i = i_hi; i >= i_lo; --i) {
         const int sidx = i % RC::NS;
         const uint8_t* st = sm + sidx * RC::STAGE;
-        if (tid < 64 && i + 1 < NC && (i + 1) % ANCH == 0) {   // exact carry rowsum(H_{i+1} (.) dH_{i+1})
-            float c0 = 0.f;
+        if (i + 1 < NC && (i + 1) % ANCH == 0) {   // exact carry rowsum(H_{i+1} (.) dH_{i+1})
             const size_t a = (i + 1) / ANCH - 1;
-            for (int j = 0; j < NVT; ++j) c0 += cpart[((a * NVT + j) * BH + bh) * K + m0 + tid];
-            carry_s[tid] = c0;
+            carry = 0.f;
+            for (int j = 0; j < NVT; ++j) carry += cpart[((a * NVT + j) * BH + bh) * K + m0 + ch];
         }
         mbar_wait(&bar[sidx], (uses[sidx]++) & 1);
         const bool slow = NQ32 && ((slow_bits >> (i - i_lo)) & 1u);
-        // (a1) chunk-local cumsum: stage g, one thread per channel scans the 64 rows
+        // (a1) chunk-local cumsum over the thread's rows, then the offset of the earlier row groups
+        float b[16];
         {
             const uint8_t* gt = st + OQ + 2 * RC::TILE;
-            float gv[16];
-            if (sizeof(TG) == 4) {
-                const uint8_t* box = gt + (cg >> 1) * 8192;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const float4 x = *reinterpret_cast<const float4*>(box + t * 128 + (((((cg & 1) * 4 + c)) ^ (t & 7)) << 4));
-                    gv[4 * c] = x.x; gv[4 * c + 1] = x.y; gv[4 * c + 2] = x.z; gv[4 * c + 3] = x.w;
-                }
-            } else {
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const uint4 x = *reinterpret_cast<const uint4*>(gt + bf_off(16 * cg + 8 * c));
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        const uint32_t u = word(x, w);
-                        gv[8 * c + 2 * w] = bf16lo(u);
-                        gv[8 * c + 2 * w + 1] = bf16hi(u);
-                    }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = gv[u];
-            if (NQ32 && slow) {
-#pragma unroll
-                for (int u = 0; u < 16; u += 4)
-                    *reinterpret_cast<float4*>(&al[t][16 * cg + u]) =
-                        make_float4(ex2f(gv[u] * L2E), ex2f(gv[u + 1] * L2E), ex2f(gv[u + 2] * L2E), ex2f(gv[u + 3] * L2E));
-                const uint4* dr = reinterpret_cast<const uint4*>(dPm + (head_row + (size_t)i * CH + t) * 64 + 16 * cg);
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const uint4 x = __ldg(dr + c);
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        const int cc = 16 * cg + 8 * c + 2 * w;
-                        sdp[t][cc] = sdpT[cc][t] = bf16lo(word(x, w));
-                        sdp[t][cc + 1] = sdpT[cc + 1][t] = bf16hi(word(x, w));
-                    }
-                }
-            }
-        }
-        named_bar_sync(1, 256);
-        if (tid < 64) {
             float run = 0.f;
-            for (int r = 0; r < CH; ++r) { run += sb[r][tid]; sb[r][tid] = run; }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float gv = sizeof(TG) == 4 ? *reinterpret_cast<const float*>(gt + f32_at(t0 + j))
+                                                 : ldbf(gt + bf_at(t0 + j));
+                if (NQ32 && slow) al[t0 + j][ch] = ex2f(gv * L2E);
+                run += gv;
+                b[j] = run;
+            }
+            gt_s[rg][ch] = run;
+            if (NQ32 && slow) {   // dP rows [t0, t0 + 16), key column ch (dP is token x token)
+                const __nv_bfloat16* dr = dPm + (head_row + (size_t)i * CH + t0) * 64 + ch;
+#pragma unroll 4
+                for (int j = 0; j < 16; ++j) sdp[t0 + j][ch] = sdpT[ch][t0 + j] = __bfloat162float(dr[(size_t)j * 64]);
+            }
         }
         named_bar_sync(1, 256);
-        float x[16], dqv[16], dkv[16], iqr[16], ikr[16];   // exact-path intra terms (zero on guarded chunks)
+        float pre = 0.f;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) { iqr[u] = 0.f; ikr[u] = 0.f; }
-        if (NQ32 && slow) {   // (all 256 threads: the call synchronises them)
-            exact_intra(st + OQ, st + OQ + RC::TILE, al, sdp, sdpT);
+        for (int g2 = 0; g2 < 3; ++g2) pre += g2 < rg ? gt_s[g2][ch] : 0.f;
+        const float r = gt_s[0][ch] + gt_s[1][ch];            // b at row CH / 2 - 1
+        const float gam = r + gt_s[2][ch] + gt_s[3][ch];      // b at row CH - 1
 #pragma unroll
-            for (int u = 0; u < 16; u += 4) {
-                const float4 a = *reinterpret_cast<const float4*>(&al[t][16 * cg + u]);
-                const float4 b = *reinterpret_cast<const float4*>(&sdp[t][16 * cg + u]);
-                iqr[u] = a.x; iqr[u + 1] = a.y; iqr[u + 2] = a.z; iqr[u + 3] = a.w;
-                ikr[u] = b.x; ikr[u + 1] = b.y; ikr[u + 2] = b.z; ikr[u + 3] = b.w;
-            }
-        }
+        for (int j = 0; j < 16; ++j) b[j] += pre;
+        // exact-path chunk: the r = 0 frame for dq, r = Gamma for dk, plus the exact intra terms
+        const float rq = slow ? 0.f : r, rk = slow ? gam : r;
+        if (NQ32 && slow) exact_intra(st + OQ, st + OQ + RC::TILE, al, sdp, sdpT);   // (all 256 threads)
+        float x[16];
+        const size_t ix0 = (head_row + (size_t)i * CH + t0) * K + m0 + ch;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const uint32_t o = bf_off(16 * cg + 8 * c);
-            float sq[8], sk[8];
+        for (int j = 0; j < 16; ++j) {
+            const int u = t0 + j;
+            float sq = 0.f, sk = 0.f;
 #pragma unroll
-            for (int w = 0; w < 8; ++w) { sq[w] = 0.f; sk[w] = 0.f; }
-#pragma unroll
-            for (int j = 0; j < NQ; ++j) {
-                if (NQ32) {   // fp32 [64 t][32 k] boxes: channels 16 cg + 8 c .. +8 are chunks 4 (cg & 1) + 2 c, +1
-                    const uint8_t* box = st + j * RC::QT + (cg >> 1) * RC::TILE + t * 128;
-                    const float4 x0 = *reinterpret_cast<const float4*>(box + ((((cg & 1) * 4 + 2 * c) ^ (t & 7)) << 4));
-                    const float4 x1 = *reinterpret_cast<const float4*>(box + ((((cg & 1) * 4 + 2 * c + 1) ^ (t & 7)) << 4));
-                    sq[0] += x0.x; sq[1] += x0.y; sq[2] += x0.z; sq[3] += x0.w;
-                    sq[4] += x1.x; sq[5] += x1.y; sq[6] += x1.z; sq[7] += x1.w;
-                } else {
-                    const uint4 a = *reinterpret_cast<const uint4*>(st + j * RC::TILE + o);
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) { sq[2 * w] += bf16lo(word(a, w)); sq[2 * w + 1] += bf16hi(word(a, w)); }
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < NQ; ++j) {
+            for (int p = 0; p < NQ; ++p) {
                 if (NQ32) {
-                    const uint8_t* box = st + ODK + j * RC::QT + (cg >> 1) * RC::TILE + t * 128;
-                    const float4 x0 = *reinterpret_cast<const float4*>(box + ((((cg & 1) * 4 + 2 * c) ^ (t & 7)) << 4));
-                    const float4 x1 = *reinterpret_cast<const float4*>(box + ((((cg & 1) * 4 + 2 * c + 1) ^ (t & 7)) << 4));
-                    sk[0] += x0.x; sk[1] += x0.y; sk[2] += x0.z; sk[3] += x0.w;
-                    sk[4] += x1.x; sk[5] += x1.y; sk[6] += x1.z; sk[7] += x1.w;
+                    sq += *reinterpret_cast<const float*>(st + p * RC::QT + f32_at(u));
+                    sk += *reinterpret_cast<const float*>(st + ODK + p * RC::QT + f32_at(u));
                 } else {
-                    const uint4 b = *reinterpret_cast<const uint4*>(st + ODK + j * RC::TILE + o);
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) { sk[2 * w] += bf16lo(word(b, w)); sk[2 * w + 1] += bf16hi(word(b, w)); }
+                    sq += ldbf(st + p * RC::TILE + bf_at(u));
+                    sk += ldbf(st + ODK + p * RC::TILE + bf_at(u));
                 }
             }
-            const uint4 qv = *reinterpret_cast<const uint4*>(st + OQ + o);
-            const uint4 kv = *reinterpret_cast<const uint4*>(st + OQ + RC::TILE + o);
-#pragma unroll
-            for (int w = 0; w < 8; ++w) {
-                const int u = 8 * c + w;
-                const float b = sb[t][16 * cg + u], r = sb[CH / 2 - 1][16 * cg + u];
-                // exact-path chunk: the r = 0 frame for dq, r = Gamma for dk, plus the exact intra terms
-                const float rq = (NQ32 && slow) ? 0.f : r, rk = (NQ32 && slow) ? sb[CH - 1][16 * cg + u] : r;
-                dqv[u] = fmaf(sq[w], ex2f((b - rq) * L2E), iqr[u]);
-                dkv[u] = fmaf(sk[w], ex2f((rk - b) * L2E), ikr[u]);
-                const float qf = (w & 1) ? bf16hi(word(qv, w >> 1)) : bf16lo(word(qv, w >> 1));
-                const float kf = (w & 1) ? bf16hi(word(kv, w >> 1)) : bf16lo(word(kv, w >> 1));
-                x[u] = qf * dqv[u] - kf * dkv[u];
-            }
+            float dqv = sq * ex2f((b[j] - rq) * L2E), dkv = sk * ex2f((rk - b[j]) * L2E);
+            if (NQ32 && slow) { dqv += al[u][ch]; dkv += sdp[u][ch]; }
+            x[j] = ldbf(st + OQ + bf_at(u)) * dqv - ldbf(st + OQ + RC::TILE + bf_at(u)) * dkv;
+            dq[ix0 + (size_t)j * K] = __float2bfloat16_rn(dqv);
+            dk[ix0 + (size_t)j * K] = __float2bfloat16_rn(dkv);
         }
-        const size_t ix = (head_row + (size_t)i * CH + t) * K + mc;
+        // reverse cumsum of x over the thread's rows; the later row groups' totals and the carry come next
+        float run = 0.f;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const uint4 oq = make_uint4(pack_bf16(dqv[8 * u], dqv[8 * u + 1]), pack_bf16(dqv[8 * u + 2], dqv[8 * u + 3]),
-                                        pack_bf16(dqv[8 * u + 4], dqv[8 * u + 5]), pack_bf16(dqv[8 * u + 6], dqv[8 * u + 7]));
-            const uint4 ok = make_uint4(pack_bf16(dkv[8 * u], dkv[8 * u + 1]), pack_bf16(dkv[8 * u + 2], dkv[8 * u + 3]),
-                                        pack_bf16(dkv[8 * u + 4], dkv[8 * u + 5]), pack_bf16(dkv[8 * u + 6], dkv[8 * u + 7]));
-            *reinterpret_cast<uint4*>(dq + ix + 8 * u) = oq;
-            *reinterpret_cast<uint4*>(dk + ix + 8 * u) = ok;
-        }
-        named_bar_sync(1, 256);            // everyone has read b and the stage buffers
+        for (int j = 15; j >= 0; --j) { run += x[j]; x[j] = run; }
+        xt_s[rg][ch] = run;
+        named_bar_sync(1, 256);            // every read of the stage (and of al / sdp) is done, xt_s complete
         if (tid == 0) mbar_arrive(&empty[sidx]);   // the producer may refill this stage
+        float post = carry;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) sb[t][16 * cg + u] = x[u];
-        named_bar_sync(1, 256);
-        if (tid < 64) {                    // reverse cumsum with the carry of all later chunks
-            float run = carry_s[tid];
-            for (int r = CH - 1; r >= 0; --r) { run += sb[r][tid]; sb[r][tid] = run; }
-            carry_s[tid] = run;
-        }
-        named_bar_sync(1, 256);
+        for (int g2 = 1; g2 < 4; ++g2) post += g2 > rg ? xt_s[g2][ch] : 0.f;
+        carry += (xt_s[0][ch] + xt_s[1][ch]) + (xt_s[2][ch] + xt_s[3][ch]);
 #pragma unroll
-        for (int u = 0; u < 16; u += 4)
-            *reinterpret_cast<float4*>(dg + ix + u) =
-                make_float4(sb[t][16 * cg + u], sb[t][16 * cg + u + 1], sb[t][16 * cg + u + 2], sb[t][16 * cg + u + 3]);
-        named_bar_sync(1, 256);
+        for (int j = 0; j < 16; ++j) dg[ix0 + (size_t)j * K] = x[j] + post;
     }
 }
 

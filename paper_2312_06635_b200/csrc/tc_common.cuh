@@ -120,6 +120,11 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 __device__ __forceinline__ void prefetch_l2(const void* gptr) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(gptr));
 }
+// Bulk L2 prefetch of a contiguous global range (TMA engine, no registers, no completion to wait on): keeps HBM busy
+// on data the CTA will load later.  bytes: a multiple of 16, gptr 16-byte aligned.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* gptr, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gptr), "r"(bytes) : "memory");
+}
 // Arrive on `bar` (count not incremented: the barrier's expected count includes it) once every cp.async this
 // thread has issued so far has completed.
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
@@ -141,6 +146,11 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
         ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
+}
+// L2 prefetch of one TMA box (no shared memory, no barrier): the box a later tma_load_2d will read.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];"
+                 ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1) : "memory");
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* smem_src, int c0, int c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"

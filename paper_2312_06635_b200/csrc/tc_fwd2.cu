@@ -37,6 +37,9 @@ constexpr int NTH = 256;
 constexpr float L2E = 1.4426950408889634f;
 constexpr float GUARD = 60.f;
 }  // namespace
+#ifndef GLA_PREP_PF
+#define GLA_PREP_PF 1
+#endif
 
 // ---------------------------------------------------------------------------------------------------------------
 template <int K>
@@ -241,6 +244,20 @@ k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     }
     ChunkRegs<K> R;
     int item = blockIdx.x;
+    // L2 prefetch of a later item's q / k / log alpha rows (contiguous: rows [crow, crow + 64) x K), so HBM stays busy
+    // through the operand build, when the register prefetch below has nothing in flight.
+    auto prefetch_item = [&](int it) {
+        if (it >= nitems) return;
+        const size_t r0 = (size_t)(it / NC) * T + (size_t)(it % NC) * CH;
+        constexpr uint32_t QB = CH * K * 2, GB = CH * K * sizeof(TG), PIECE = 16384;
+        for (uint32_t o = 0; o < QB; o += PIECE) {
+            prefetch_l2_bulk(reinterpret_cast<const uint8_t*>(q + r0 * K) + o, PIECE < QB - o ? PIECE : QB - o);
+            prefetch_l2_bulk(reinterpret_cast<const uint8_t*>(k + r0 * K) + o, PIECE < QB - o ? PIECE : QB - o);
+        }
+        for (uint32_t o = 0; o < GB; o += PIECE)
+            prefetch_l2_bulk(reinterpret_cast<const uint8_t*>(g + r0 * K) + o, PIECE < GB - o ? PIECE : GB - o);
+    };
+    if (tid == 32) prefetch_item(item + gridDim.x);
     if (item < nitems)
         load_chunk<K, TG, true, true>(R, q, k, g, (size_t)(item / NC) * T + (size_t)(item % NC) * CH, row0, ch0);
     tc_fence_before();
@@ -252,6 +269,7 @@ k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         const int chunk = item % NC, bh = item / NC;
         const size_t crow = (size_t)bh * T + (size_t)chunk * CH;
         if (tid == 0) tma_store_wait_read();    // the previous item's Q~ / K~ / P stores have read their smem
+        if (tid == 32 && GLA_PREP_PF) prefetch_item(item + 2 * gridDim.x);
         float2 off[4], rr[4], Gm[4];
         chunk_cumsum<K>(R, gtot, rg, ch0, off, rr, Gm);   // (its barrier also orders the wait above)
         bool bad = false;
