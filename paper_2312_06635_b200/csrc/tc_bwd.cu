@@ -38,9 +38,6 @@ namespace tc {
 
 namespace {
 constexpr int CH = 64;
-#ifndef GLA_RED_PF
-#define GLA_RED_PF 1
-#endif
 constexpr int VT = 128;
 constexpr int NTH = 256;
 constexpr float L2E = 1.4426950408889634f;
@@ -239,18 +236,6 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             tma_load_2d(st + OQ + 2 * RC::TILE, &tmG, b, m0, row);
         }
     };
-    auto l2pf = [&](int i) {          // the same boxes as issue(i), prefetched into L2 only
-        const int row = (int)(head_row + (size_t)i * CH);
-        for (int j = 0; j < NQ; ++j) {
-            tma_prefetch_2d(&tmDQP, m0, row + j * BH * T);
-            tma_prefetch_2d(&tmDKP, m0, row + j * BH * T);
-            if (NQ32) { tma_prefetch_2d(&tmDQP, m0 + 32, row + j * BH * T); tma_prefetch_2d(&tmDKP, m0 + 32, row + j * BH * T); }
-        }
-        tma_prefetch_2d(&tmQ, m0, row);
-        tma_prefetch_2d(&tmK, m0, row);
-        tma_prefetch_2d(&tmG, m0, row);
-        if (sizeof(TG) == 4) tma_prefetch_2d(&tmG, m0 + 32, row);
-    };
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -267,7 +252,6 @@ k_bwd_reduce_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 const int slot = c % RC::NS;
                 if (n >= (uint32_t)RC::NS) mbar_wait(&empty[slot], ((n / RC::NS) - 1) & 1);
                 issue(c);
-                if (GLA_RED_PF && c - RC::NS >= i_lo) l2pf(c - RC::NS);   // HBM busy while the ring is full
             }
         }
         return;
