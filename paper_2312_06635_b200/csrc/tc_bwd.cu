@@ -566,10 +566,14 @@ k_bwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
 
 // k_bwd_dp: dP = (dO V^T) (.) M per chunk over the full V, for the backward that reuses a forward's saved
 // Q~, K~, P (gla_chunk_bwd_saved).  Persistent; warp 0 streams 64-column dO / V boxes through a 4-stage TMA
-// ring, warp 1 issues the M=64 N=64 MMAs, warps 2-5 drain the accumulator (causal mask, bf16, TMA store).
+// ring, warp 1 issues the M=64 N=64 MMAs into a double-buffered accumulator (the next item's MMAs run while warps
+// 2-5 drain this one: causal mask, bf16, TMA store).
 // It also ORs the forward's per-chunk exact-path flags into the backward's flag (R9) when given them (the
 // V-tiled walks have no exact path; the K-tiled ones and the reduce do, so the K-tiled backward passes NULL).
-constexpr int DP_NSTG = 4;
+#ifndef GLA_DP_NSTG
+#define GLA_DP_NSTG 4
+#endif
+constexpr int DP_NSTG = GLA_DP_NSTG;
 __global__ void __launch_bounds__(192, 1)
 k_bwd_dp(const __grid_constant__ CUtensorMap tmDP, const __grid_constant__ CUtensorMap tmV,
          const __grid_constant__ CUtensorMap tmD, const int* __restrict__ fflags, int* __restrict__ flag, int T,
@@ -577,15 +581,14 @@ k_bwd_dp(const __grid_constant__ CUtensorMap tmDP, const __grid_constant__ CUten
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_align1k(smem_raw);
     uint8_t* sdP = sm + DP_NSTG * 16384;
-    __shared__ uint64_t full[DP_NSTG], empty[DP_NSTG], acc_full, acc_empty;
+    __shared__ uint64_t full[DP_NSTG], empty[DP_NSTG], acc_full[2], acc_empty[2];
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int NKB = V / 64;
-    if (warp == 0) tmem_alloc(&tmem_base, 64);
+    if (warp == 0) tmem_alloc(&tmem_base, 128);
     if (tid == 0) {
         for (int s2 = 0; s2 < DP_NSTG; ++s2) { mbar_init(&full[s2], 1); mbar_init(&empty[s2], 1); }
-        mbar_init(&acc_full, 1);
-        mbar_init(&acc_empty, 1);
+        for (int b = 0; b < 2; ++b) { mbar_init(&acc_full[b], 1); mbar_init(&acc_empty[b], 1); }
         fence_mbar_init();
         prefetch_tmap(&tmDP); prefetch_tmap(&tmV); prefetch_tmap(&tmD);
     }
@@ -614,7 +617,8 @@ k_bwd_dp(const __grid_constant__ CUtensorMap tmDP, const __grid_constant__ CUten
         const uint32_t idDP = idesc_bf16(64, 64, 0, 0);
         uint32_t cnt = 0, it = 0;
         for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
-            if (it > 0) mbar_wait(&acc_empty, (it - 1) & 1);
+            const uint32_t ab = it & 1, acc = tdP + 64 * ab;
+            if (it >= 2) mbar_wait(&acc_empty[ab], ((it >> 1) - 1) & 1);
             tc_fence_after();
             for (int kb = 0; kb < NKB; ++kb, ++cnt) {
                 const uint32_t s2 = cnt % DP_NSTG, use = cnt / DP_NSTG;
@@ -623,11 +627,11 @@ k_bwd_dp(const __grid_constant__ CUtensorMap tmDP, const __grid_constant__ CUten
                 const uint32_t aD = smem_u32(sm + s2 * 16384), aV = aD + 8192;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                    mma_bf16_w(tdP, sdesc_sw128(aD + kk * 32, 16, 1024), sdesc_sw128(aV + kk * 32, 16, 1024), idDP,
+                    mma_bf16_w(acc, sdesc_sw128(aD + kk * 32, 16, 1024), sdesc_sw128(aV + kk * 32, 16, 1024), idDP,
                                (kb | kk) > 0);
                 mma_commit_w(&empty[s2]);
             }
-            mma_commit_w(&acc_full);
+            mma_commit_w(&acc_full[ab]);
             __syncwarp();
         }
     } else {
@@ -636,16 +640,17 @@ k_bwd_dp(const __grid_constant__ CUtensorMap tmDP, const __grid_constant__ CUten
         uint32_t it = 0;
         for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
             const int row = (int)((size_t)(item / NC) * T + (size_t)(item % NC) * CH);
-            mbar_wait(&acc_full, it & 1);
+            const uint32_t ab = it & 1;
+            mbar_wait(&acc_full[ab], (it >> 1) & 1);
             tc_fence_after();
             if (et == 0) tma_store_wait_read();    // the previous item's dP store has read the staging tile
             named_bar_sync(1, 128);
-            m64_epilogue(tdP, lane_base, lq, lane, sdP);
+            m64_epilogue(tdP + 64 * ab, lane_base, lq, lane, sdP);
             tc_fence_before();
             fence_async_smem();
             named_bar_sync(1, 128);
             if (et == 0) {
-                mbar_arrive(&acc_empty);
+                mbar_arrive(&acc_empty[ab]);
                 tma_store_2d(&tmDP, sdP, 0, row);
                 tma_store_commit();
             }
@@ -654,7 +659,7 @@ k_bwd_dp(const __grid_constant__ CUtensorMap tmDP, const __grid_constant__ CUten
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem_base, 64);
+    if (warp == 0) tmem_dealloc(tmem_base, 128);
 }
 
 
