@@ -521,7 +521,7 @@ def report(args, cfg, W, world, ms_step, value, prof, launches, clk, e2e, chain,
                 "tc::bwd_dq": [f"k_bwd_kwalk<{K}, 0,", f"k_bwd_kwalk<{K}, false", f"k_bwd_dq3<{K}>"],
                 "tc::bwd_dk": [f"k_bwd_kwalk<{K}, 1,", f"k_bwd_kwalk<{K}, true"],
                 "tc::bwd_dv": [f"k_bwd_dkv3<{K}, 2>"], "tc::bwd_dkv": [f"k_bwd_dkv3<{K}, 1>"],
-                "tc::bwd_reduce": [f"k_bwd_reduce_tma<{K},"]}
+                "tc::bwd_reduce": [f"k_bwd_reduce_tma<{K},"], "simt::bwd_gate": ["k_bwd_gate"]}
 
     def traffic_of(name):
         for key in ncu_keys.get(name, []):

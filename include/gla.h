@@ -9,10 +9,13 @@
  * (`chunk`), sub-chunk size c (`subchunk`).  The result is the recurrence's (the method is exact);
  * `chunk`/`subchunk` change only the rounding and the speed.  On the SIMT path both are honoured as given.
  * On the tensor-core path C = 64 and `subchunk` must divide 64 but is otherwise ignored: the TC kernels form
- * the whole 64 x 64 intra-chunk score block with one per-chunk normaliser under a range guard (R8/R9)
- * instead of per-sub-chunk normalisers.  A chunk that fails the guard (some channel's half-chunk log decay
- * exceeds 60) runs an exact fp32 log-space path in the forward, and sends the WHOLE backward call to the
- * fp32 CUDA-core kernels (correct, but several times slower: the "guard cliff").
+ * the 64 x 64 intra-chunk score block with one per-chunk normaliser under a range guard (R8/R9).
+ * A chunk that fails the guard (some channel's half-chunk log decay exceeds 60) takes the exact path for that
+ * chunk only: P from the paper's per-sub-chunk-pair normalisers taken down to single tokens (six
+ * levels, tensor cores, every factor <= 1), the walks in the r = 0 frame, and (gla_chunk_bwd_saved with K-tiled
+ * walks: K in {128,256}, V in {256,512}) the exact intra-chunk backward terms in fp32 in the reduce.  The other
+ * TC backward configurations (gla_chunk_bwd, or other V) still send the WHOLE backward call to the fp32
+ * CUDA-core kernels when any chunk is flagged (correct, but ~40x slower: the "guard cliff").
  *
  * Conventions shared by every entry point
  *   - Layout: row-major, [B, H, T, K] for q/k/log_alpha/dq/dk/d_log_alpha, [B, H, T, V] for v/out/d_out/dv,
