@@ -37,6 +37,9 @@ constexpr int NTH = 256;
 constexpr float L2E = 1.4426950408889634f;
 constexpr float GUARD = 60.f;
 }  // namespace
+#ifndef GLA_FWD_OB2
+#define GLA_FWD_OB2 1
+#endif
 #ifndef GLA_PREP_PF
 #define GLA_PREP_PF 1
 #endif
@@ -419,7 +422,12 @@ struct StateCfg {
     static_assert(SMEM <= 232448, "dynamic shared memory");
     // TMEM: Y [K] | SB bf16 pairs [K/2] | O [64] (64-column aligned; both O issuers accumulate into it in turn)
     static constexpr uint32_t COL_SB = K, COL_OA = (K + K / 2 + 63) / 64 * 64;
-    static constexpr uint32_t TCOLS = COL_OA + 64 > 256 ? 512 : 256;
+    // OB2: the two channel halves' output MMAs go to separate accumulators O_a, O_b, issued concurrently by warps 9
+    // and 10 (one thread issues ~1 MMA per 120 cycles, so the ordered issue into one accumulator serialised ~16
+    // issue slots per chunk); the epilogue sums O_a + O_b (fixed order: deterministic).
+    static constexpr bool OB2 = GLA_FWD_OB2 && K >= 128;
+    static constexpr uint32_t COL_OB = COL_OA + (OB2 ? 64 : 0);
+    static constexpr uint32_t TCOLS = COL_OB + 64 > 256 ? 512 : 256;
     static constexpr int NST = 256, NTHR = NST + 3 * 32 + 128;  // state, 3 MMA issuers, epilogue
     static constexpr int NSB = K / 16;                           // K-steps of the SB Q~^T product
     static constexpr int NHALF = K >= 128 ? 2 : 1;               // channel halves of the pipelined state pass
@@ -497,7 +505,7 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     __syncthreads();
     tc_fence_after();
     const uint32_t tS = tmem_base, tSB = tmem_base + Cfg::COL_SB;
-    const uint32_t tOa = tmem_base + Cfg::COL_OA;
+    const uint32_t tOa = tmem_base + Cfg::COL_OA, tOb = tmem_base + Cfg::COL_OB;
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const int vrow = 32 * (warp & 3) + lane;
 
@@ -636,7 +644,8 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         const bool is_a = warp == 9;
         const uint32_t idO = idesc_bf16(128, 64, 0, 0);      // O^T[v][t] = SB . Q~hi^T  (SB from TMEM)
         const uint32_t idPV = idesc_bf16(128, 64, 1, 0);     // O^T += V^T P^T
-        const uint32_t tD = tOa;                            // O_b accumulates onto O_a (after it, fixed order)
+        // O_b accumulates onto O_a after it (fixed order), or (OB2) into its own accumulator concurrently
+        const uint32_t tD = (is_a || !Cfg::OB2) ? tOa : tOb;
         const int k0 = is_a ? 0 : Cfg::NSB_A, k1 = is_a ? Cfg::NSB_A : Cfg::NSB;
         for (int i = 0; i < NC; ++i) {
             const int b = i & 1;
@@ -645,13 +654,13 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             if (emit) mbar_wait(&bar_q[b], (i >> 1) & 1);
             if (is_a) mbar_wait(&bar_vp[b], (i >> 1) & 1);
             if (i >= 1) mbar_wait(&bar_ofree, (i - 1) & 1);
-            if (!is_a) mbar_wait(&bar_oa, i & 1);   // O_a of this chunk complete: accumulate after it
+            if (!is_a && !Cfg::OB2) mbar_wait(&bar_oa, i & 1);   // O_a of this chunk complete: accumulate after it
             tc_fence_after();
             if (is_a && lane == 0) TR(3, i);
             if (emit)
                 for (int kk = k0; kk < k1; ++kk)
                     mma_bf16_ta_w(tD, tSB + 8 * kk, sdesc_sw128(aQ + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idO,
-                                  !is_a || kk > k0);
+                                  (!is_a && !Cfg::OB2) || kk > k0);
             if (is_a && emit) {
                 const uint32_t aV = smem_u32(sV + b * 16384), aP = smem_u32(sP + b * 8192);
 #pragma unroll
@@ -719,7 +728,14 @@ k_fwd_state(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 uint32_t ra[32];
-                tmem_ld32(tOa + 32 * h + lane_base, ra);   // O = O_a (O_b's MMAs accumulated onto it)
+                tmem_ld32(tOa + 32 * h + lane_base, ra);   // O = O_a (O_b's MMAs accumulated onto it), or O_a + O_b
+                if (Cfg::OB2) {
+                    uint32_t rb[32];
+                    tmem_ld32(tOb + 32 * h + lane_base, rb);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) ra[j] = __float_as_uint(__uint_as_float(ra[j]) + __uint_as_float(rb[j]));
+                }
                 tmem_wait_ld();
                 if (h == 1) {
                     tc_fence_before();
