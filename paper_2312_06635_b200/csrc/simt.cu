@@ -686,7 +686,7 @@ constexpr int MAXK_STEP = 1024;
 // Decode step.  grid (ceil(V / (4 CQ)), BH), CQ x RG threads = CQ column-quads x RG row groups; every thread
 // streams its K / RG state rows (float4 read-modify-write, rows of a warp contiguous), o reduced over the row
 // groups in shared memory (fixed order).  Small batches use narrow tiles (CQ = 8, RG = 16) to spread the state
-// over more SMs; large batches the wide ones (CQ = 32, RG = 8).
+// over more SMs (CQ = 4, RG = 32 when even those leave SMs idle); large batches the wide ones (CQ = 32, RG = 8).
 template <typename TQ, typename TG, int CQ, int RG>
 __global__ void __launch_bounds__(CQ * RG) k_step(const TQ* __restrict__ q, const TQ* __restrict__ k,
                                                   const TQ* __restrict__ v, const TG* __restrict__ g,
@@ -901,7 +901,12 @@ static cudaError_t step_impl(int BH, int K, int V, const void* q, const void* k,
                              float* state, void* out, cudaStream_t st) {
     {
         GLA_PROF("simt::k_step", st);
-        if ((long)BH * cdiv(V, 128) < 2 * 148)   // few units: narrow tiles, more CTAs
+        // (measured: the 16-column tiles also for up to 4x148 units were equal at B = 16, slower beyond)
+        if ((long)BH * cdiv(V, 32) <= 148 && K <= 8 * 32)   // very few units (B = 1 decode): 16-column tiles and
+            // one batch of 8 rows per thread, so each thread's state traffic is one round trip to HBM
+            k_step<TQ, TG, 4, 32><<<dim3(cdiv(V, 16), BH), 128, 0, st>>>((const TQ*)q, (const TQ*)k, (const TQ*)v,
+                                                                       (const TG*)g, state, (TQ*)out, K, V);
+        else if ((long)BH * cdiv(V, 128) < 2 * 148)   // few units: narrow tiles, more CTAs
             k_step<TQ, TG, 8, 16><<<dim3(cdiv(V, 32), BH), 128, 0, st>>>((const TQ*)q, (const TQ*)k, (const TQ*)v,
                                                                        (const TG*)g, state, (TQ*)out, K, V);
         else

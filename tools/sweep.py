@@ -15,6 +15,7 @@ PEAKS = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.absp
                                     "MEASURED_PEAKS.json")))
 HBM = PEAKS["hbm_gbs"]
 TF = PEAKS["bf16_tflops"]
+DEC = bool(os.environ.get("SWEEP_DECODE_ONLY"))   # decode table only
 flush = torch.empty(256 * 2**20 // 4, device="cuda")
 
 
@@ -39,7 +40,7 @@ print("# One-GPU sweep (B200, tools/sweep.py)\n")
 print("## fwd + bwd (gla_chunk_fwd + gla_chunk_bwd_saved), C = 64\n")
 print("| config | B, H, T, K, V | ms / step | M tokens/s | algorithmic TFLOP/s (% of bf16 peak) |")
 print("|---|---|---|---|---|")
-for name, (B, H, T, K, V) in [("340M (configs[1])", (8, 4, 2048, 128, 256)), ("1.3B (configs[2])", (16, 4, 2048, 256, 512)),
+for name, (B, H, T, K, V) in [] if DEC else [("340M (configs[1])", (8, 4, 2048, 128, 256)), ("1.3B (configs[2])", (16, 4, 2048, 256, 512)),
                               ("1.3B T=4K (configs[3])", (8, 4, 4096, 256, 512)),
                               ("1.3B T=8K (configs[3])", (4, 4, 8192, 256, 512)),
                               ("1.3B T=16K (configs[3])", (2, 4, 16384, 256, 512)),
@@ -66,7 +67,7 @@ print("\n## Guard cliff: the same 1.3B step with `mixed` gates (half the channel
       "the factorisation guard, DESIGN.md R9)\n")
 print("| gates | ms / step | M tokens/s |")
 print("|---|---|---|")
-for gate in ("std", "mixed"):
+for gate in (() if DEC else ("std", "mixed")):
     B, H, T, K, V = 16, 4, 2048, 256, 512
     p = synth.problem(B, H, T, K, V, seed=1, gate=gate)
     q, k, v, g, do = (p[n].cuda() for n in ("q", "k", "v", "g", "do"))
