@@ -570,6 +570,9 @@ k_bwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
 // 2-5 drain this one: causal mask, bf16, TMA store).
 // It also ORs the forward's per-chunk exact-path flags into the backward's flag (R9) when given them (the
 // V-tiled walks have no exact path; the K-tiled ones and the reduce do, so the K-tiled backward passes NULL).
+#ifndef GLA_ANCH_PF
+#define GLA_ANCH_PF 1
+#endif
 #ifndef GLA_DP_NSTG
 #define GLA_DP_NSTG 4
 #endif
@@ -1046,6 +1049,13 @@ k_bwd_dkv3(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         named_bar_sync(1, DC::NST);
         for (int i = NC - 1; i >= 0; --i) {
             const int j = NC - 1 - i;
+            // The next step's anchor carry (boundary i, if it is one) reads this CTA's 128 rows of the anchor state
+            // (one contiguous 64 KB block): prefetch them into L2 a chunk ahead, so the pass does not wait on HBM.
+            if (GLA_ANCH_PF && tid == 0 && anch && i > 0 && i % ANCH == 0) {
+                const uint8_t* a0 = reinterpret_cast<const uint8_t*>(
+                    anch + (((size_t)(i / ANCH - 1) * gridDim.y + bh) * V + v0) * K);
+                for (uint32_t o = 0; o < (uint32_t)VT * K * 2; o += 16384) prefetch_l2_bulk(a0 + o, 16384);
+            }
             if (tid < K) {   // dSB = bf16(dH_{i+1} e^{Gamma - r}); Z <- same; next pending = r
                 const float r_ = st_r, G_ = st_G;
                 const bool slow = st_slow != 0;
