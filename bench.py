@@ -449,7 +449,7 @@ def main():
     if not args.no_e2e:
         host_in = [x.cpu().pin_memory() for x in W.inputs]
         host_out = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
-        n_e2e = max(2, min(args.steps, 10))
+        n_e2e = max(2, min(args.steps, 20))
         h2d = sum(x.numel() * x.element_size() for x in host_in)
         d2h = sum(x.numel() * x.element_size() for x in host_out)
         dd = [[torch.empty_like(x) for x in W.inputs] for _ in range(2)]
