@@ -1,6 +1,6 @@
 """Small-shape run of every kernel family under compute-sanitizer (memcheck / racecheck / synccheck):
 TC forward + saved backward (K-tiled dq / dk walks, dv walk, reduce), recomputing TC backward, SIMT forward +
-backward, TC segment summaries, decode step, the two-gate (beta) path.  python tools/sanitize_small.py  (run under compute-sanitizer)."""
+backward, TC segment summaries, the exact path (mixed gates), decode step, the two-gate (beta) path.  python tools/sanitize_small.py  (run under compute-sanitizer)."""
 import os
 import sys
 
@@ -13,8 +13,9 @@ from paper_2312_06635_b200 import binding as G
 torch.cuda.set_device(0)
 if os.environ.get("GLA_SERIAL"):   # the launch tracer runs every kernel on the caller's stream, one at a time
     G.profile(True)
-for (B, H, T, K, V) in [(1, 2, 256, 256, 512), (1, 1, 192, 128, 256)]:
-    p = {n: t.cuda() for n, t in synth.problem(B, H, T, K, V, seed=0).items()}
+for (B, H, T, K, V, gate) in [(1, 2, 256, 256, 512, "std"), (1, 1, 192, 128, 256, "std"),
+                              (1, 1, 256, 256, 512, "mixed")]:   # mixed: every chunk on the exact path (R9)
+    p = {n: t.cuda() for n, t in synth.problem(B, H, T, K, V, seed=0, gate=gate).items()}
     h0 = synth.state(B, H, K, V, 1).cuda()
     df = synth.state(B, H, K, V, 2).cuda()
     wf = G.fwd_workspace(p["q"], p["v"], p["g"], 64, 16, "tc")
