@@ -57,6 +57,24 @@ def test_tc_bwd_deterministic():
         assert torch.equal(x, y)
 
 
+@pytest.mark.parametrize("gate", ["std", "mixed"])
+def test_tc_saved_path_deterministic(gate):
+    """The bench's path (forward with saved operands, K-tiled 2-CTA-cluster walks, dv walk, reduce; `mixed`: every
+    chunk on the exact path) gives bitwise-identical outputs and gradients when rerun."""
+    pc = cuda(problem(2, 4, 512, 256, 512, seed=26, gate=gate, h0=True, dfinal=True))
+    runs = []
+    for _ in range(2):
+        wf = G.fwd_workspace(pc["q"], pc["v"], pc["g"], 64, 16, "tc")
+        o, fs = G.chunk_fwd(pc["q"], pc["k"], pc["v"], pc["g"], 64, 16, pc["h0"], True, "tc", workspace=wf)
+        gr = G.chunk_bwd(pc["q"], pc["k"], pc["v"], pc["g"], pc["do"], 64, 16, pc["h0"], pc["dfinal"], True, "tc",
+                         fwd_workspace=wf)
+        runs.append((o, fs) + tuple(gr))
+    torch.cuda.synchronize()
+    for x, y in zip(*runs):
+        if x is not None:
+            assert torch.equal(x, y)
+
+
 def test_tc_bwd_full_size_sampled():
     """BASELINE.json configs[2] in the bench's launch configuration; oracle on 2 sampled (b,h) slices."""
     B, H, T, K, V = 16, 4, 2048, 256, 512
