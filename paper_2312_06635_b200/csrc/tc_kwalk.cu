@@ -77,7 +77,7 @@ k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     // start), pending 0 -- the forward walk's exact path -- and its intra term is left to the reduce (the
     // factorised product would overflow there).
     // dbg (GLA_KW_DBG, timing experiments only; results are wrong when set): 4 epilogue only drains the
-    // accumulator, 8 no output MMAs
+    // accumulator, 8 no output MMAs, 16 no peer exchange, 32 no global stores of the rows
     using Cfg = KwCfg;
     if (*flag) return;
     extern __shared__ uint8_t smem_raw[];
@@ -329,7 +329,7 @@ k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     acc[t] = __uint_as_float(a[t]);
                     acc[32 + t] = __uint_as_float(a2[t]);
                 }
-                if (NVH == 2) {
+                if (NVH == 2 && !(dbg & 16)) {
                     // our partial of the peer's 32 tokens -> the peer's buffer (row kk) once the peer has read the
                     // previous one; then the peer's partial of ours, added in a fixed order (own + peer)
                     if (j > 0) mbar_wait_cluster(&bar_pfree, (j - 1) & 1);
@@ -353,6 +353,7 @@ k_bwd_kwalk(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     }
                 }
                 float* o = outp + ((size_t)chunk_of(j) * CH + T0) * K;
+                if (!(dbg & 32))
 #pragma unroll
                 for (int t = 0; t < (NVH == 2 ? 32 : 64); ++t) o[(size_t)t * K] = acc[T0 + t];
             }
