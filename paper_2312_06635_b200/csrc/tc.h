@@ -15,7 +15,10 @@ size_t fwd_ws(int B, int H, int T, int K, int V, int C);
 size_t bwd_ws(int B, int H, int T, int K, int V, int C);
 // 2-D bf16 TMA map over a [rows][cols] row-major tensor, box {64 cols, 64 rows}, optional 128B swizzle.
 // d log alpha carry re-anchored from exact states every ANCH chunks (R12).
-constexpr int ANCH = 8;
+#ifndef GLA_ANCH
+#define GLA_ANCH 8
+#endif
+constexpr int ANCH = GLA_ANCH;
 // The per-chunk operands a TC forward (tc_fwd2.cu) leaves in its workspace, reused by the backward.
 struct FwdSaved {
     const void *Qt, *Kt, *Pm;     // Q~hi, K~hi [B*H*T, K] bf16; P [B*H*T, 64] bf16

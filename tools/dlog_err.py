@@ -12,6 +12,9 @@ import oracle
 import synth
 from paper_2312_06635_b200 import binding as G
 
+if os.environ.get("GLA_LIB"):   # another build of the library (variants/)
+    G.LIB_PATH = os.environ["GLA_LIB"]
+
 
 def nerr(x, y):
     x = x.float().cpu().double().numpy()
