@@ -123,7 +123,9 @@ def test_bf16_gates():
 # ---- decode, segments, determinism ---------------------------------------------------------------------
 @pytest.mark.parametrize("dtype,tol,B,H,T,K,V", [(torch.float32, F32_TOL, 2, 2, 64, 64, 96),
                                                   (torch.bfloat16, BF16_TOL, 2, 2, 64, 64, 96),
-                                                  (torch.bfloat16, BF16_TOL, 80, 4, 8, 32, 256)])   # wide tiles
+                                                  (torch.bfloat16, BF16_TOL, 80, 4, 8, 32, 256),    # wide tiles
+                                                  (torch.bfloat16, BF16_TOL, 16, 4, 8, 64, 128),    # narrow tiles
+                                                  (torch.bfloat16, BF16_TOL, 1, 4, 16, 256, 512)])  # B = 1 decode shape
 def test_recurrent_step_matches_oracle_and_chunk_fwd(dtype, tol, B, H, T, K, V):
     p = problem(B, H, T, K, V, seed=7, dtype=dtype, h0=True)
     pc = cuda(p)
