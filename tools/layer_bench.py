@@ -9,6 +9,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
 from paper_2312_06635_b200 import binding as G
+
+if os.environ.get("GLA_LIB"):   # another build of the library (variants/)
+    G.LIB_PATH = os.environ["GLA_LIB"]
 from paper_2312_06635_b200.layer import GLALayer
 
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
