@@ -36,6 +36,25 @@ __device__ __forceinline__ void ldf8(const float* p, float (&x)[8]) {   // 8 fp3
     const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p + 4));
     x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
 }
+// 8 parameters from shared memory (SP) or global memory
+template <bool SP>
+__device__ __forceinline__ void ldp8(const float* p, float (&x)[8]) {
+    if (SP) {
+        const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
+        ldf8(p, x);
+    }
+}
+// CTA-cooperative copy of the three n-float parameter vectors into shared memory [3][n] (n % 4 == 0), then a barrier
+__device__ __forceinline__ void stage_params(float* s, const float* a, const float* b, const float* c, int n) {
+    for (int i = threadIdx.x; i < 3 * n / 4; i += blockDim.x) {
+        const int v = i / (n / 4), j = i - v * (n / 4);
+        const float* src = v == 0 ? a : (v == 1 ? b : c);
+        reinterpret_cast<float4*>(s)[i] = __ldg(reinterpret_cast<const float4*>(src) + j);
+    }
+    __syncthreads();
+}
 __device__ __forceinline__ void st8(__nv_bfloat16* p, const float (&x)[8]) {
     *reinterpret_cast<uint4*>(p) = make_uint4(tc::pack_bf16(x[0], x[1]), tc::pack_bf16(x[2], x[3]),
                                               tc::pack_bf16(x[4], x[5]), tc::pack_bf16(x[6], x[7]));
@@ -79,11 +98,19 @@ __global__ void k_prep(const __nv_bfloat16* __restrict__ P, int ldP, const __nv_
 
 // ---- forward output: Z = LN_h(O) * ln_w + ln_b, times Swish(r_pre + b_r); saves mean, rstd per (row, head) -----
 // One warp per (row, head): lane l owns the 8-element chunks l, l + 32, ... of the head's V values.
-template <int NCH>   // chunks of 8 per lane: V = 256 * NCH
+// SP: the per-column parameters (b_r, ln_w, ln_b: 3 H V floats) are staged once per CTA in shared memory (their
+// global loads sat on every item's critical path).
+template <int NCH, bool SP>   // chunks of 8 per lane: V = 256 * NCH
 __global__ void k_out(const __nv_bfloat16* __restrict__ O, const __nv_bfloat16* __restrict__ P, int ldP, int r_off,
                       const float* __restrict__ b_r, const float* __restrict__ ln_w, const float* __restrict__ ln_b,
                       __nv_bfloat16* __restrict__ Z, float* __restrict__ mean_out, float* __restrict__ rstd_out,
                       int B, int T, int H, int V, float eps) {
+    extern __shared__ float4 sparam4[];
+    float* sparam = reinterpret_cast<float*>(sparam4);
+    if (SP) {
+        stage_params(sparam, b_r, ln_w, ln_b, H * V);
+        b_r = sparam; ln_w = sparam + H * V; ln_b = sparam + 2 * H * V;
+    }
     const int lane = threadIdx.x & 31;
     const int nw = B * T * H;   // (row, head) items; B*T*H < 2^31 (checked by the caller's shapes)
     for (int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); w < nw; w += (int)((gridDim.x * blockDim.x) >> 5)) {
@@ -115,9 +142,9 @@ __global__ void k_out(const __nv_bfloat16* __restrict__ O, const __nv_bfloat16* 
         for (int c = 0; c < NCH; ++c) {
             const int e = 8 * (lane + 32 * c), col = h * V + e;
             float z[8], br[8], lw[8], lb[8];
-            ldf8(b_r + col, br);
-            ldf8(ln_w + col, lw);
-            ldf8(ln_b + col, lb);
+            ldp8<SP>(b_r + col, br);
+            ldp8<SP>(ln_w + col, lw);
+            ldp8<SP>(ln_b + col, lb);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const float r = rp[c][j] + br[j];
@@ -130,7 +157,7 @@ __global__ void k_out(const __nv_bfloat16* __restrict__ O, const __nv_bfloat16* 
 
 // ---- backward of the output: dZ -> dO [B,H,T,V] (bf16), d r_pre into dP's r block (bf16), parameter partials ---
 // part[3][gridDim.x][H*V]: d ln_w, d ln_b, d b_r, accumulated over this CTA's rows in a fixed order.
-template <int NCH>
+template <int NCH, bool SP>
 __global__ void k_out_bwd(const __nv_bfloat16* __restrict__ dZ, const __nv_bfloat16* __restrict__ O,
                           const __nv_bfloat16* __restrict__ P, int ldP, int r_off, const float* __restrict__ b_r,
                           const float* __restrict__ ln_w, const float* __restrict__ ln_b,
@@ -139,6 +166,12 @@ __global__ void k_out_bwd(const __nv_bfloat16* __restrict__ dZ, const __nv_bfloa
                           int B, int T, int H, int V, int rows_per_cta) {
     // blockDim = 32 * H: warp h handles head h of each of this CTA's rows, the next row's loads in flight while
     // the current row is computed (the kernel is latency-bound otherwise: one row of loads per warp at a time).
+    extern __shared__ float4 sparam4[];
+    float* sparam = reinterpret_cast<float*>(sparam4);
+    if (SP) {   // per-column parameters staged once per CTA (see k_out)
+        stage_params(sparam, b_r, ln_w, ln_b, H * V);
+        b_r = sparam; ln_w = sparam + H * V; ln_b = sparam + 2 * H * V;
+    }
     const int lane = threadIdx.x & 31, h = threadIdx.x >> 5;
     const size_t nrows = (size_t)B * T, HV = (size_t)H * V;
     float aw[NCH][8] = {}, ab[NCH][8] = {}, ar[NCH][8] = {};
@@ -173,9 +206,9 @@ __global__ void k_out_bwd(const __nv_bfloat16* __restrict__ dZ, const __nv_bfloa
             const uint32_t xw[4] = {Xc[c].x, Xc[c].y, Xc[c].z, Xc[c].w}, rw[4] = {Rc[c].x, Rc[c].y, Rc[c].z, Rc[c].w},
                            dw[4] = {Dc[c].x, Dc[c].y, Dc[c].z, Dc[c].w};
             float drp[8], br[8], lw[8], lb[8];
-            ldf8(b_r + col, br);
-            ldf8(ln_w + col, lw);
-            ldf8(ln_b + col, lb);
+            ldp8<SP>(b_r + col, br);
+            ldp8<SP>(ln_w + col, lw);
+            ldp8<SP>(ln_b + col, lb);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const float xj = (j & 1) ? tc::bf16hi(xw[j >> 1]) : tc::bf16lo(xw[j >> 1]);
@@ -347,8 +380,13 @@ int gla_layer_out(int B, int T, int H, int V, const void* O, const void* P, int 
     const size_t warps = (size_t)B * T * H;
     cudaStream_t st = (cudaStream_t)stream;
     GLA_PROF("layer::out", st);
-    const int grid = grid_for(warps * 32, 256);
-#define GLA_OUT(N) gla::layer::k_out<N><<<grid, 256, 0, st>>>((const __nv_bfloat16*)O, (const __nv_bfloat16*)P, ldP, \
+    // parameters in shared memory when they fit the default 48 KB (then a persistent grid of 4 CTAs per SM, so
+    // the per-CTA staging stays small against the data)
+    const size_t spb = (size_t)3 * H * V * sizeof(float);
+    const bool sp = spb <= 48 * 1024;
+    const int grid0 = grid_for(warps * 32, 256), grid = sp && grid0 > 148 * 4 ? 148 * 4 : grid0;
+#define GLA_OUT(N) (sp ? gla::layer::k_out<N, true> : gla::layer::k_out<N, false>)<<<grid, 256, sp ? spb : 0, st>>>( \
+        (const __nv_bfloat16*)O, (const __nv_bfloat16*)P, ldP, \
         r_off, b_r, ln_w, ln_b, (__nv_bfloat16*)Z, mean, rstd, B, T, H, V, eps)
     switch (V / 256) {
         case 1: GLA_OUT(1); break;
@@ -393,7 +431,9 @@ int gla_layer_out_bwd(int B, int T, int H, int V, const void* dZ, const void* O,
     float* part = (float*)workspace;
     {
         GLA_PROF("layer::out_bwd", st);
-#define GLA_OUTB(N) gla::layer::k_out_bwd<N><<<nblk, 32 * H, 0, st>>>((const __nv_bfloat16*)dZ, \
+        const size_t spb = (size_t)3 * H * V * sizeof(float);
+        const bool sp = spb <= 48 * 1024;
+#define GLA_OUTB(N) (sp ? gla::layer::k_out_bwd<N, true> : gla::layer::k_out_bwd<N, false>)<<<nblk, 32 * H, sp ? spb : 0, st>>>((const __nv_bfloat16*)dZ, \
         (const __nv_bfloat16*)O, (const __nv_bfloat16*)P, ldP, r_off, b_r, ln_w, ln_b, mean, rstd, \
         (__nv_bfloat16*)dO, (__nv_bfloat16*)dP, part, B, T, H, V, rpc)
         switch (V / 256) {
