@@ -40,6 +40,9 @@ constexpr float GUARD = 60.f;
 #ifndef GLA_FWD_OB2
 #define GLA_FWD_OB2 1
 #endif
+#ifndef GLA_PREP_PFD
+#define GLA_PREP_PFD 1   // L2 prefetch distance of the prep, in items per CTA (measured: 1 86 us, 2 90.5, 3-4 106)
+#endif
 #ifndef GLA_PREP_PF
 #define GLA_PREP_PF 1
 #endif
@@ -260,7 +263,8 @@ k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         for (uint32_t o = 0; o < GB; o += PIECE)
             prefetch_l2_bulk(reinterpret_cast<const uint8_t*>(g + r0 * K) + o, PIECE < GB - o ? PIECE : GB - o);
     };
-    if (tid == 32) prefetch_item(item + gridDim.x);
+    if (tid == 32)
+        for (int d = 1; d < GLA_PREP_PFD; ++d) prefetch_item(item + d * gridDim.x);
     if (item < nitems)
         load_chunk<K, TG, true, true>(R, q, k, g, (size_t)(item / NC) * T + (size_t)(item % NC) * CH, row0, ch0);
     tc_fence_before();
@@ -272,7 +276,7 @@ k_fwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         const int chunk = item % NC, bh = item / NC;
         const size_t crow = (size_t)bh * T + (size_t)chunk * CH;
         if (tid == 0) tma_store_wait_read();    // the previous item's Q~ / K~ / P stores have read their smem
-        if (tid == 32 && GLA_PREP_PF) prefetch_item(item + 2 * gridDim.x);
+        if (tid == 32 && GLA_PREP_PF) prefetch_item(item + GLA_PREP_PFD * gridDim.x);
         float2 off[4], rr[4], Gm[4];
         chunk_cumsum<K>(R, gtot, rg, ch0, off, rr, Gm);   // (its barrier also orders the wait above)
         bool bad = false;
