@@ -573,6 +573,9 @@ k_bwd_prep(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
 #ifndef GLA_ANCH_PF
 #define GLA_ANCH_PF 1
 #endif
+#ifndef GLA_DP_GRID
+#define GLA_DP_GRID 2   // bwd_dp CTAs per SM (persistent)
+#endif
 #ifndef GLA_DP_NSTG
 #define GLA_DP_NSTG 4
 #endif
@@ -1398,7 +1401,7 @@ static cudaError_t launch_bwd2(const BwdProblem& p, cudaStream_t st) {
         const int smem = DP_NSTG * 16384 + 8192 + 1024;
         if ((e = cudaFuncSetAttribute(k_bwd_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess)
             return e;
-        const int grid_dp = nitems < 2 * num_sms() ? nitems : 2 * num_sms();
+        const int grid_dp = nitems < GLA_DP_GRID * num_sms() ? nitems : GLA_DP_GRID * num_sms();
         k_bwd_dp<<<(unsigned)grid_dp, 192, smem, st>>>(mDP, mV, mD, kw ? nullptr : fflags, flag, p.T, p.V, NC,
                                                         nitems);
     } else {
