@@ -590,7 +590,10 @@ def report(args, cfg, W, world, ms_step, value, prof, launches, clk, e2e, chain,
         line["device_sharing"] = f"{world} ranks on {torch.cuda.device_count()} GPU(s): timing valid per rank, " \
                                  "not a scaling number"
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = {k_: v_ for k_, v_ in cpu_oracle_sample(cfg, T_sample=min(cfg[2], 2048)).items()
+        # ~10 s of oracle work on the host cores (5 slices per core): the contract's bounded 10-30 s sample
+        n_cpu = 5 * min(host_cores(), 32)
+        line["cpu_baseline"] = {k_: v_ for k_, v_ in cpu_oracle_sample(cfg, n_slices=n_cpu,
+                                                                        T_sample=min(cfg[2], 2048)).items()
                                 if k_ != "seconds"}
     return line
 
